@@ -1,0 +1,673 @@
+// powersort.cu -- host orchestration + C ABI (include/powersort_b200.h).
+//
+// ps_sort = stable_sort_with (policy.py:201-262) as a stream of kernels:
+//   N1 pass 1  rd_types -> suffix-min(F) -> rd_tables -> chain scan -> rd_emit
+//   N2         powers -> min tree -> nearest<= -> classify (x2) -> spine
+//              -> depth / stack scans -> node finalize -> chunk plan
+//   N1 pass 2  form_leaves (into buffer depth&1)
+//   N3/N4      per stage (power levels high..low, then merge_down nodes):
+//              partition (big nodes) + merge_chunks
+// Two host synchronisations read the run count and the tree summary.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/powersort_b200.h"
+#include "ps_common.cuh"
+#include "ps_form.cuh"
+#include "ps_merge.cuh"
+#include "ps_runs.cuh"
+#include "ps_scan.cuh"
+#include "ps_tree.cuh"
+
+using namespace ps;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define PS_CUDA(call)                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(PS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                                      __FILE__ + ":" + std::to_string(__LINE__));                  \
+    } while (0)
+
+constexpr uint64_t WS_MAGIC = 0x5053423230304b31ull;  // "PSB200K1"
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Workspace header (device memory at offset 0; copied to host by ps_result_*).
+struct WsHeader {
+    uint64_t magic;
+    int64_t n;
+    int64_t m;
+    int32_t k, dtype;
+    uint32_t r;
+    uint32_t nmain, nspine_nodes;
+    uint32_t pad;
+    uint64_t off_sum, off_b, off_nat, off_nodes;
+};
+
+struct Layout {
+    uint64_t n, m, kb, rmax, ngroups, ntiles, chunks_max, scan_tmp;
+    uint32_t nlev;
+    uint64_t lev_size[8];
+    uint64_t tab_levels;  // number of chain-scan levels
+    uint64_t lvlP[16];
+    // offsets
+    uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
+        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, chunk2node, cuts,
+        scantmp_u32, scantmp_i32, total;
+};
+
+Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint64_t rmax_override = 0) {
+    Layout L;
+    memset(&L, 0, sizeof(L));
+    L.n = n;
+    L.m = m;
+    L.kb = kb;
+    uint64_t rmax = rmax_override ? rmax_override : std::min<uint64_t>(n, cdiv(n, std::max<uint64_t>(m, 1)));
+    L.rmax = rmax + 2;
+    L.ngroups = std::max<uint64_t>(1, cdiv(n, GROUP));
+    L.ntiles = L.ngroups * TILES_PER_GROUP;
+    // total chunks <= nodes + merge_cost / (CHUNK_CAP / MAX_WAY); merge_cost <= 64 n
+    L.chunks_max = L.rmax + cdiv(64 * n, CHUNK_CAP / MAX_WAY) + 16;
+    // min tree levels over P (size rmax + 1)
+    uint64_t s = align_up(L.rmax + 1, 32);
+    L.nlev = 0;
+    for (;;) {
+        L.lev_size[L.nlev++] = s;
+        if (s <= 32 || L.nlev == 8) break;
+        s = align_up(cdiv(s, 32), 32);
+    }
+    // chain-scan levels
+    uint64_t P = L.ngroups;
+    L.tab_levels = 0;
+    for (;;) {
+        L.lvlP[L.tab_levels++] = P;
+        if (P <= TSCAN_FAN) break;
+        P = cdiv(P, TSCAN_FAN);
+    }
+    uint64_t big = std::max<uint64_t>({L.rmax + 2, L.ngroups + 2, (uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2,
+                                       L.rmax});
+    L.scan_tmp = scan_tmp_elems(big);
+
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t o = off;
+        off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
+        return o;
+    };
+    const uint64_t M1 = std::min<uint64_t>(m, MAX_M_TILED) + 1;
+    L.header = take(sizeof(WsHeader));
+    L.sum = take(sizeof(Summary));
+    if (sort_buffers) {
+        L.k1 = take(n * kb);
+        L.v1 = take(n * 4);
+        L.ty = take((L.ngroups * GROUP_WORDS + 64) * 4);
+        L.cg = take((L.ngroups + 1) * 4);
+        L.Fg = take((L.ngroups + 1) * 4);
+        L.Ft = take((L.ntiles + 1) * 4);
+        if (m <= MAX_M_TILED) {
+            L.tile_tab = take(L.ntiles * M1 * 8);
+            for (uint64_t l = 0; l < L.tab_levels; ++l) {
+                L.lvl_tab[l] = take(L.lvlP[l] * M1 * 8);
+                L.lvl_ent[l] = take((L.lvlP[l] + 1) * 8);
+            }
+        }
+        L.nat = take(L.rmax * 4);
+        L.leafpar = take(L.rmax);
+        L.cuts = take(L.chunks_max * 16);
+    }
+    L.b = take((L.rmax + 2) * 4);
+    for (uint32_t l = 0; l < L.nlev; ++l) L.minlev[l] = take(L.lev_size[l] + 32);
+    L.P = L.minlev[0];
+    L.Rle = take(L.rmax * 4);
+    L.Lle = take(L.rmax * 4);
+    L.Dd = take((L.rmax + 2) * 4);
+    L.Sd = take((L.rmax + 2) * 4);
+    L.hist = take(((uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2) * 4);
+    L.hist_off = take(((uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2) * 4);
+    L.hist_tot = take(16);
+    L.spine = take(MAX_SPINE * 4);
+    L.nodes = take((L.rmax + MAX_SPINE) * sizeof(Node));
+    L.nch = take((L.rmax + MAX_SPINE + 2) * 4);
+    L.chunk_base = take((L.rmax + MAX_SPINE + 2) * 4);
+    L.chunk2node = take(L.chunks_max * 4);
+    L.scantmp_u32 = take(L.scan_tmp * 4);
+    L.scantmp_i32 = take(L.scan_tmp * 4);
+    L.total = off;
+    return L;
+}
+
+// Host copy of the summary plus the per-stage chunk ranges.
+struct TreeInfo {
+    Summary s;
+    std::vector<uint32_t> node_chunk;  // chunk_base per node (+ total at end)
+};
+
+template <class T>
+T* at(uint8_t* ws, uint64_t off) {
+    return reinterpret_cast<T*>(ws + off);
+}
+
+inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)std::max<uint64_t>(1, cdiv(n, t)); }
+
+// Builds the merge tree of the run boundaries b[0..r] (device, already in
+// place) for an array of n elements.  Leaves leaf parities when leafpar != 0.
+int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int strict, int slack_mode,
+               uint8_t* leafpar, TreeInfo& info, cudaStream_t s) {
+    Summary* sum = at<Summary>(ws, L.sum);
+    uint32_t* err = &sum->err;
+    const uint32_t* b = at<uint32_t>(ws, L.b);
+    uint8_t* P = at<uint8_t>(ws, L.P);
+    const uint32_t log2k = k == 4 ? 2 : 1;
+    // T1 powers (array over 0..padded)
+    const uint32_t padded = (uint32_t)L.lev_size[0];
+    tree_powers_kernel<<<grid_for(padded, 256), 256, 0, s>>>(b, r, n, log2k, P, padded, err);
+    PS_CUDA(cudaGetLastError());
+    // T2 min tree
+    MinTree mt;
+    memset(&mt, 0, sizeof(mt));
+    mt.lev[0] = P;
+    uint32_t nlev = 1;
+    {
+        uint64_t size = align_up((uint64_t)r + 1, 32);
+        while (size > 32 && nlev < L.nlev) {
+            const uint64_t groups = size / 32;
+            const uint64_t outp = align_up(groups, 32);
+            uint8_t* out = at<uint8_t>(ws, L.minlev[nlev]);
+            tree_minlevel_kernel<<<grid_for(outp, 256), 256, 0, s>>>(mt.lev[nlev - 1], (uint32_t)groups, out,
+                                                                     (uint32_t)outp);
+            PS_CUDA(cudaGetLastError());
+            mt.lev[nlev++] = out;
+            size = outp;
+        }
+    }
+    mt.nlev = nlev;
+    uint32_t* Rle = at<uint32_t>(ws, L.Rle);
+    uint32_t* Lle = at<uint32_t>(ws, L.Lle);
+    tree_nearest_kernel<<<grid_for(r, 256), 256, 0, s>>>(mt, P, r, Rle, Lle);
+    PS_CUDA(cudaGetLastError());
+    // T3 classify
+    int32_t* Dd = at<int32_t>(ws, L.Dd);
+    int32_t* Sd = at<int32_t>(ws, L.Sd);
+    PS_CUDA(cudaMemsetAsync(Dd, 0, ((uint64_t)r + 2) * 4, s));
+    PS_CUDA(cudaMemsetAsync(Sd, 0, ((uint64_t)r + 2) * 4, s));
+    const uint32_t nblocks = (uint32_t)std::max<uint64_t>(1, cdiv(r > 1 ? r - 1 : 1, CLS_THREADS));
+    uint32_t* hist = at<uint32_t>(ws, L.hist);
+    uint32_t* hoff = at<uint32_t>(ws, L.hist_off);
+    uint32_t* htot = at<uint32_t>(ws, L.hist_tot);
+    uint32_t* spine = at<uint32_t>(ws, L.spine);
+    Node* nodes = at<Node>(ws, L.nodes);
+    tree_classify_kernel<0><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
+                                                            spine, nodes, sum);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist, hoff, (int64_t)NPOW * nblocks, false, true,
+                                                   at<uint32_t>(ws, L.scantmp_u32), htot, s)));
+    tree_level_offsets_kernel<<<1, 128, 0, s>>>(hoff, htot, nblocks, sum);
+    PS_CUDA(cudaGetLastError());
+    tree_classify_kernel<1><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
+                                                            spine, nodes, sum);
+    PS_CUDA(cudaGetLastError());
+    tree_spine_kernel<<<1, 1, 0, s>>>(b, r, k, strict, spine, nodes, Dd, sum);
+    PS_CUDA(cudaGetLastError());
+    // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
+    PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Dd, Dd, (int64_t)r + 1, false, false,
+                                                 at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
+    PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Sd, Sd, (int64_t)r + 1, false, false,
+                                                 at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
+    // Need node count for finalize: read the summary (sync #2a)
+    PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
+    const int64_t cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
+    tree_stack_max_kernel<<<grid_for(r, 256), 256, 0, s>>>(Sd, r, sum, (uint32_t)cap);
+    PS_CUDA(cudaGetLastError());
+    if (leafpar) {
+        tree_leaf_parity_kernel<<<grid_for(r, 256), 256, 0, s>>>(Dd, r, leafpar);
+        PS_CUDA(cudaGetLastError());
+    }
+    if (nnodes) {
+        tree_nodes_finalize_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, Dd, slack_mode, sum);
+        PS_CUDA(cudaGetLastError());
+        uint32_t* nch = at<uint32_t>(ws, L.nch);
+        uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
+        tree_nchunks_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, nch);
+        PS_CUDA(cudaGetLastError());
+        PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nnodes, false, true,
+                                                       at<uint32_t>(ws, L.scantmp_u32), cb + nnodes, s)));
+        tree_copy_chunk_base_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, cb, nnodes);
+        PS_CUDA(cudaGetLastError());
+        info.node_chunk.resize(nnodes + 1);
+        PS_CUDA(cudaMemcpyAsync(info.node_chunk.data(), cb, (nnodes + 1) * 4, cudaMemcpyDeviceToHost, s));
+    }
+    PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    if (nnodes) {
+        const uint32_t total = info.node_chunk[nnodes];
+        if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
+        tree_chunk_map_kernel<<<grid_for(total, 256), 256, 0, s>>>(nodes, nnodes, total,
+                                                                   at<uint32_t>(ws, L.chunk2node));
+        PS_CUDA(cudaGetLastError());
+    }
+    if (info.s.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
+    if (info.s.err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(info.s.err) + ")");
+    return PS_OK;
+}
+
+int write_header(uint8_t* ws, const Layout& L, int64_t n, int64_t m, int k, int dtype, uint32_t r, uint32_t nmain,
+                 uint32_t nspine, cudaStream_t s) {
+    WsHeader h;
+    memset(&h, 0, sizeof(h));
+    h.magic = WS_MAGIC;
+    h.n = n;
+    h.m = m;
+    h.k = k;
+    h.dtype = dtype;
+    h.r = r;
+    h.nmain = nmain;
+    h.nspine_nodes = nspine;
+    h.off_sum = L.sum;
+    h.off_b = L.b;
+    h.off_nat = L.nat;
+    h.off_nodes = L.nodes;
+    PS_CUDA(cudaMemcpyAsync(ws + L.header, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    return PS_OK;
+}
+
+int validate_cfg(const ps_config* cfg) {
+    if (!cfg) return fail(PS_EINVAL, "config is NULL");
+    if (cfg->k != 2 && cfg->k != 4) return fail(PS_EINVAL, "k must be 2 or 4, got " + std::to_string(cfg->k));
+    int vk;
+    switch (cfg->variant) {
+        case PS_VARIANT_2WAY:
+        case PS_VARIANT_2WAY_COPY_SMALLER:
+        case PS_VARIANT_2WAY_NOSENTINEL:
+            vk = 2;
+            break;
+        case PS_VARIANT_4WAY:
+        case PS_VARIANT_4WAY_NOSENTINEL:
+            vk = 4;
+            break;
+        default:
+            return fail(PS_EINVAL, "unknown merge variant " + std::to_string(cfg->variant));
+    }
+    if (vk != cfg->k)
+        return fail(PS_EINVAL, "variant implements k=" + std::to_string(vk) + ", but config asks for k=" +
+                                   std::to_string(cfg->k));
+    if (cfg->min_run_len < 1) return fail(PS_EINVAL, "min_run_len must be >= 1");
+    if (cfg->min_run_len > (int64_t)MAX_FORM_M && cfg->min_run_len < (int64_t)1 << 40) {
+        // windows longer than MAX_FORM_M are not staged yet
+    }
+    return PS_OK;
+}
+
+int slack_mode_of(int variant) {
+    switch (variant) {
+        case PS_VARIANT_4WAY:
+        case PS_VARIANT_2WAY:
+            return 0;  // sentinel kernels: +arity writes per merge
+        case PS_VARIANT_4WAY_NOSENTINEL:
+            return 1;  // 2-way no-sentinel +0, stages +1
+        default:
+            return 2;
+    }
+}
+
+template <class K>
+int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t* ws, size_t wsb, ps_stats* st,
+              cudaStream_t s) {
+    const uint64_t m = (uint64_t)cfg.min_run_len;
+    const Layout L = make_layout((uint64_t)n, sizeof(K), m, true);
+    if (wsb < L.total)
+        return fail(PS_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
+    if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M)
+        return fail(PS_EINVAL, "min_run_len > " + std::to_string(MAX_FORM_M) + " is not supported on device yet");
+    const bool argsort = cfg.values_mode == PS_VALUES_ARGSORT;
+    Summary* sum = at<Summary>(ws, L.sum);
+    PS_CUDA(cudaMemsetAsync(sum, 0, sizeof(Summary), s));
+    uint32_t* err = &sum->err;
+    uint32_t* ty = at<uint32_t>(ws, L.ty);
+    uint32_t* cg = at<uint32_t>(ws, L.cg);
+    uint32_t* Fg = at<uint32_t>(ws, L.Fg);
+    uint32_t* Ft = at<uint32_t>(ws, L.Ft);
+    uint32_t* b = at<uint32_t>(ws, L.b);
+    uint32_t* nat = at<uint32_t>(ws, L.nat);
+    const uint32_t ngroups = (uint32_t)L.ngroups;
+
+    // ---- N1 pass 1: run detection ------------------------------------------
+    rd_types_kernel<K><<<ngroups, 256, 0, s>>>(keys, (uint64_t)n, ty, cg);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA((device_scan<uint32_t, OpMin<uint32_t>>(cg, Fg, ngroups, true, false, at<uint32_t>(ws, L.scantmp_u32),
+                                                   nullptr, s)));
+    if (m <= MAX_M_TILED) {
+        const uint32_t M1 = (uint32_t)m + 1;
+        uint64_t* tile_tab = at<uint64_t>(ws, L.tile_tab);
+        uint64_t* gtab = at<uint64_t>(ws, L.lvl_tab[0]);
+        const size_t smem = (size_t)TILES_PER_GROUP * M1 * 8;
+        rd_tables_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
+                                                   err);
+        PS_CUDA(cudaGetLastError());
+        uint64_t span = GROUP;
+        std::vector<uint64_t> spans(L.tab_levels);
+        for (uint64_t l = 0; l < L.tab_levels; ++l) {
+            spans[l] = span;
+            if (l + 1 < L.tab_levels) {
+                rd_compose_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
+                    at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
+                    at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
+                PS_CUDA(cudaGetLastError());
+                span *= TSCAN_FAN;
+            }
+        }
+        const uint64_t top = L.tab_levels - 1;
+        rd_top_kernel<<<1, 32, 0, s>>>(at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
+                                       (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
+        PS_CUDA(cudaGetLastError());
+        for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
+            rd_down_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
+                at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
+                at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
+            PS_CUDA(cudaGetLastError());
+        }
+        rd_emit_kernel<<<ngroups, 256, 0, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
+                                               at<uint64_t>(ws, L.lvl_ent[0]), b, nat, err);
+        PS_CUDA(cudaGetLastError());
+    } else {
+        rd_serial_kernel<<<1, 32, 0, s>>>(ty, (uint64_t)n, m, b, nat, sum);
+        PS_CUDA(cudaGetLastError());
+    }
+    Summary h;
+    PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    if (h.err) return fail(PS_EINVARIANT, "run detection invariant violated (flags " + std::to_string(h.err) + ")");
+    const uint32_t r = h.r;
+    if (r < 1 || r + 2 > L.rmax) return fail(PS_EINVARIANT, "run count out of range: " + std::to_string(r));
+
+    // ---- N2: merge tree --------------------------------------------------------
+    uint8_t* leafpar = at<uint8_t>(ws, L.leafpar);
+    TreeInfo info;
+    memset(&info.s, 0, sizeof(info.s));
+    uint32_t nnodes = 0;
+    if (r >= 2) {
+        int rc = build_tree(ws, L, r, (uint64_t)n, cfg.k, cfg.strict_merge_down, slack_mode_of(cfg.variant), leafpar,
+                            info, s);
+        if (rc) return rc;
+        nnodes = info.s.nmain + info.s.nspine_nodes;
+    } else {
+        PS_CUDA(cudaMemsetAsync(leafpar, 0, 1, s));
+    }
+
+    // ---- N1 pass 2: leaves -----------------------------------------------------
+    Bufs<K> bufs;
+    bufs.k[0] = keys;
+    bufs.v[0] = values;
+    bufs.k[1] = at<K>(ws, L.k1);
+    bufs.v[1] = at<int32_t>(ws, L.v1);
+    {
+        const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M));
+        const unsigned grid = grid_for((uint64_t)n, FORM_TILE);
+        if (argsort) {
+            PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            form_leaves_kernel<K, true><<<grid, FORM_THREADS, smem, s>>>(bufs, (uint64_t)n, b, nat, leafpar, r, ty,
+                                                                         (uint32_t)m);
+        } else {
+            PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            form_leaves_kernel<K, false><<<grid, FORM_THREADS, smem, s>>>(bufs, (uint64_t)n, b, nat, leafpar, r, ty,
+                                                                          (uint32_t)m);
+        }
+        PS_CUDA(cudaGetLastError());
+    }
+
+    // ---- N3/N4: merges, stage by stage ------------------------------------------
+    if (nnodes) {
+        const Node* nodes = at<Node>(ws, L.nodes);
+        const uint32_t* c2n = at<uint32_t>(ws, L.chunk2node);
+        uint4* cuts = at<uint4>(ws, L.cuts);
+        const size_t msmem = merge_smem_bytes<K>();
+        PS_CUDA(cudaFuncSetAttribute(merge_chunks_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+        auto run_stage = [&](uint32_t nlo, uint32_t nhi) -> int {
+            if (nhi <= nlo) return PS_OK;
+            const uint32_t c0 = info.node_chunk[nlo], c1 = info.node_chunk[nhi];
+            if (c1 - c0 > nhi - nlo) {
+                merge_partition_kernel<K><<<grid_for(c1 - c0, 128), 128, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
+                PS_CUDA(cudaGetLastError());
+            }
+            merge_chunks_kernel<K><<<c1 - c0, MERGE_THREADS, msmem, s>>>(bufs, nodes, c2n, cuts, c0, err);
+            PS_CUDA(cudaGetLastError());
+            return PS_OK;
+        };
+        for (int p = (int)NPOW - 1; p >= 1; --p) {
+            int rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1]);
+            if (rc) return rc;
+        }
+        for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
+            int rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1);
+            if (rc) return rc;
+        }
+    }
+    PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    if (h.err) return fail(PS_EINVARIANT, "merge invariant violated (flags " + std::to_string(h.err) + ")");
+    int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
+    if (rc) return rc;
+
+    // ---- N5: SortStats (statskit.py:75-98) ----------------------------------------
+    memset(st, 0, sizeof(*st));
+    const int64_t M = (int64_t)h.merge_cost;
+    st->merge_cost = M;
+    st->merges2 = (int64_t)h.merges[2];
+    st->merges3 = (int64_t)h.merges[3];
+    st->merges4 = (int64_t)h.merges[4];
+    st->runs_detected = r;
+    st->max_stack_height = h.max_stack;
+    st->buffer_cost = M;
+    st->scan_reads = n + 2 * M;
+    st->scan_writes = n + 2 * M + (int64_t)h.scan_slack;
+    st->comparisons = -1;
+    st->moves = -1;
+    st->comparisons_valid = 0;
+    st->moves_valid = 0;
+    return PS_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* ps_last_error(void) { return g_last_error.c_str(); }
+
+const char* ps_version(void) { return "powersort-b200 0.1.0 (sm_100a)"; }
+
+size_t ps_workspace_size(int64_t n, int32_t dtype, const ps_config* cfg) {
+    if (n < 0 || !cfg || cfg->min_run_len < 1) return 0;
+    uint64_t kb = dtype == PS_INT32 || dtype == PS_FLOAT32 ? 4 : (dtype == PS_INT64 || dtype == PS_FLOAT64 ? 8 : 0);
+    if (!kb) return 0;
+    return (size_t)make_layout((uint64_t)n, kb, (uint64_t)cfg->min_run_len, true).total;
+}
+
+int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_config* cfg, void* workspace,
+            size_t workspace_bytes, ps_stats* stats, void* stream) {
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (n < 0) return fail(PS_EINVAL, "n must be >= 0");
+    if (n > ((int64_t)1 << 31)) return fail(PS_EINVAL, "n > 2^31 is not supported (int32 payload)");
+    if (!stats) return fail(PS_EINVAL, "stats is NULL");
+    memset(stats, 0, sizeof(*stats));
+    if (n == 0) return PS_OK;  // policy.py:207-209
+    if (!keys || !values || !workspace) return fail(PS_EINVAL, "NULL pointer argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)workspace;
+    switch (dtype) {
+        case PS_INT32:
+            return sort_impl<int32_t>((int32_t*)keys, values, n, *cfg, ws, workspace_bytes, stats, s);
+        case PS_INT64:
+            return sort_impl<int64_t>((int64_t*)keys, values, n, *cfg, ws, workspace_bytes, stats, s);
+        case PS_FLOAT32:
+            return sort_impl<float>((float*)keys, values, n, *cfg, ws, workspace_bytes, stats, s);
+        case PS_FLOAT64:
+            return sort_impl<double>((double*)keys, values, n, *cfg, ws, workspace_bytes, stats, s);
+        default:
+            return fail(PS_EINVAL, "unsupported dtype " + std::to_string(dtype));
+    }
+}
+
+static int read_header(const void* workspace, WsHeader& h) {
+    if (!workspace) return fail(PS_EINVAL, "workspace is NULL");
+    PS_CUDA(cudaMemcpy(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h.magic != WS_MAGIC) return fail(PS_EINVAL, "workspace holds no sort result");
+    return PS_OK;
+}
+
+int ps_result_counts(const void* workspace, int64_t* runs, int64_t* merges) {
+    WsHeader h;
+    int rc = read_header(workspace, h);
+    if (rc) return rc;
+    if (runs) *runs = h.r;
+    if (merges) *merges = (int64_t)h.nmain + h.nspine_nodes;
+    return PS_OK;
+}
+
+int ps_result_runs(const void* workspace, int64_t* run_lengths, int64_t* natural_run_lengths, int64_t cap) {
+    WsHeader h;
+    int rc = read_header(workspace, h);
+    if (rc) return rc;
+    if (cap < (int64_t)h.r) return fail(PS_EINVAL, "capacity below the run count");
+    const uint8_t* ws = (const uint8_t*)workspace;
+    std::vector<uint32_t> b(h.r + 1), nat(h.r);
+    PS_CUDA(cudaMemcpy(b.data(), ws + h.off_b, (h.r + 1) * 4, cudaMemcpyDeviceToHost));
+    if (natural_run_lengths && h.off_nat)
+        PS_CUDA(cudaMemcpy(nat.data(), ws + h.off_nat, h.r * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < h.r; ++i) {
+        if (run_lengths) run_lengths[i] = (int64_t)b[i + 1] - b[i];
+        if (natural_run_lengths) natural_run_lengths[i] = h.off_nat ? nat[i] : (int64_t)b[i + 1] - b[i];
+    }
+    return PS_OK;
+}
+
+int ps_result_trace(const void* workspace, int64_t* rows, int64_t cap) {
+    WsHeader h;
+    int rc = read_header(workspace, h);
+    if (rc) return rc;
+    const uint32_t nn = h.nmain + h.nspine_nodes;
+    if (cap < (int64_t)nn) return fail(PS_EINVAL, "capacity below the merge count");
+    std::vector<Node> nodes(nn);
+    if (nn)
+        PS_CUDA(cudaMemcpy(nodes.data(), (const uint8_t*)workspace + h.off_nodes, nn * sizeof(Node),
+                           cudaMemcpyDeviceToHost));
+    // main-loop merges execute when boundary R arrives, higher powers first
+    // (policy.py:250-259); then _merge_down in sequence (policy.py:146-175).
+    std::vector<uint32_t> idx(h.nmain);
+    for (uint32_t i = 0; i < h.nmain; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
+        const Node &x = nodes[a], &y = nodes[b];
+        const uint32_t ex = x.pos[x.arity], ey = y.pos[y.arity];
+        if (ex != ey) return ex < ey;
+        return x.power > y.power;
+    });
+    for (uint32_t i = 0; i < h.nspine_nodes; ++i) idx.push_back(h.nmain + i);
+    for (uint32_t i = 0; i < nn; ++i) {
+        const Node& x = nodes[idx[i]];
+        int64_t* row = rows + 7 * i;
+        row[0] = x.arity;
+        for (int j = 0; j < 5; ++j) row[1 + j] = -1;
+        for (int j = 0; j <= x.arity; ++j) row[1 + j] = x.pos[j];
+        row[6] = (int64_t)x.pos[x.arity] - x.pos[0];
+    }
+    return PS_OK;
+}
+
+size_t ps_profile_workspace_size(int64_t r, int64_t n) {
+    if (r < 1 || n < r) return 0;
+    return (size_t)make_layout((uint64_t)n, 4, 1, false, (uint64_t)r).total;
+}
+
+int ps_tree_from_profile(const int64_t* lengths, int64_t r, int32_t k, int32_t strict_merge_down, void* workspace,
+                         size_t workspace_bytes, int64_t* merge_cost, int64_t* max_stack_height, void* stream) {
+    if (k != 2 && k != 4) return fail(PS_EINVAL, "k must be 2 or 4, got " + std::to_string(k));
+    if (r < 1 || !lengths) return fail(PS_EINVAL, "a run profile has at least one run");
+    uint64_t n = 0;
+    std::vector<uint32_t> b(r + 1);
+    for (int64_t i = 0; i < r; ++i) {
+        if (lengths[i] < 1) return fail(PS_EINVAL, "run lengths must be positive");
+        b[i] = (uint32_t)n;
+        n += (uint64_t)lengths[i];
+        if (n > ((uint64_t)1 << 31)) return fail(PS_EINVAL, "profile longer than 2^31");
+    }
+    b[r] = (uint32_t)n;
+    const Layout L = make_layout(n, 4, 1, false, (uint64_t)r);
+    if (workspace_bytes < L.total) return fail(PS_ENOMEM, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)workspace;
+    PS_CUDA(cudaMemsetAsync(ws + L.sum, 0, sizeof(Summary), s));
+    PS_CUDA(cudaMemcpyAsync(ws + L.b, b.data(), (r + 1) * 4, cudaMemcpyHostToDevice, s));
+    TreeInfo info;
+    memset(&info.s, 0, sizeof(info.s));
+    if (r >= 2) {
+        int rc = build_tree(ws, L, (uint32_t)r, n, k, strict_merge_down, 0, nullptr, info, s);
+        if (rc) return rc;
+    }
+    int rc = write_header(ws, L, (int64_t)n, 1, k, 0, (uint32_t)r, info.s.nmain, info.s.nspine_nodes, s);
+    if (rc) return rc;
+    if (merge_cost) *merge_cost = (int64_t)info.s.merge_cost;
+    if (max_stack_height) *max_stack_height = info.s.max_stack;
+    return PS_OK;
+}
+
+int ps_node_power(int32_t k, int64_t n, int64_t b1, int64_t e1, int64_t b2, int64_t e2, int32_t any_k) {
+    // power.py:47-74, exact in 128-bit integers
+    if (!any_k && k != 2 && k != 3 && k != 4) return fail(-PS_EINVAL, "node_power supports k in {2, 3, 4}");
+    if (k < 2) return fail(-PS_EINVAL, "boundary power needs k >= 2");
+    if (!(0 <= b1 && b1 < e1 && e1 == b2 && b2 < e2 && e2 <= n)) return fail(-PS_EINVAL, "malformed run bounds");
+    const unsigned __int128 A = (unsigned __int128)(b1 + e1), B = (unsigned __int128)(b2 + e2);
+    const unsigned __int128 two_n = (unsigned __int128)2 * (unsigned __int128)n;
+    unsigned __int128 kp = (unsigned __int128)k;
+    int p = 1;
+    while ((A * kp) / two_n == (B * kp) / two_n) {
+        p++;
+        kp *= (unsigned __int128)k;
+    }
+    return p;
+}
+
+int64_t ps_run_stack_capacity(int64_t k, int64_t n) {
+    if (k < 2 || n < 1) return -PS_EINVAL;
+    int64_t m = 0;
+    unsigned __int128 p = 1;
+    while (p < (unsigned __int128)n) {
+        p *= (unsigned __int128)k;
+        m++;
+    }
+    return (k - 1) * (m + 1);
+}
+
+size_t ps_shard_merge_workspace_size(int32_t nshards, int64_t slab_n) {
+    (void)nshards;
+    (void)slab_n;
+    return 0;
+}
+
+int ps_shard_merge(int32_t, int32_t, const void* const*, const int32_t* const*, const int64_t*, int64_t, int64_t,
+                   void*, int32_t*, void*, size_t, void*) {
+    return fail(PS_EINVAL, "ps_shard_merge: not implemented yet");
+}
+
+}  // extern "C"

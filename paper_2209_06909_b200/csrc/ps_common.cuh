@@ -1,0 +1,98 @@
+// ps_common.cuh -- shared constants, types and device helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PS_DEV __device__ __forceinline__
+#define PS_FULL 0xFFFFFFFFu
+
+namespace ps {
+
+// ---- run detection geometry --------------------------------
+constexpr uint32_t TILE = 2048;                   // positions per chain tile (one warp)
+constexpr uint32_t TILES_PER_GROUP = 8;           // tiles per CTA
+constexpr uint32_t GROUP = TILE * TILES_PER_GROUP; // positions per CTA
+constexpr uint32_t GROUP_WORDS = GROUP / 32;      // type-bit words per CTA
+constexpr uint32_t MAX_M_TILED = 256;             // larger min_run_len -> serial chain walker
+constexpr uint32_t TSCAN_FAN = 32;                // tables composed per warp in the chain scan
+
+// ---- merge geometry ------------------------------------------------------
+constexpr uint32_t CHUNK_CAP = 4096;  // max records per merge chunk (k * cut spacing)
+constexpr uint32_t MERGE_THREADS = 256;
+constexpr uint32_t MERGE_VT = CHUNK_CAP / MERGE_THREADS;  // 16 records per thread
+constexpr uint32_t MAX_WAY = 4;
+
+constexpr uint32_t INF32 = 0xFFFFFFFFu;
+constexpr uint32_t MAX_SPINE = 256;
+constexpr uint32_t NPOW = 64;  // power buckets (powers are <= 33 for n <= 2^31)
+
+// Error flags raised on the device (bitmask in Summary.err).
+enum : uint32_t {
+    ERR_CHAIN = 1u,      // run-chain candidate lemma violated
+    ERR_GROUP = 2u,      // more than k-1 equal powers in a group (policy.py:139)
+    ERR_SPINE = 4u,      // spine larger than MAX_SPINE
+    ERR_STACK = 8u,      // run stack above run_stack_capacity (policy.py:117-120)
+    ERR_CUT = 16u,       // merge chunk larger than CHUNK_CAP
+    ERR_POWER = 32u,     // power outside 1..NPOW-1
+};
+
+// One merge of the tree.  pos[0..arity] are the run boundaries (positions):
+// children are [pos[a], pos[a+1]).
+struct Node {
+    uint32_t pos[5];
+    uint8_t arity;
+    uint8_t parity;   // output buffer (depth & 1)
+    uint8_t power;    // boundary power (0 for merge_down/spine nodes)
+    uint8_t flags;
+    uint32_t probe;   // a member boundary index (depth lookup)
+    uint32_t chunk_base;
+    uint32_t nchunks;
+    uint32_t order;   // reference execution order key helper
+};
+static_assert(sizeof(Node) == 40, "Node layout");
+
+// Device -> host summary, read once after the tree is built.
+struct Summary {
+    uint32_t r;              // runs
+    uint32_t err;            // ERR_* bitmask
+    uint32_t nmain;          // main-loop merge nodes
+    uint32_t nspine;         // spine boundaries
+    uint32_t nspine_nodes;   // merge_down nodes
+    uint32_t max_stack;      // max_stack_height
+    uint32_t total_chunks;
+    uint32_t pad0;
+    uint32_t level_off[NPOW + 1];  // node offsets per power bucket (ascending power)
+    unsigned long long merge_cost;
+    unsigned long long merges[5];      // by arity
+    unsigned long long scan_slack;     // sum of per-merge slack (variant-specific)
+    unsigned long long buffer_cost;
+};
+
+PS_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
+PS_DEV uint32_t warp_id() { return threadIdx.x >> 5; }
+
+PS_DEV uint64_t pack_xc(uint32_t x, uint32_t c) { return ((uint64_t)c << 32) | x; }
+PS_DEV uint32_t unpack_x(uint64_t v) { return (uint32_t)v; }
+PS_DEV uint32_t unpack_c(uint64_t v) { return (uint32_t)(v >> 32); }
+
+template <class T>
+PS_DEV T shfl(T v, int src) {
+    return __shfl_sync(PS_FULL, v, src);
+}
+template <class T>
+PS_DEV T shfl_up(T v, int d) {
+    return __shfl_up_sync(PS_FULL, v, d);
+}
+
+// Key comparisons: the reference's `le` is `key(a) <= key(b)` (statskit.py:68-72).
+template <class K>
+PS_DEV bool key_le(K a, K b) {
+    return a <= b;
+}
+template <class K>
+PS_DEV bool key_lt(K a, K b) {
+    return a < b;
+}
+
+}  // namespace ps

@@ -1,0 +1,203 @@
+// ps_form.cuh -- N1 pass 2: leaf-run formation.
+//
+// Every leaf run of the reference is, after find_first_run's reversal
+// (runs.py:41-47) and extend_run's insertion sort (runs.py:50-82), the stable
+// sort of the original elements of its window.  Natural runs are
+// copied (ascending) or reversed (strictly descending); extended windows
+// (natural length < run length <= min_run_len) are ranked by (key, position).
+// Each leaf is written straight into ping-pong buffer (leaf depth & 1), so
+// no merge ever copies back.  Buffer 0 is the caller's array:
+// parity-0 leaves are formed in place (reversals swap mirrored pairs owned by
+// one thread; windows are staged in shared memory before being written).
+#pragma once
+
+#include "ps_common.cuh"
+#include "ps_scan.cuh"
+
+namespace ps {
+
+constexpr uint32_t FORM_TILE = 2048;
+constexpr uint32_t FORM_THREADS = 256;
+constexpr uint32_t MAX_FORM_M = 1024;
+
+template <class K>
+struct Bufs {
+    K* k[2];
+    int32_t* v[2];
+};
+
+// shared layout: sb[FORM_TILE+2] u32, snat[FORM_TILE+1] u32, spar[FORM_TILE+1] u8,
+//   wlist[FORM_TILE+1] u32 (window leaf ids), woff[FORM_TILE+2] u32,
+//   wk[FORM_TILE+MAX_M] K, wv[...] i32
+template <class K>
+size_t form_smem_bytes(uint32_t m) {
+    size_t s = 0;
+    s += (FORM_TILE + 2) * 4;
+    s += (FORM_TILE + 1) * 4;
+    s += ((FORM_TILE + 1) + 15) / 16 * 16;
+    s += (FORM_TILE + 1) * 4;
+    s += (FORM_TILE + 2) * 4;
+    s = (s + 15) / 16 * 16;
+    const size_t cap = FORM_TILE + (m < MAX_FORM_M ? m : MAX_FORM_M);
+    s += cap * sizeof(K);
+    s += cap * 4;
+    return s;
+}
+
+template <class K, bool ARGSORT>
+__global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs, uint64_t n,
+                                                                   const uint32_t* __restrict__ b,
+                                                                   const uint32_t* __restrict__ nat,
+                                                                   const uint8_t* __restrict__ leafpar, uint32_t r,
+                                                                   const uint32_t* __restrict__ ty, uint32_t m) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* snat = sb + (FORM_TILE + 2);
+    uint8_t* spar = reinterpret_cast<uint8_t*>(snat + (FORM_TILE + 1));
+    uint32_t* wlist = reinterpret_cast<uint32_t*>(spar + ((FORM_TILE + 1) + 15) / 16 * 16);
+    uint32_t* woff = wlist + (FORM_TILE + 1);
+    size_t off = (reinterpret_cast<uint8_t*>(woff + (FORM_TILE + 2)) - smem + 15) / 16 * 16;
+    const uint32_t cap = FORM_TILE + (m < MAX_FORM_M ? m : MAX_FORM_M);
+    K* wk = reinterpret_cast<K*>(smem + off);
+    int32_t* wv = reinterpret_cast<int32_t*>(wk + cap);
+    __shared__ uint32_t s_first, s_cnt, s_nwin, s_wtot;
+    __shared__ uint32_t sw32[32];
+
+    K* const K0 = bufs.k[0];
+    int32_t* const V0 = bufs.v[0];
+    const uint64_t t0 = (uint64_t)blockIdx.x * FORM_TILE;
+    const uint64_t t1 = min(t0 + FORM_TILE, n);
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        // last leaf with b <= t0, last leaf with b <= t1-1
+        uint32_t lo = 0, hi = r;  // b[lo] <= t0 < b[hi]
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (b[mid] <= t0) lo = mid; else hi = mid;
+        }
+        uint32_t lo2 = lo, hi2 = r;
+        while (hi2 - lo2 > 1) {
+            uint32_t mid = (lo2 + hi2) >> 1;
+            if (b[mid] <= t1 - 1) lo2 = mid; else hi2 = mid;
+        }
+        s_first = lo;
+        s_cnt = lo2 - lo + 1;
+    }
+    __syncthreads();
+    const uint32_t first = s_first, cnt = s_cnt;
+    for (uint32_t i = tid; i <= cnt; i += FORM_THREADS) sb[i] = b[first + i];
+    for (uint32_t i = tid; i < cnt; i += FORM_THREADS) {
+        snat[i] = nat[first + i];
+        spar[i] = leafpar[first + i];
+    }
+    __syncthreads();
+
+    // ---- natural leaves: copy / mirrored swap ------------------------------
+    for (uint64_t pos = t0 + tid; pos < t1; pos += FORM_THREADS) {
+        uint32_t lo = 0, hi = cnt;  // sb[lo] <= pos < sb[hi]
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (sb[mid] <= pos) lo = mid; else hi = mid;
+        }
+        const uint64_t bj = sb[lo], ej = sb[lo + 1];
+        const uint32_t len = (uint32_t)(ej - bj);
+        if (snat[lo] < len) continue;  // extended window, below
+        const uint32_t par = spar[lo];
+        K* dk = bufs.k[par];
+        int32_t* dv = bufs.v[par];
+        bool desc = false;
+        if (len >= 2) {
+            const uint64_t q = bj + 1;
+            desc = !((ty[q >> 5] >> (q & 31)) & 1u);
+        }
+        if (!desc) {
+            if (par) {
+                dk[pos] = K0[pos];
+                dv[pos] = ARGSORT ? (int32_t)pos : V0[pos];
+            } else if (ARGSORT) {
+                V0[pos] = (int32_t)pos;
+            }
+        } else {
+            const uint64_t mirror = bj + ej - 1 - pos;
+            if (pos < mirror) {
+                const K ka = K0[pos], kb = K0[mirror];
+                const int32_t va = ARGSORT ? (int32_t)pos : V0[pos];
+                const int32_t vb = ARGSORT ? (int32_t)mirror : V0[mirror];
+                dk[pos] = kb;
+                dv[pos] = vb;
+                dk[mirror] = ka;
+                dv[mirror] = va;
+            } else if (pos == mirror) {
+                if (par) {
+                    dk[pos] = K0[pos];
+                    dv[pos] = ARGSORT ? (int32_t)pos : V0[pos];
+                } else if (ARGSORT) {
+                    V0[pos] = (int32_t)pos;
+                }
+            }
+        }
+    }
+
+    // ---- extended windows starting in this tile: stable rank ---------------
+    // compact the window leaf ids (block scan of flags, several rounds)
+    uint32_t nwin = 0;
+    for (uint32_t base = 0; base < cnt; base += FORM_THREADS) {
+        const uint32_t i = base + tid;
+        uint32_t flag = 0;
+        if (i < cnt) {
+            const uint32_t len = sb[i + 1] - sb[i];
+            flag = (snat[i] < len) && (sb[i] >= t0);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_exclusive<uint32_t, OpSum<uint32_t>>(flag, tot, sw32);
+        if (flag) wlist[nwin + ex] = i;
+        nwin += tot;
+    }
+    if (nwin == 0) return;
+    // element offsets of the windows
+    uint32_t wtot = 0;
+    for (uint32_t base = 0; base < nwin; base += FORM_THREADS) {
+        const uint32_t i = base + tid;
+        uint32_t len = 0;
+        if (i < nwin) len = sb[wlist[i] + 1] - sb[wlist[i]];
+        uint32_t tot;
+        const uint32_t ex = block_exclusive<uint32_t, OpSum<uint32_t>>(len, tot, sw32);
+        if (i < nwin) woff[i] = wtot + ex;
+        wtot += tot;
+    }
+    if (tid == 0) woff[nwin] = wtot;
+    __syncthreads();
+    // stage
+    for (uint32_t e = tid; e < wtot; e += FORM_THREADS) {
+        uint32_t lo = 0, hi = nwin;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (woff[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint64_t p = (uint64_t)sb[wlist[lo]] + (e - woff[lo]);
+        wk[e] = K0[p];
+        wv[e] = ARGSORT ? (int32_t)p : V0[p];
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < wtot; e += FORM_THREADS) {
+        uint32_t lo = 0, hi = nwin;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (woff[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint32_t wb = woff[lo], we = woff[lo + 1];
+        const K x = wk[e];
+        uint32_t rank = 0;
+        for (uint32_t f = wb; f < we; ++f) {
+            const K y = wk[f];
+            rank += (y < x) || (!(x < y) && f < e);
+        }
+        const uint32_t leaf = wlist[lo];
+        const uint32_t par = spar[leaf];
+        const uint64_t dst = (uint64_t)sb[leaf] + rank;
+        bufs.k[par][dst] = x;
+        bufs.v[par][dst] = wv[e];
+    }
+}
+
+}  // namespace ps

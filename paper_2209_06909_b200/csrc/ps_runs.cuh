@@ -1,0 +1,414 @@
+// ps_runs.cuh -- N1 pass 1: parallel run detection.
+//
+// The reference detects runs left to right (policy.py:241-248 next_run ->
+// runs.py:23-47 find_first_run, runs.py:71-82 extend_run): from position p
+// the natural run ends at E(p) (maximal weakly increasing or strictly
+// decreasing stretch starting with pair (p, p+1)) and the next run starts at
+//     next(p) = max(E(p), min(n, p + m)),   m = min_run_len.
+// This chain is inherently sequential; we make it parallel with SURVEY F6:
+//   * pair types t(q) = [a[q-1] <= a[q]] are packed into bit words (RD1), and
+//     E(p) = first "type change" position > p+1 (or n).
+//   * For a tile starting at t, the first chain node >= t lies in the
+//     candidate set C(t) = {t, ..., t+m-1} U {F(t)}, F(t) = first change > t.
+//   * Each tile therefore has an (m+1)-entry transfer table
+//     candidate -> (first chain node >= next tile start, #nodes in tile);
+//     tables compose associatively (function composition with pass-through),
+//     so the chain is a scan over tables (hierarchical, fan-out 32).
+//   * Once every tile knows its entry node, one lane re-walks the tile and
+//     emits the run boundaries b[] and natural lengths (policy.py:243,247).
+#pragma once
+
+#include "ps_common.cuh"
+
+namespace ps {
+
+// Bits j of the returned mask are set iff lo <= q0 + j < hi.
+PS_DEV uint32_t range_mask(uint64_t q0, uint64_t lo, uint64_t hi) {
+    if (q0 + 32 <= lo || q0 >= hi || lo >= hi) return 0u;
+    uint32_t m = PS_FULL;
+    if (q0 < lo) m &= PS_FULL << (uint32_t)(lo - q0);
+    if (q0 + 32 > hi) m &= PS_FULL >> (uint32_t)(q0 + 32 - hi);
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// RD1: type bits t(q) for q in the group, plus c_g = first change position in
+// (G, G+GROUP] (2 <= q <= n-1), INF if none.  One CTA per group; each warp
+// streams 1024 keys per round with coalesced loads, ballots give the words.
+template <class K>
+__global__ void __launch_bounds__(256) rd_types_kernel(const K* __restrict__ a, uint64_t n,
+                                                       uint32_t* __restrict__ ty, uint32_t* __restrict__ cg) {
+    __shared__ uint32_t sw[GROUP_WORDS];
+    __shared__ uint32_t smin[8];
+    const uint32_t g = blockIdx.x;
+    const uint64_t G = (uint64_t)g * GROUP;
+    const uint32_t lane = lane_id(), warp = warp_id();
+#pragma unroll 1
+    for (int round = 0; round < 2; ++round) {
+        const uint32_t wbase = warp * 64 + round * 32;
+        const uint64_t p0 = G + 32ull * wbase;
+        K carry = (p0 >= 1 && p0 - 1 < n) ? a[p0 - 1] : K(0);
+        uint32_t myword = 0;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+            const uint64_t p = p0 + 32ull * i + lane;
+            K x = (p < n) ? a[p] : K(0);
+            K xp = shfl_up(x, 1);
+            if (lane == 0) xp = carry;
+            bool bit = (p >= 1) && (p < n) && key_le(xp, x);
+            uint32_t word = __ballot_sync(PS_FULL, bit);
+            carry = shfl(x, 31);
+            if ((int)lane == i) myword = word;
+        }
+        sw[wbase + lane] = myword;
+    }
+    __syncthreads();
+    uint32_t best = INF32;
+    const uint64_t Gend = G + GROUP;
+    for (uint32_t w = threadIdx.x; w < GROUP_WORDS; w += blockDim.x) {
+        uint32_t cur = sw[w];
+        ty[(uint64_t)g * GROUP_WORDS + w] = cur;
+        uint32_t prevbit = w ? (sw[w - 1] >> 31) : 0u;
+        uint32_t chg = cur ^ ((cur << 1) | prevbit);
+        if (w == 0) chg &= ~1u;  // q = G is not in (G, Gend]
+        const uint64_t q0 = G + 32ull * w;
+        chg &= range_mask(q0, 2, n);
+        if (chg) best = min(best, (uint32_t)(q0 + __ffs(chg) - 1));
+    }
+    if (threadIdx.x == 0 && Gend >= 2 && Gend < n) {
+        // q = Gend: t(Gend) ^ t(Gend - 1)
+        uint32_t tend = key_le(a[Gend - 1], a[Gend]) ? 1u : 0u;
+        uint32_t tprev = sw[GROUP_WORDS - 1] >> 31;
+        if (tend != tprev) best = min(best, (uint32_t)Gend);
+    }
+    for (int d = 16; d; d >>= 1) best = min(best, __shfl_xor_sync(PS_FULL, best, d));
+    if (lane == 0) smin[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = INF32;
+        for (int i = 0; i < 8; ++i) m = min(m, smin[i]);
+        cg[g] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-CTA view of one group's change bits, with O(1) "next change" lookup.
+struct ChainView {
+    const uint32_t* chg;  // GROUP_WORDS + 1 words; bit j of word w = change at G + 32w + j
+    const uint16_t* nzn;  // nzn[w] = first w' >= w with chg[w'] != 0, else 0xFFFF (size GROUP_WORDS+2)
+    uint64_t G, Gend, n;
+    uint64_t Fnext;  // first change > Gend (or n)
+    uint64_t m;
+
+    // First change position >= y (y >= G + 1), or n.
+    PS_DEV uint64_t next_change_ge(uint64_t y) const {
+        if (y > Gend) return Fnext;
+        const uint32_t off = (uint32_t)(y - G);
+        const uint32_t w = off >> 5;
+        const uint32_t bits = chg[w] & (PS_FULL << (off & 31));
+        if (bits) return G + 32ull * w + (__ffs(bits) - 1);
+        const uint32_t w2 = nzn[w + 1];
+        if (w2 != 0xFFFFu) return G + 32ull * w2 + (__ffs(chg[w2]) - 1);
+        return Fnext;
+    }
+    // E(p): end of the natural run starting at p (runs.py:23-47).
+    PS_DEV uint64_t E(uint64_t p) const {
+        const uint64_t q = p + 1;
+        if (q >= n) return n;
+        uint64_t c = next_change_ge(q + 1);
+        return c < n ? c : n;
+    }
+    // next(p) = max(E(p), min(n, p+m))  (policy.py:241-248 with runs.py:71-82)
+    PS_DEV uint64_t next(uint64_t p, uint64_t* e_out = nullptr) const {
+        const uint64_t e = E(p);
+        if (e_out) *e_out = e;
+        uint64_t s = p + m;
+        if (s > n) s = n;
+        return e > s ? e : s;
+    }
+};
+
+// Build chg / nzn in shared memory for group g (all threads of the CTA).
+PS_DEV void build_chain_view(const uint32_t* __restrict__ ty, uint64_t n, uint32_t g, uint32_t ngroups,
+                             const uint32_t* __restrict__ Fg, uint32_t* s_chg, uint16_t* s_nzn, ChainView& cv,
+                             uint64_t m) {
+    const uint64_t G = (uint64_t)g * GROUP;
+    const uint64_t wg0 = (uint64_t)g * GROUP_WORDS;
+    const uint64_t nwords_total = (uint64_t)ngroups * GROUP_WORDS;
+    // chg words 0..GROUP_WORDS (inclusive; the last only for position Gend)
+    for (uint32_t w = threadIdx.x; w <= GROUP_WORDS; w += blockDim.x) {
+        const uint64_t gw = wg0 + w;
+        uint32_t cur = gw < nwords_total ? ty[gw] : 0u;
+        uint32_t prv = (gw >= 1 && gw - 1 < nwords_total) ? ty[gw - 1] : 0u;
+        uint32_t chg = cur ^ ((cur << 1) | (prv >> 31));
+        const uint64_t q0 = G + 32ull * w;
+        uint64_t hi = n;
+        if (w == GROUP_WORDS) hi = min(hi, q0 + 1);  // only position Gend
+        chg &= range_mask(q0, 2, hi);
+        if (w == 0) chg &= ~1u;
+        s_chg[w] = chg;
+    }
+    __syncthreads();
+    // nzn: suffix "first nonzero word" -- each thread owns 2 words of 0..511,
+    // word 512 handled by all (cheap), then a block suffix-min over threads.
+    __shared__ uint32_t s_red[32];
+    const uint32_t t = threadIdx.x;  // blockDim.x == 256
+    const uint32_t w0 = 2 * t, w1 = 2 * t + 1;
+    const uint32_t NONE = 0xFFFFu;
+    uint32_t v0 = s_chg[w0] ? w0 : NONE;
+    uint32_t v1 = s_chg[w1] ? w1 : NONE;
+    uint32_t vlast = s_chg[GROUP_WORDS] ? GROUP_WORDS : NONE;
+    uint32_t loc = min(v0, v1);
+    // exclusive suffix-min over threads t' > t
+    const uint32_t lane = lane_id(), warp = warp_id();
+    uint32_t x = loc;
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_down_sync(PS_FULL, x, d);
+        if (lane + d < 32) x = min(x, y);
+    }
+    // x = inclusive suffix-min within warp from this lane
+    if (lane == 0) s_red[warp] = x;
+    __syncthreads();
+    uint32_t after_warp = vlast;
+    for (uint32_t ww = warp + 1; ww < 8; ++ww) after_warp = min(after_warp, s_red[ww]);
+    uint32_t excl = __shfl_down_sync(PS_FULL, x, 1);
+    if (lane == 31) excl = NONE;
+    excl = min(excl, after_warp);
+    s_nzn[w1] = (uint16_t)min(v1, excl);
+    s_nzn[w0] = (uint16_t)min(v0, min(v1, excl));
+    if (t == 0) {
+        s_nzn[GROUP_WORDS] = (uint16_t)vlast;
+        s_nzn[GROUP_WORDS + 1] = (uint16_t)NONE;
+    }
+    __syncthreads();
+    cv.chg = s_chg;
+    cv.nzn = s_nzn;
+    cv.G = G;
+    cv.Gend = G + GROUP;
+    cv.n = n;
+    uint64_t fn = (g + 1 < ngroups) ? (uint64_t)Fg[g + 1] : (uint64_t)n;
+    cv.Fnext = fn < n ? fn : n;
+    cv.m = m;
+}
+
+// Candidate index of position x in the table of a span starting at t with
+// F(t) = Ft:  x - t if < m, else the F(t) slot m.
+PS_DEV void tab_apply(const uint64_t* tab, uint64_t t, uint64_t tnext, uint64_t Ft, uint64_t m, uint64_t n,
+                      uint64_t& x, uint64_t& c, uint32_t* err) {
+    if (x >= tnext || x >= n) return;  // pass-through
+    const uint64_t d = x - t;
+    uint32_t idx = d < m ? (uint32_t)d : (uint32_t)m;
+    if (idx == m && x != Ft) atomicOr(err, ERR_CHAIN);
+    const uint64_t v = tab[idx];
+    x = unpack_x(v);
+    c += unpack_c(v);
+}
+
+// ---------------------------------------------------------------------------
+// RD2a: per-tile transfer tables (one warp per tile, lanes over the m+1
+// candidates) and their composition into one table per group.
+// Dynamic smem: TILES_PER_GROUP * (m+1) uint64.
+__global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
+                                                        const uint32_t* __restrict__ Fg, uint32_t ngroups,
+                                                        uint64_t* __restrict__ tile_tab, uint32_t* __restrict__ Ft,
+                                                        uint64_t* __restrict__ group_tab, uint32_t* err) {
+    __shared__ uint32_t s_chg[GROUP_WORDS + 1];
+    __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
+    __shared__ uint64_t s_Ft[TILES_PER_GROUP];
+    extern __shared__ uint64_t s_tab[];  // [TILES_PER_GROUP][m+1]
+    const uint32_t g = blockIdx.x;
+    ChainView cv;
+    build_chain_view(ty, n, g, ngroups, Fg, s_chg, s_nzn, cv, m);
+    const uint32_t lane = lane_id(), w = warp_id();
+    const uint32_t M1 = m + 1;
+    const uint64_t t = cv.G + (uint64_t)w * TILE;
+    const uint64_t tend = t + TILE;
+    const uint64_t lim = tend < n ? tend : n;
+    uint64_t F_t = cv.next_change_ge(t + 1);
+    if (F_t > n) F_t = n;
+    if (lane == 0) s_Ft[w] = F_t;
+    for (uint32_t e = lane; e < M1; e += 32) {
+        uint64_t x = e < m ? t + e : F_t;
+        uint64_t cnt = 0;
+        while (x < lim) {
+            cnt++;
+            x = cv.next(x);
+        }
+        s_tab[w * M1 + e] = pack_xc((uint32_t)x, (uint32_t)cnt);
+    }
+    __syncthreads();
+    const uint64_t tile0 = (uint64_t)g * TILES_PER_GROUP;
+    for (uint32_t i = threadIdx.x; i < TILES_PER_GROUP * M1; i += blockDim.x)
+        tile_tab[tile0 * M1 + i] = s_tab[i];
+    if (threadIdx.x < TILES_PER_GROUP) Ft[tile0 + threadIdx.x] = (uint32_t)s_Ft[threadIdx.x];
+    if (w == 0) {
+        for (uint32_t e = lane; e < M1; e += 32) {
+            uint64_t x = e < m ? cv.G + e : s_Ft[0];
+            uint64_t c = 0;
+            for (uint32_t k = 0; k < TILES_PER_GROUP; ++k) {
+                const uint64_t tk = cv.G + (uint64_t)k * TILE;
+                tab_apply(s_tab + k * M1, tk, tk + TILE, s_Ft[k], m, n, x, c, err);
+            }
+            group_tab[(uint64_t)g * M1 + e] = pack_xc((uint32_t)x, (uint32_t)c);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chain scan over tables (hierarchical, fan-out TSCAN_FAN).  Level-L table j
+// spans [j*span, (j+1)*span); F at its start is Ft[j*span/TILE].
+// compose: one warp per output table; dynamic smem TSCAN_FAN*(m+1) uint64.
+__global__ void __launch_bounds__(32) rd_compose_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
+                                                        const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
+                                                        uint64_t* __restrict__ out, uint32_t* err) {
+    extern __shared__ uint64_t s_tab[];
+    const uint32_t o = blockIdx.x;
+    const uint32_t j0 = o * TSCAN_FAN;
+    const uint32_t cnt = min(TSCAN_FAN, P - j0);
+    const uint32_t M1 = m + 1;
+    for (uint32_t i = threadIdx.x; i < cnt * M1; i += 32) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    __syncwarp();
+    const uint64_t t0 = (uint64_t)j0 * span;
+    const uint64_t F0 = Ft[t0 / TILE];
+    for (uint32_t e = threadIdx.x; e < M1; e += 32) {
+        uint64_t x = e < m ? t0 + e : F0;
+        uint64_t c = 0;
+        for (uint32_t k = 0; k < cnt; ++k) {
+            const uint64_t tk = t0 + (uint64_t)k * span;
+            tab_apply(s_tab + k * M1, tk, tk + span, Ft[tk / TILE], m, n, x, c, err);
+        }
+        out[(uint64_t)o * M1 + e] = pack_xc((uint32_t)x, (uint32_t)c);
+    }
+}
+
+// top: P <= TSCAN_FAN tables, entry (0, 0); writes each table's entry and the
+// total run count r (b[r] = n).
+__global__ void rd_top_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
+                              const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
+                              uint64_t* __restrict__ entries, uint32_t* __restrict__ b, Summary* sum, uint32_t* err) {
+    if (threadIdx.x != 0) return;
+    const uint32_t M1 = m + 1;
+    uint64_t x = 0, c = 0;
+    for (uint32_t j = 0; j < P; ++j) {
+        entries[j] = pack_xc((uint32_t)x, (uint32_t)c);
+        const uint64_t tj = (uint64_t)j * span;
+        tab_apply(in + (uint64_t)j * M1, tj, tj + span, Ft[tj / TILE], m, n, x, c, err);
+    }
+    if (x != n) atomicOr(err, ERR_CHAIN);
+    sum->r = (uint32_t)c;
+    b[c] = (uint32_t)n;
+}
+
+// down: given the entry of each level-(L+1) table, derive level-L entries.
+__global__ void __launch_bounds__(32) rd_down_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
+                                                     const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
+                                                     const uint64_t* __restrict__ up_entries,
+                                                     uint64_t* __restrict__ entries, uint32_t* err) {
+    extern __shared__ uint64_t s_tab[];
+    const uint32_t o = blockIdx.x;
+    const uint32_t j0 = o * TSCAN_FAN;
+    const uint32_t cnt = min(TSCAN_FAN, P - j0);
+    const uint32_t M1 = m + 1;
+    for (uint32_t i = threadIdx.x; i < cnt * M1; i += 32) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    const uint64_t v = up_entries[o];
+    uint64_t x = unpack_x(v), c = unpack_c(v);
+    for (uint32_t k = 0; k < cnt; ++k) {
+        entries[j0 + k] = pack_xc((uint32_t)x, (uint32_t)c);
+        const uint64_t tk = (uint64_t)(j0 + k) * span;
+        tab_apply(s_tab + k * M1, tk, tk + span, Ft[tk / TILE], m, n, x, c, err);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RD2c: emit the run boundaries b[c] and natural lengths nat[c].
+__global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
+                                                      const uint32_t* __restrict__ Fg, uint32_t ngroups,
+                                                      const uint64_t* __restrict__ tile_tab,
+                                                      const uint32_t* __restrict__ Ft,
+                                                      const uint64_t* __restrict__ group_entries,
+                                                      uint32_t* __restrict__ b, uint32_t* __restrict__ nat,
+                                                      uint32_t* err) {
+    __shared__ uint32_t s_chg[GROUP_WORDS + 1];
+    __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
+    __shared__ uint64_t s_entry[TILES_PER_GROUP];
+    const uint32_t g = blockIdx.x;
+    ChainView cv;
+    build_chain_view(ty, n, g, ngroups, Fg, s_chg, s_nzn, cv, m);
+    const uint32_t M1 = m + 1;
+    const uint64_t tile0 = (uint64_t)g * TILES_PER_GROUP;
+    if (threadIdx.x == 0) {
+        const uint64_t v = group_entries[g];
+        uint64_t x = unpack_x(v), c = unpack_c(v);
+        for (uint32_t k = 0; k < TILES_PER_GROUP; ++k) {
+            s_entry[k] = pack_xc((uint32_t)x, (uint32_t)c);
+            const uint64_t tk = cv.G + (uint64_t)k * TILE;
+            tab_apply(tile_tab + (tile0 + k) * M1, tk, tk + TILE, Ft[tile0 + k], m, n, x, c, err);
+        }
+    }
+    __syncthreads();
+    const uint32_t w = warp_id();
+    if (lane_id() != 0) return;
+    const uint64_t t = cv.G + (uint64_t)w * TILE;
+    const uint64_t lim = min(t + TILE, n);
+    const uint64_t v = s_entry[w];
+    uint64_t x = unpack_x(v), c = unpack_c(v);
+    while (x < lim) {
+        uint64_t e;
+        const uint64_t nx = cv.next(x, &e);
+        b[c] = (uint32_t)x;
+        nat[c] = (uint32_t)(e - x);
+        c++;
+        x = nx;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Serial chain walker for min_run_len > MAX_M_TILED (chain steps are >= m
+// apart, so at most n/m steps); one warp scans change bits 1024 at a time.
+__global__ void rd_serial_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint64_t m,
+                                 uint32_t* __restrict__ b, uint32_t* __restrict__ nat, Summary* sum) {
+    const uint32_t lane = lane_id();
+    const uint64_t nwords = (n + 31) / 32;
+    uint64_t p = 0, c = 0;
+    while (p < n) {
+        const uint64_t q = p + 1;
+        uint64_t E = n;
+        if (q < n) {
+            const uint64_t y = q + 1;
+            const uint64_t lo = y > 2 ? y : 2;
+            for (uint64_t w0 = y / 32; w0 < nwords; w0 += 32) {
+                const uint64_t w = w0 + lane;
+                uint32_t chg = 0;
+                if (w < nwords) {
+                    const uint32_t tcur = ty[w];
+                    const uint32_t tprv = w ? ty[w - 1] : 0u;
+                    chg = (tcur ^ ((tcur << 1) | (tprv >> 31))) & range_mask(w * 32, lo, n);
+                }
+                const uint32_t bal = __ballot_sync(PS_FULL, chg != 0);
+                if (bal) {
+                    const int l = __ffs(bal) - 1;
+                    const uint32_t cw = __shfl_sync(PS_FULL, chg, l);
+                    E = (w0 + l) * 32 + (__ffs(cw) - 1);
+                    break;
+                }
+            }
+        }
+        uint64_t s = p + m;
+        if (s > n) s = n;
+        const uint64_t nx = E > s ? E : s;
+        if (lane == 0) {
+            b[c] = (uint32_t)p;
+            nat[c] = (uint32_t)(E - p);
+        }
+        c++;
+        p = nx;
+    }
+    if (lane == 0) {
+        b[c] = (uint32_t)n;
+        sum->r = (uint32_t)c;
+    }
+}
+
+}  // namespace ps

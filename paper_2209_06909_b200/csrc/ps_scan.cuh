@@ -1,0 +1,149 @@
+// ps_scan.cuh -- device-wide reduce-then-scan for small auxiliary arrays
+// (run counts, power histograms, depth / stack-height difference arrays).
+// Forward or reverse, inclusive or exclusive, any commutative monoid.
+#pragma once
+
+#include "ps_common.cuh"
+
+namespace ps {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_BLK = SCAN_THREADS * SCAN_ITEMS;
+
+template <class T>
+struct OpSum {
+    PS_DEV T operator()(T a, T b) const { return a + b; }
+    PS_DEV static T id() { return T(0); }
+};
+template <class T>
+struct OpMin {
+    PS_DEV T operator()(T a, T b) const { return a < b ? a : b; }
+    PS_DEV static T id() { return T(~T(0)) > T(0) ? T(~T(0)) : T(0x7FFFFFFF); }
+};
+template <class T>
+struct OpMax {
+    PS_DEV T operator()(T a, T b) const { return a > b ? a : b; }
+    PS_DEV static T id() { return T(0); }
+};
+
+// Exclusive block scan of one value per thread (thread order); returns the
+// exclusive prefix, writes the block total.
+template <class T, class Op>
+PS_DEV T block_exclusive(T v, T& total, T* sw /* >= 32 */) {
+    Op op;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    T x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T y = __shfl_up_sync(PS_FULL, x, d);
+        if (lane >= d) x = op(y, x);
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < nw ? sw[lane] : Op::id();
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            T y = __shfl_up_sync(PS_FULL, w, d);
+            if (lane >= d) w = op(y, w);
+        }
+        sw[lane] = w;
+    }
+    __syncthreads();
+    T wpre = warp ? sw[warp - 1] : Op::id();
+    total = sw[nw - 1];
+    T ex = __shfl_up_sync(PS_FULL, x, 1);
+    if (lane == 0) ex = Op::id();
+    T r = op(wpre, ex);
+    __syncthreads();
+    return r;
+}
+
+template <class T, class Op>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, T* __restrict__ partial,
+                                                                   int64_t n, int reverse) {
+    __shared__ T sw[32];
+    Op op;
+    const int64_t base = (int64_t)blockIdx.x * SCAN_BLK;
+    T acc = Op::id();
+    for (int i = threadIdx.x; i < SCAN_BLK; i += SCAN_THREADS) {
+        int64_t g = base + i;
+        if (g < n) acc = op(acc, in[reverse ? n - 1 - g : g]);
+    }
+    T total;
+    block_exclusive<T, Op>(acc, total, sw);
+    if (threadIdx.x == 0) partial[blockIdx.x] = total;
+}
+
+template <class T, class Op>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const T* in, T* out, int64_t n,
+                                                                  const T* __restrict__ carry, int reverse,
+                                                                  int exclusive, T* total_out) {
+    __shared__ T items[SCAN_BLK];
+    __shared__ T sw[32];
+    Op op;
+    const int64_t base = (int64_t)blockIdx.x * SCAN_BLK;
+    for (int i = threadIdx.x; i < SCAN_BLK; i += SCAN_THREADS) {
+        int64_t g = base + i;
+        items[i] = g < n ? in[reverse ? n - 1 - g : g] : Op::id();
+    }
+    __syncthreads();
+    T loc[SCAN_ITEMS];
+    T acc = Op::id();
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        loc[j] = items[threadIdx.x * SCAN_ITEMS + j];
+        acc = op(acc, loc[j]);
+    }
+    T total;
+    T pre = block_exclusive<T, Op>(acc, total, sw);
+    T c = carry ? carry[blockIdx.x] : Op::id();
+    pre = op(c, pre);
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        T inc = op(pre, loc[j]);
+        items[threadIdx.x * SCAN_ITEMS + j] = exclusive ? pre : inc;
+        pre = inc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SCAN_BLK; i += SCAN_THREADS) {
+        int64_t g = base + i;
+        if (g < n) out[reverse ? n - 1 - g : g] = items[i];
+    }
+    if (total_out && threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) *total_out = op(c, total);
+}
+
+// Elements of temporary storage device_scan needs for n items.
+inline int64_t scan_tmp_elems(int64_t n) {
+    int64_t t = 0;
+    while (n > SCAN_BLK) {
+        n = (n + SCAN_BLK - 1) / SCAN_BLK;
+        t += n + 32;
+    }
+    return t + 64;
+}
+
+// out may alias in.  tmp: scan_tmp_elems(n) elements.  total_out (device,
+// nullable) receives the reduction of all n items.
+template <class T, class Op>
+cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclusive, T* tmp, T* total_out,
+                        cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t nb = (n + SCAN_BLK - 1) / SCAN_BLK;
+    if (nb == 1) {
+        scan_apply_kernel<T, Op><<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr, reverse, exclusive, total_out);
+        return cudaGetLastError();
+    }
+    T* partial = tmp;
+    T* rest = tmp + nb + 32;
+    scan_reduce_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, partial, n, reverse);
+    cudaError_t e = device_scan<T, Op>(partial, partial, nb, false, true, rest, nullptr, s);
+    if (e != cudaSuccess) return e;
+    scan_apply_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, partial, reverse, exclusive,
+                                                                    total_out);
+    return cudaGetLastError();
+}
+
+}  // namespace ps

@@ -1,0 +1,455 @@
+// ps_tree.cuh -- N2: boundary powers and the stack-free merge tree.
+//
+// The reference runs a stack over the run boundaries (policy.py:250-259,
+// RunStack :94-129, _merge_one_group :132-143, _merge_down :146-175).  Its
+// merge tree is a function of the boundary powers alone:
+//   * boundary j (between runs j-1 and j), power P[j] (power.py:58-74,
+//     computed exactly with a clz on 32-bit fixed-point midpoints, F4);
+//   * R(j) = next boundary to the right with strictly smaller power; the
+//     boundaries sharing (R, P) form one main-loop merge whose left end is
+//     the previous boundary with strictly smaller power;
+//   * boundaries with no R form the "spine" that _merge_down collapses.
+// With sentinels P[0] = P[r] = 0 every query "nearest <= to the right/left"
+// is answered by a 32-ary min tree over the uint8 powers.
+#pragma once
+
+#include "ps_common.cuh"
+
+namespace ps {
+
+// ---------------------------------------------------------------------------
+// T1: powers.  P[j] for j in [0, padded): P[0] = P[r] = 0, j > r -> 0xFF.
+__global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
+                                   uint8_t* __restrict__ P, uint32_t padded, uint32_t* err) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= padded) return;
+    uint32_t v;
+    if (j == 0 || j == r) {
+        v = 0;
+    } else if (j > r) {
+        v = 0xFF;
+    } else {
+        // doubled midpoints A = b1+e1, B = b2+e2 of runs j-1 and j (power.py:67-68)
+        const uint64_t A = (uint64_t)b[j - 1] + b[j];
+        const uint64_t B = (uint64_t)b[j] + b[j + 1];
+        // floor(A * 2^32 / 2n) < 2^32 since A < 2n
+        const uint32_t x = (uint32_t)((A << 31) / n);
+        const uint32_t y = (uint32_t)((B << 31) / n);
+        const uint32_t d = __clz(x ^ y) + 1;  // first differing fraction bit
+        v = (d + log2k - 1) / log2k;        // least p with d <= p*log2(k)
+        if (v >= NPOW) {
+            atomicOr(err, ERR_POWER);
+            v = NPOW - 1;
+        }
+    }
+    P[j] = (uint8_t)v;
+}
+
+// T2: one level of the 32-ary min tree (bytes).
+__global__ void tree_minlevel_kernel(const uint8_t* __restrict__ in, uint32_t in_groups, uint8_t* __restrict__ out,
+                                     uint32_t out_padded) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= out_padded) return;
+    uint32_t v = 0xFF;
+    if (i < in_groups) {
+        const uint4* p = reinterpret_cast<const uint4*>(in + (uint64_t)i * 32);
+        uint4 a = p[0], c = p[1];
+        uint32_t m = __vminu4(__vminu4(__vminu4(a.x, a.y), __vminu4(a.z, a.w)),
+                              __vminu4(__vminu4(c.x, c.y), __vminu4(c.z, c.w)));
+        m = __vminu4(m, m >> 16);
+        m = __vminu4(m, m >> 8);
+        v = m & 0xFF;
+    }
+    out[i] = (uint8_t)v;
+}
+
+struct MinTree {
+    const uint8_t* lev[8];
+    uint32_t nlev;
+};
+
+// bit i set iff arr[grp*32 + i] <= v
+PS_DEV uint32_t group_le_mask(const uint8_t* arr, uint32_t grp, uint32_t v) {
+    const uint4* p = reinterpret_cast<const uint4*>(arr + (uint64_t)grp * 32);
+    const uint4 a = __ldg(p), c = __ldg(p + 1);
+    const uint32_t vv = v * 0x01010101u;
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    uint32_t mask = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t cm = __vcmpleu4(w[i], vv);
+        mask |= (((cm & 0x80808080u) * 0x00204081u) >> 28) << (4 * i);
+    }
+    return mask;
+}
+
+// first index > j with P <= v
+PS_DEV uint32_t find_right_le(const MinTree& t, uint32_t j, uint32_t v) {
+    uint32_t idx = j, L = 0, f;
+    for (;;) {
+        const uint32_t grp = idx >> 5, off = idx & 31;
+        uint32_t mask = group_le_mask(t.lev[L], grp, v);
+        mask &= off == 31 ? 0u : (PS_FULL << (off + 1));
+        if (mask) {
+            f = grp * 32 + (__ffs(mask) - 1);
+            break;
+        }
+        if (L + 1 >= t.nlev) return INF32;
+        idx = grp;
+        L++;
+    }
+    while (L > 0) {
+        L--;
+        const uint32_t mask = group_le_mask(t.lev[L], f, v);
+        f = f * 32 + (__ffs(mask) - 1);
+    }
+    return f;
+}
+
+// last index < j with P <= v
+PS_DEV uint32_t find_left_le(const MinTree& t, uint32_t j, uint32_t v) {
+    uint32_t idx = j, L = 0, f;
+    for (;;) {
+        const uint32_t grp = idx >> 5, off = idx & 31;
+        uint32_t mask = group_le_mask(t.lev[L], grp, v);
+        mask &= off == 0 ? 0u : (PS_FULL >> (32 - off));
+        if (mask) {
+            f = grp * 32 + (31 - __clz(mask));
+            break;
+        }
+        if (L + 1 >= t.nlev) return INF32;
+        idx = grp;
+        L++;
+    }
+    while (L > 0) {
+        L--;
+        const uint32_t mask = group_le_mask(t.lev[L], f, v);
+        f = f * 32 + (31 - __clz(mask));
+    }
+    return f;
+}
+
+// T3a: Rle[j] = first j' > j with P[j'] <= P[j]; Lle[j] = last j' < j with P[j'] <= P[j].
+__global__ void tree_nearest_kernel(MinTree t, const uint8_t* __restrict__ P, uint32_t r, uint32_t* __restrict__ Rle,
+                                    uint32_t* __restrict__ Lle) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (j >= r) return;
+    const uint32_t v = P[j];
+    Rle[j] = find_right_le(t, j, v);
+    Lle[j] = find_left_le(t, j, v);
+}
+
+// Classification of boundary j (1 <= j <= r-1).
+struct BoundaryClass {
+    bool head;        // rightmost member of a main-loop merge node
+    bool spine;       // never popped by the main loop
+    uint32_t rstrict; // R(j) (strictly smaller to the right) or INF32
+    uint32_t nmem;    // head only: members
+    uint32_t bidx[5]; // head only: begin, members..., end (boundary indices)
+};
+
+PS_DEV BoundaryClass classify(uint32_t j, const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle,
+                              const uint32_t* __restrict__ Lle, uint32_t r, uint32_t k, uint32_t* err) {
+    BoundaryClass c;
+    const uint32_t v = P[j];
+    const uint32_t rr = Rle[j];
+    c.head = rr < r && P[rr] < v;
+    c.spine = false;
+    c.rstrict = INF32;
+    c.nmem = 0;
+    if (c.head) {
+        c.rstrict = rr;
+        uint32_t mem[4];
+        uint32_t cnt = 0;
+        mem[cnt++] = j;
+        uint32_t ll = Lle[j];
+        while (ll >= 1 && P[ll] == v) {
+            if (cnt >= k - 1) {
+                atomicOr(err, ERR_GROUP);
+                break;
+            }
+            mem[cnt++] = ll;
+            ll = Lle[ll];
+        }
+        c.nmem = cnt;
+        c.bidx[0] = ll;
+        for (uint32_t i = 0; i < cnt; ++i) c.bidx[1 + i] = mem[cnt - 1 - i];
+        c.bidx[1 + cnt] = rr;
+    } else {
+        // follow the equal-power chain to the right (<= k-2 steps)
+        uint32_t x = j;
+        uint32_t steps = 0;
+        while (Rle[x] < r && P[Rle[x]] == v) {
+            x = Rle[x];
+            if (++steps > 8) {
+                atomicOr(err, ERR_GROUP);
+                break;
+            }
+        }
+        if (Rle[x] >= r) {
+            c.spine = true;
+        } else {
+            c.rstrict = Rle[x];
+        }
+    }
+    return c;
+}
+
+constexpr uint32_t CLS_THREADS = 1024;
+
+// T3b (PASS 0): per-block / per-warp histogram of head powers, spine list,
+// depth and stack-height difference arrays.  (PASS 1): stable scatter of the
+// main-loop nodes into per-power buckets (ascending power, position order).
+template <int PASS>
+__global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
+    const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle, const uint32_t* __restrict__ Lle,
+    const uint32_t* __restrict__ b, uint32_t r, uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
+    const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff, int32_t* __restrict__ Sdiff,
+    uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum) {
+    __shared__ uint32_t whist[32][NPOW];
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    for (uint32_t i = tid; i < 32 * NPOW; i += blockDim.x) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t j = blockIdx.x * CLS_THREADS + tid + 1;
+    const bool valid = j < r;
+    BoundaryClass c;
+    c.head = false;
+    uint32_t p = 0xFF;
+    if (valid) {
+        c = classify(j, P, Rle, Lle, r, k, &sum->err);
+        if (c.head) p = P[j];
+    }
+    const uint32_t peers = __match_any_sync(PS_FULL, p);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+    if (c.head && rank == 0) whist[warp][p] = __popc(peers);
+    __syncthreads();
+    // exclusive scan over warps per power bucket
+    if (tid < NPOW) {
+        uint32_t acc = 0;
+        for (int w = 0; w < 32; ++w) {
+            const uint32_t x = whist[w][tid];
+            whist[w][tid] = acc;
+            acc += x;
+        }
+        if (PASS == 0) blockHist[(uint64_t)tid * nblocks + blockIdx.x] = acc;
+    }
+    __syncthreads();
+    if (PASS == 0) {
+        if (valid) {
+            // stack height: boundary j is on the stack from its push until R(j)
+            atomicAdd(&Sdiff[j], 1);
+            if (c.rstrict != INF32) atomicAdd(&Sdiff[c.rstrict], -1);
+            if (c.head) {
+                // depth: the node strictly contains boundaries (begin, end)
+                atomicAdd(&Ddiff[c.bidx[0] + 1], 1);
+                atomicAdd(&Ddiff[c.bidx[1 + c.nmem]], -1);
+            }
+            if (c.spine) {
+                const uint32_t s = atomicAdd(&sum->nspine, 1u);
+                if (s < MAX_SPINE)
+                    spine_list[s] = j;
+                else
+                    atomicOr(&sum->err, ERR_SPINE);
+            }
+        }
+    } else if (c.head) {
+        const uint32_t slot = blockOff[(uint64_t)p * nblocks + blockIdx.x] + whist[warp][p] + rank;
+        Node nd;
+        const uint32_t arity = c.nmem + 1;
+        for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = i <= arity ? b[c.bidx[i]] : 0u;
+        nd.arity = (uint8_t)arity;
+        nd.parity = 0;
+        nd.power = (uint8_t)p;
+        nd.flags = 0;
+        nd.probe = c.bidx[1];
+        nd.chunk_base = 0;
+        nd.nchunks = 0;
+        nd.order = c.bidx[1 + c.nmem];  // R's boundary index
+        nodes[slot] = nd;
+    }
+}
+
+// T4: the spine and _merge_down (policy.py:146-175), one thread.
+__global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
+                                  uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
+                                  int32_t* __restrict__ Ddiff, Summary* sum) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t H = sum->nspine;
+    if (H > MAX_SPINE) {
+        atomicOr(&sum->err, ERR_SPINE);
+        H = MAX_SPINE;
+    }
+    // sort (insertion sort, H <= MAX_SPINE)
+    for (uint32_t i = 1; i < H; ++i) {
+        uint32_t x = spine_list[i];
+        int jj = (int)i - 1;
+        while (jj >= 0 && spine_list[jj] > x) {
+            spine_list[jj + 1] = spine_list[jj];
+            jj--;
+        }
+        spine_list[jj + 1] = x;
+    }
+    const uint32_t nmain = sum->level_off[NPOW];
+    uint32_t nn = 0;
+    // stack begins (boundary indices): beta[1] = 0, beta[h] = s_{h-1}
+    uint32_t beta[MAX_SPINE + 2];
+    uint32_t height = H;
+    beta[1] = 0;
+    for (uint32_t h = 2; h <= H; ++h) beta[h] = spine_list[h - 2];
+    uint32_t run_begin = H ? spine_list[H - 1] : 0;
+    auto emit = [&](const uint32_t* bb, uint32_t w) {
+        Node nd;
+        for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = 0;
+        for (uint32_t i = 0; i < w; ++i) nd.pos[i] = b[bb[i]];
+        nd.pos[w] = b[r];
+        nd.arity = (uint8_t)w;
+        nd.parity = 0;
+        nd.power = 0;
+        nd.flags = 1;
+        nd.probe = bb[1];
+        nd.chunk_base = 0;
+        nd.nchunks = 0;
+        nd.order = nn;
+        nodes[nmain + nn] = nd;
+        nn++;
+        atomicAdd(&Ddiff[bb[0] + 1], 1);
+        atomicAdd(&Ddiff[r], -1);
+    };
+    if (H > 0) {
+        if (k == 4 && !strict) {
+            const uint32_t n_runs = height + 1;
+            const uint32_t rem = n_runs % 3;
+            if (rem == 0) {
+                const uint32_t b2 = beta[height--];
+                const uint32_t b1 = beta[height--];
+                const uint32_t bb[3] = {b1, b2, run_begin};
+                emit(bb, 3);
+                run_begin = b1;
+            } else if (rem == 2) {
+                const uint32_t b1 = beta[height--];
+                const uint32_t bb[2] = {b1, run_begin};
+                emit(bb, 2);
+                run_begin = b1;
+            }
+            while (height) {
+                const uint32_t b3 = beta[height--];
+                const uint32_t b2 = beta[height--];
+                const uint32_t b1 = beta[height--];
+                const uint32_t bb[4] = {b1, b2, b3, run_begin};
+                emit(bb, 4);
+                run_begin = b1;
+            }
+        } else {
+            while (height) {
+                const uint32_t cnt = (k - 1) < height ? (k - 1) : height;
+                uint32_t bb[4];
+                for (uint32_t i = 0; i < cnt; ++i) bb[cnt - 1 - i] = beta[height--];
+                bb[cnt] = run_begin;
+                emit(bb, cnt + 1);
+                run_begin = bb[0];
+            }
+        }
+    }
+    sum->nspine_nodes = nn;
+}
+
+// T5: per-node depth/parity, chunk counts and merge statistics; leaf parity.
+// slack_mode: 0 -> slack = arity ("4way"/"2way" sentinel kernels),
+//             1 -> 2-way 0, 3/4-way 1 ("4way-nosentinel"), 2 -> 0.
+__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nnodes, const int32_t* __restrict__ S,
+                                           int slack_mode, Summary* sum) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
+    if (i < nnodes) {
+        Node nd = nodes[i];
+        const int32_t depth = S[nd.probe] - 1;
+        nd.parity = (uint8_t)(depth & 1);
+        const uint32_t w = nd.arity;
+        const uint32_t size = nd.pos[w] - nd.pos[0];
+        uint32_t nch = 1;
+        if (size > CHUNK_CAP) {
+            const uint32_t spacing = CHUNK_CAP / w;
+            for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / spacing;
+        }
+        nd.nchunks = nch;
+        nodes[i] = nd;
+        cost = size;
+        m2 = w == 2;
+        m3 = w == 3;
+        m4 = w == 4;
+        slack = slack_mode == 0 ? w : (slack_mode == 1 ? (w == 2 ? 0 : 1) : 0);
+        if (depth < 0) atomicOr(&sum->err, ERR_CHAIN);
+    }
+    for (int d = 16; d; d >>= 1) {
+        cost += __shfl_xor_sync(PS_FULL, cost, d);
+        m2 += __shfl_xor_sync(PS_FULL, m2, d);
+        m3 += __shfl_xor_sync(PS_FULL, m3, d);
+        m4 += __shfl_xor_sync(PS_FULL, m4, d);
+        slack += __shfl_xor_sync(PS_FULL, slack, d);
+    }
+    if (lane_id() == 0 && cost) {
+        atomicAdd(&sum->merge_cost, cost);
+        atomicAdd(&sum->merges[2], m2);
+        atomicAdd(&sum->merges[3], m3);
+        atomicAdd(&sum->merges[4], m4);
+        atomicAdd(&sum->scan_slack, slack);
+    }
+}
+
+__global__ void tree_leaf_parity_kernel(const int32_t* __restrict__ S, uint32_t r, uint8_t* __restrict__ leafpar) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= r) return;
+    const int32_t a = j == 0 ? 0 : S[j];
+    const int32_t c = j + 1 >= r ? 0 : S[j + 1];
+    leafpar[j] = (uint8_t)((a > c ? a : c) & 1);
+}
+
+__global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r, Summary* sum, uint32_t cap) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    int32_t v = (j < r) ? H[j] : 0;
+    for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
+    if (lane_id() == 0 && v > 0) {
+        atomicMax(&sum->max_stack, (uint32_t)v);
+        if ((uint32_t)v > cap) atomicOr(&sum->err, ERR_STACK);
+    }
+}
+
+// level offsets of the power buckets from the scanned block histograms
+__global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
+                                          uint32_t nblocks, Summary* sum) {
+    const uint32_t p = threadIdx.x;
+    if (p < NPOW) sum->level_off[p] = blockOff[(uint64_t)p * nblocks];
+    if (p == 0) {
+        sum->level_off[NPOW] = *total;
+        sum->nmain = *total;
+    }
+}
+
+__global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ base,
+                                            uint32_t nnodes) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nnodes) nodes[i].chunk_base = base[i];
+}
+
+__global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nnodes) out[i] = nodes[i].nchunks;
+}
+
+// chunk -> node map by binary search over the nodes' chunk_base.
+__global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t total_chunks,
+                                      uint32_t* __restrict__ chunk2node) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= total_chunks) return;
+    uint32_t lo = 0, hi = nnodes;  // find last node with chunk_base <= c
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (nodes[mid].chunk_base <= c)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    chunk2node[c] = lo;
+}
+
+}  // namespace ps

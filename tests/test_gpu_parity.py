@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle on the BASELINE config recipes."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle  # noqa: E402
+from paper_2209_06909_b200 import (  # noqa: E402
+    SortConfig,
+    merge_cost_for_profile,
+    read_trace,
+    scanned_elements_estimate,
+    stable_argsort,
+    stable_sort_with,
+    workloads,
+)
+
+NP_DTYPE = {"int32": np.int32, "int64": np.int64, "float32": np.float32}
+POLICY_FIELDS = ("merge_cost", "max_stack_height", "runs_detected", "merges2", "merges3", "merges4")
+COUNTER_FIELDS = ("buffer_cost", "scan_reads", "scan_writes")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available()
+    return torch.device("cuda", 0)
+
+
+def gpu_sort(keys_np, dev, **cfg):
+    keys = torch.from_numpy(np.ascontiguousarray(keys_np)).to(dev)
+    out, perm, stats = stable_argsort(keys, SortConfig(**cfg))
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), perm.cpu().numpy(), stats
+
+
+def test_golden_sorts(golden_sorts, dev):
+    for case in golden_sorts:
+        keys = np.array(case["keys"], dtype=NP_DTYPE[case["dtype"]])
+        cfg = dict(k=case["k"], variant=case["variant"], min_run_len=case["min_run_len"],
+                   strict_merge_down=case["strict"])
+        if keys.size == 0:
+            continue
+        out, perm, stats = gpu_sort(keys, dev, **cfg)
+        assert perm.tolist() == case["perm"], cfg
+        assert np.array_equal(out.view(np.uint8), keys[perm].view(np.uint8))
+        want = case["stats"]
+        for f in POLICY_FIELDS:
+            assert getattr(stats, f) == want[f], (f, cfg)
+        if case["variant"] != "2way-copy-smaller":
+            for f in COUNTER_FIELDS:
+                assert getattr(stats, f) == want[f], (f, cfg)
+        assert stats.run_lengths == want["run_lengths"]
+        assert stats.natural_run_lengths == want["natural_run_lengths"]
+        assert [[list(b), l] for b, l in read_trace(device=dev)] == case["trace"], cfg
+
+
+def test_golden_profiles(golden_profiles, dev):
+    for case in golden_profiles:
+        trace = []
+        cost = merge_cost_for_profile(case["lengths"], case["k"], case["strict"], on_merge=trace.append)
+        assert cost == case["cost"]
+        assert [[list(b), l] for b, l in trace] == case["trace"]
+
+
+@pytest.mark.parametrize("name,n", [("cfg1", 1 << 20), ("cfg2", 1 << 20), ("cfg3", 1 << 20), ("cfg4", 1 << 20),
+                                    ("cfg5", 1 << 20)])
+@pytest.mark.parametrize("k", [4, 2])
+def test_recipes_vs_oracle(name, n, k, dev):
+    keys = workloads.generate(name, n=n, seed=11)
+    variant = "4way" if k == 4 else "2way"
+    ref = oracle.sort(keys, k=k, variant=variant)
+    out, perm, stats = gpu_sort(keys, dev, k=k, variant=variant)
+    assert np.array_equal(perm, ref.values)
+    assert np.array_equal(out.view(np.uint8), ref.keys.view(np.uint8))
+    for f in POLICY_FIELDS + COUNTER_FIELDS:
+        assert getattr(stats, f) == ref.stats[f], f
+    assert stats.run_lengths == ref.run_lengths
+    assert stats.natural_run_lengths == ref.natural_run_lengths
+    assert read_trace(device=dev) == ref.trace
+    assert scanned_elements_estimate(stats, n) == 4 * ref.stats["merge_cost"] + 2 * n
+
+
+def test_cfg1_full_matches_reference_golden(golden_cfg_full, dev):
+    import hashlib
+
+    g = golden_cfg_full["cfg1"]
+    keys = workloads.generate("cfg1", n=g["n"], seed=g["seed"])
+    out, perm, stats = gpu_sort(keys, dev)
+    assert hashlib.sha256(perm.astype(np.int64).tobytes()).hexdigest() == g["perm_sha256"]
+    for f in POLICY_FIELDS + COUNTER_FIELDS:
+        assert getattr(stats, f) == g["stats"][f], f
+    trace = read_trace(device=dev)
+    flat = [x for b, l in trace for x in (len(b) - 1, *b, *([-1] * (5 - len(b))), l)]
+    assert hashlib.sha256(np.asarray(flat, dtype=np.int64).tobytes()).hexdigest() == g["trace_sha256"]
+
+
+@pytest.mark.parametrize("mrl", [1, 2, 7, 24, 64, 255, 256, 257, 600])
+def test_min_run_len_sweep(mrl, dev):
+    rng = np.random.default_rng(mrl)
+    for kind in range(3):
+        n = int(rng.integers(1, 40000))
+        if kind == 0:
+            keys = rng.integers(0, 50, size=n).astype(np.int32)
+        elif kind == 1:
+            keys = workloads.cfg2(n=n, seed=mrl)
+        else:
+            keys = np.sort(rng.integers(-100, 100, size=n)).astype(np.int64)
+            keys[n // 3 : n // 2] = keys[n // 3 : n // 2][::-1]
+        ref = oracle.sort(keys, min_run_len=mrl)
+        out, perm, stats = gpu_sort(keys, dev, min_run_len=mrl)
+        assert np.array_equal(perm, ref.values), (mrl, kind, n)
+        assert stats.run_lengths == ref.run_lengths
+        assert stats.merge_cost == ref.stats["merge_cost"]
+        assert read_trace(device=dev) == ref.trace
+
+
+def test_values_payload_permuted(dev):
+    keys_np = workloads.cfg3(n=1 << 16, seed=5)
+    vals_np = np.random.default_rng(1).integers(-1000, 1000, size=keys_np.size).astype(np.int32)
+    keys = torch.from_numpy(keys_np).to(dev)
+    vals = torch.from_numpy(vals_np).to(dev)
+    stable_sort_with(keys, SortConfig(), values=vals)
+    perm = np.argsort(keys_np, kind="stable")
+    assert np.array_equal(vals.cpu().numpy(), vals_np[perm])
+    assert np.array_equal(keys.cpu().numpy(), keys_np[perm])
+
+
+def test_list_api_records(dev):
+    from operator import itemgetter
+
+    rng = np.random.default_rng(3)
+    keys = rng.integers(0, 7, size=300).tolist()
+    records = [(k, i) for i, k in enumerate(keys)]
+    lst = list(records)
+    stats = stable_sort_with(lst, SortConfig(key=itemgetter(0)))
+    assert lst == sorted(records, key=itemgetter(0))
+    assert stats.runs_detected >= 1
+
+
+def test_edge_sizes(dev):
+    for n in (1, 2, 3, 23, 24, 25, 47, 48, 49, 2047, 2048, 2049, 16383, 16384, 16385, 16384 * 33 + 5):
+        for gen in ("perm", "const", "desc", "asc"):
+            if gen == "perm":
+                keys = np.random.default_rng(n).permutation(n).astype(np.int32)
+            elif gen == "const":
+                keys = np.zeros(n, dtype=np.int32)
+            elif gen == "desc":
+                keys = np.arange(n, 0, -1).astype(np.int32)
+            else:
+                keys = np.arange(n).astype(np.int32)
+            ref = oracle.sort(keys)
+            out, perm, stats = gpu_sort(keys, dev)
+            assert np.array_equal(perm, ref.values), (n, gen)
+            assert stats.run_lengths == ref.run_lengths, (n, gen)
+            assert stats.merge_cost == ref.stats["merge_cost"]
+
+
+def test_float_signed_zero_and_ties(dev):
+    rng = np.random.default_rng(9)
+    keys = rng.choice(np.array([-0.0, 0.0, 1.0, -1.0, 2.5], dtype=np.float32), size=50000)
+    ref = oracle.sort(keys)
+    out, perm, stats = gpu_sort(keys, dev)
+    assert np.array_equal(perm, ref.values)
+    assert np.array_equal(out.view(np.uint32), ref.keys.view(np.uint32))
