@@ -1,0 +1,454 @@
+"""Benchmark: sorted keys/sec (4-way, stable) on BASELINE.json's configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A "step" is one full stable sort (run detection, merge tree, leaf formation,
+all merge levels) of one synthetic input resident in HBM.  Before every step
+the working array is restored from a pristine copy and L2 is flushed (a
+512 MiB write); neither is inside the timed interval, which is bracketed by
+CUDA events on the sort's stream.  ``e2e`` repeats the measurement through the
+public API (``stable_argsort``) with the input copied from pinned host memory
+and the sorted keys + permutation copied back inside the timed interval.
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, a C++ port of /root/reference/pkg/src/powersort, which is pure
+Python and cannot be installed on the GPU box) on the host cores: one
+independent full-size sort per thread.
+
+Multi-GPU (torchrun, one process per GPU): every rank sorts its own shard of
+the same size (weak scaling); the time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "sorted keys/sec (4-way, stable)"
+UNIT = "keys/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--n", type=int, default=None, help="override the config size (default: BASELINE size)")
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def config_dict(args, n, extra=None):
+    from paper_2209_06909_b200 import workloads
+
+    d = {
+        "workload": "%s: %s" % (args.config, workloads.DESCRIPTIONS[args.config]),
+        "n": n,
+        "k": args.k,
+        "variant": "4way" if args.k == 4 else "2way",
+        "min_run_len": 24,
+        "seed": args.seed,
+        "key_dtype": None,
+        "payload": "int32 source index (stable argsort)",
+        "l2": "flushed before every step (512 MiB write); inputs restored from a pristine copy outside the timed interval",
+    }
+    if extra:
+        d.update(extra)
+    return d
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config):
+    """dram bytes per merge launch from the committed ncu capture, or None."""
+    path = os.path.join(REPO, "profiles", "merge_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_baseline(keys_np, k, seconds):
+    """Single-thread oracle (C++ port of the reference) on the full input,
+    repeated for about `seconds`."""
+    from oracle import oracle
+
+    variant = "4way" if k == 4 else "2way"
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        oracle.sort(keys_np, k=k, variant=variant, want_trace=False, want_runs=False)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 20:
+            break
+    n = keys_np.shape[0]
+    return {
+        "value": n * len(times) / sum(times),
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "port",
+        "sample": "%d full-size sort(s) of the same %d-key input, oracle/ C++ restatement of the reference "
+                  "(single-threaded, as the reference)" % (len(times), n),
+    }
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    from paper_2209_06909_b200 import workloads
+
+    n = args.n or workloads.FULL_N[args.config]
+    keys_np = workloads.generate(args.config, n=n, seed=args.seed)
+    variant = "4way" if args.k == 4 else "2way"
+    ncpu = os.cpu_count() or 1
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    per_sort = keys_np.nbytes * 3 + n * 4 * 3 + (64 << 20)
+    threads = max(1, min(ncpu, int(avail * 0.6 // per_sort), 64))
+
+    def one():
+        oracle.sort(keys_np, k=args.k, variant=variant, want_trace=False, want_runs=False)
+
+    def step():
+        ts = [threading.Thread(target=one) for _ in range(threads)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    total = 0.0
+    for _ in range(args.steps):
+        total += step()
+    value = threads * n * args.steps / total
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": str(keys_np.dtype),
+        "data": "synthetic (seeded %s recipe, SURVEY 8d)" % args.config,
+        "config": config_dict(args, n, {"key_dtype": str(keys_np.dtype)}),
+        "cpu_baseline": {
+            "value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "%d threads, each one independent full %d-key sort per step (oracle/ C++ restatement of "
+                      "the pure-Python reference; the algorithm is sequential, so threads run separate sorts)"
+                      % (threads, n),
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def certificate_gpu(torch, src, keys, perm):
+    """O(n) stable-sort certificate on the device."""
+    n = src.numel()
+    p = perm.long()
+    seen = torch.zeros(n, dtype=torch.int32, device=src.device)
+    seen.index_fill_(0, p, 1)
+    assert int(seen.sum()) == n, "perm is not a permutation"
+    assert torch.equal(src[p], keys), "keys != src[perm]"
+    a, b = keys[:-1], keys[1:]
+    assert bool((a <= b).all()), "keys not sorted"
+    eq = a == b
+    assert not bool((p[:-1][eq] > p[1:][eq]).any()), "equal keys out of source order"
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_06909_b200 import SortConfig, _lib, stable_argsort, workloads
+    from paper_2209_06909_b200.policy import _sort_tensor
+
+    rank, local, world = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    n = args.n or workloads.FULL_N[args.config]
+    keys_np = workloads.generate(args.config, n=n, seed=args.seed + rank)
+    cfg = SortConfig(k=args.k, variant="4way" if args.k == 4 else "2way")
+    src = torch.from_numpy(keys_np).to(dev)
+    keys = torch.empty_like(src)
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def reset():
+        keys.copy_(src)
+        flush.fill_(1)
+
+    def sort_once():
+        return _sort_tensor(keys, perm, cfg, _lib.VALUES_ARGSORT, collect_runs=False)
+
+    # warm-up (+ one certified run)
+    for i in range(max(args.warmup, 1)):
+        reset()
+        stats = sort_once()
+        if i == 0:
+            torch.cuda.synchronize()
+            certificate_gpu(torch, src, keys, perm)
+    torch.cuda.synchronize()
+
+    # timed region: K sorts, each bracketed by events (reset/flush outside)
+    lib.ps_profile_enable(1)
+    phases = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches0 = lib.ps_launch_count()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        reset()
+        ev[i][0].record(stream)
+        sort_once()
+        ev[i][1].record(stream)
+        phases.append(_lib.profile_read())
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = lib.ps_launch_count() - launches0
+    clocks = sampler.stop()
+    lib.ps_profile_enable(0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms = float(t.item())
+
+    # e2e through the public API: pinned H2D, sort, D2H of keys + permutation
+    e2e = None
+    if not args.no_e2e:
+        h_keys = torch.from_numpy(keys_np).pin_memory()
+        h_out = torch.empty_like(h_keys).pin_memory()
+        h_perm = torch.empty(n, dtype=torch.int32).pin_memory()
+        d_keys = torch.empty_like(src)
+
+        def e2e_step():
+            d_keys.copy_(h_keys, non_blocking=True)
+            _, p, _ = stable_argsort(d_keys, cfg, collect_runs=False)
+            h_out.copy_(d_keys, non_blocking=True)
+            h_perm.copy_(p, non_blocking=True)
+
+        for _ in range(max(args.warmup, 1)):
+            flush.fill_(1)
+            e2e_step()
+        torch.cuda.synchronize()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.fill_(1)
+            eev[i][0].record(stream)
+            e2e_step()
+            eev[i][1].record(stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(h_out.numpy(), keys.cpu().numpy())
+        e_ms = sum(a.elapsed_time(b) for a, b in eev)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {
+            "value": world * n * args.steps / (e_ms / 1e3),
+            "unit": UNIT,
+            "h2d_bytes_per_step": int(h_keys.numel() * h_keys.element_size()),
+            "d2h_bytes_per_step": int(h_out.numel() * h_out.element_size() + h_perm.numel() * 4),
+            "ms_per_step": e_ms / args.steps,
+            "api": "paper_2209_06909_b200.stable_argsort (C ABI ps_sort)",
+        }
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (merge_chunks) and phase breakdown
+    peak, peak_src = load_peaks()
+    agg = {}
+    merge_bytes = merge_ms = part_ms = 0.0
+    merge_launches = 0
+    for ph in phases:
+        for e in ph:
+            a = agg.setdefault(e["kind"], {"ms": 0.0, "bytes": 0})
+            a["ms"] += e["ms"]
+            a["bytes"] += e["bytes"]
+            if e["kind"] == "merge":
+                merge_bytes += e["bytes"]
+                merge_ms += e["ms"]
+                merge_launches += 1
+            if e["kind"] == "partition":
+                part_ms += e["ms"]
+    K = args.steps
+    per_step = {k: {"ms": v["ms"] / K, "GB": v["bytes"] / K / 1e9} for k, v in agg.items()}
+    achieved = merge_bytes / (merge_ms / 1e3) / 1e9 if merge_ms else 0.0
+    pass_gbs = merge_bytes / ((merge_ms + part_ms) / 1e3) / 1e9 if merge_ms else 0.0
+    traffic = load_traffic(args.config)
+    roofline = {
+        "bound": "hbm",
+        "kernel": "merge_chunks_kernel (all merge launches of a step)",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": achieved / peak if peak else None,
+        "peak_source": peak_src,
+        "traffic": traffic,
+        "algorithmic_bytes_per_step": merge_bytes / K,
+        "launches_per_step": merge_launches / K,
+        "merge_pass_gbs_incl_partition": pass_gbs,
+        "merge_pass_frac_of_8TBps": pass_gbs / 8000.0,
+    }
+    line = {
+        "metric": METRIC,
+        "value": world * n * K / (total_ms / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": str(keys_np.dtype),
+        "data": "synthetic (seeded %s recipe, SURVEY 8d; numpy PCG64)" % args.config,
+        "config": config_dict(args, n, {"key_dtype": str(keys_np.dtype),
+                                        "parallelism": "1 GPU" if world == 1 else "%d independent shards" % world}),
+        "e2e": e2e,
+        "roofline": roofline,
+        "phases_per_step": per_step,
+        "stats": {"merge_cost": stats.merge_cost, "runs": stats.runs_detected,
+                  "merges": [stats.merges2, stats.merges3, stats.merges4]},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "wall_s_timed_loop": wall,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_baseline(keys_np, args.k, args.cpu_seconds)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

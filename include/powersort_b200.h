@@ -140,6 +140,27 @@ int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys
                    const int64_t* shard_n, int64_t out_begin, int64_t out_end, void* out_keys, int32_t* out_vals,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* Phase timing of ps_sort (CUDA events on the sort's stream).  Enabled per
+ * host thread; ps_profile_read returns the entries of the last profiled sort.
+ * kind: 0 run detection, 1 merge tree, 2 leaf formation, 3 cut partition,
+ * 4 merge launch.  bytes = algorithmic HBM bytes of the entry: merges read
+ * and write every record once (2 * sum(node sizes) * record bytes). */
+typedef struct {
+    int32_t kind;
+    int32_t stage;   /* merge stage index (power levels high..low, then merge_down) */
+    int64_t nodes;
+    int64_t chunks;
+    int64_t bytes;
+    float ms;
+    float pad;
+} ps_prof_entry;
+
+int ps_profile_enable(int32_t on);
+int ps_profile_read(ps_prof_entry* out, int32_t cap, int32_t* count);
+
+/* Number of kernels this library has launched in this process. */
+int64_t ps_launch_count(void);
+
 /* Message for the last non-OK status on this thread. */
 const char* ps_last_error(void);
 

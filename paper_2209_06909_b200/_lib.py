@@ -33,6 +33,9 @@ EXPORTS = (
     "ps_run_stack_capacity",
     "ps_shard_merge_workspace_size",
     "ps_shard_merge",
+    "ps_profile_enable",
+    "ps_profile_read",
+    "ps_launch_count",
     "ps_last_error",
     "ps_version",
 )
@@ -65,6 +68,20 @@ class PsStats(ctypes.Structure):
         ("moves_valid", ctypes.c_int32),
     ]
 
+
+class PsProfEntry(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("stage", ctypes.c_int32),
+        ("nodes", ctypes.c_int64),
+        ("chunks", ctypes.c_int64),
+        ("bytes", ctypes.c_int64),
+        ("ms", ctypes.c_float),
+        ("pad", ctypes.c_float),
+    ]
+
+
+PROF_KINDS = {0: "run_detection", 1: "merge_tree", 2: "leaf_formation", 3: "partition", 4: "merge"}
 
 _lib = None
 
@@ -104,6 +121,12 @@ def load():
     lib.ps_shard_merge_workspace_size.restype = sz
     lib.ps_shard_merge.argtypes = [i32, i32, vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]
     lib.ps_shard_merge.restype = ctypes.c_int
+    lib.ps_profile_enable.argtypes = [i32]
+    lib.ps_profile_enable.restype = ctypes.c_int
+    lib.ps_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
+    lib.ps_profile_read.restype = ctypes.c_int
+    lib.ps_launch_count.argtypes = []
+    lib.ps_launch_count.restype = i64
     lib.ps_last_error.argtypes = []
     lib.ps_last_error.restype = ctypes.c_char_p
     lib.ps_version.argtypes = []
@@ -127,3 +150,17 @@ def check(code):
     if code == PS_EOVERFLOW:
         raise OverflowError(msg)
     raise RuntimeError(msg)
+
+
+def profile_read():
+    """Phase entries of the last profiled ps_sort on this thread."""
+    lib = load()
+    cnt = ctypes.c_int32(0)
+    lib.ps_profile_read(None, 0, ctypes.byref(cnt))
+    arr = (PsProfEntry * max(cnt.value, 1))()
+    lib.ps_profile_read(arr, cnt.value, ctypes.byref(cnt))
+    return [
+        dict(kind=PROF_KINDS.get(e.kind, str(e.kind)), stage=e.stage, nodes=e.nodes, chunks=e.chunks,
+             bytes=e.bytes, ms=e.ms)
+        for e in arr[: cnt.value]
+    ]

@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -30,6 +31,56 @@ using namespace ps;
 namespace {
 
 thread_local std::string g_last_error;
+thread_local bool g_prof_on = false;
+thread_local std::vector<ps_prof_entry> g_prof_last;
+
+// CUDA-event phase timer (only active when ps_profile_enable(1) was called).
+struct Prof {
+    struct Rec {
+        ps_prof_entry e;
+        cudaEvent_t a, b;
+    };
+    bool on;
+    cudaStream_t s;
+    std::vector<Rec> recs;
+    explicit Prof(cudaStream_t st) : on(g_prof_on), s(st) {}
+    ~Prof() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    }
+    int begin(int kind, int stage, int64_t nodes, int64_t chunks, int64_t bytes) {
+        if (!on) return -1;
+        Rec r;
+        memset(&r.e, 0, sizeof(r.e));
+        r.e.kind = kind;
+        r.e.stage = stage;
+        r.e.nodes = nodes;
+        r.e.chunks = chunks;
+        r.e.bytes = bytes;
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        cudaEventRecord(r.a, s);
+        recs.push_back(r);
+        return (int)recs.size() - 1;
+    }
+    void end(int i) {
+        if (i >= 0) cudaEventRecord(recs[i].b, s);
+    }
+    void finish() {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        g_prof_last.clear();
+        for (auto& r : recs) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            r.e.ms = ms;
+            g_prof_last.push_back(r.e);
+        }
+    }
+};
+
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -42,6 +93,13 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess)                                                                     \
             return fail(PS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
                                       __FILE__ + ":" + std::to_string(__LINE__));                  \
+    } while (0)
+
+// after every kernel launch: count it and surface launch errors
+#define PS_LAUNCH_CHECK()            \
+    do {                             \
+        launch_counter()++;          \
+        PS_CUDA(cudaGetLastError()); \
     } while (0)
 
 constexpr uint64_t WS_MAGIC = 0x5053423230304b31ull;  // "PSB200K1"
@@ -178,7 +236,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     // T1 powers (array over 0..padded)
     const uint32_t padded = (uint32_t)L.lev_size[0];
     tree_powers_kernel<<<grid_for(padded, 256), 256, 0, s>>>(b, r, n, log2k, P, padded, err);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     // T2 min tree
     MinTree mt;
     memset(&mt, 0, sizeof(mt));
@@ -192,7 +250,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
             uint8_t* out = at<uint8_t>(ws, L.minlev[nlev]);
             tree_minlevel_kernel<<<grid_for(outp, 256), 256, 0, s>>>(mt.lev[nlev - 1], (uint32_t)groups, out,
                                                                      (uint32_t)outp);
-            PS_CUDA(cudaGetLastError());
+            PS_LAUNCH_CHECK();
             mt.lev[nlev++] = out;
             size = outp;
         }
@@ -201,7 +259,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     uint32_t* Rle = at<uint32_t>(ws, L.Rle);
     uint32_t* Lle = at<uint32_t>(ws, L.Lle);
     tree_nearest_kernel<<<grid_for(r, 256), 256, 0, s>>>(mt, P, r, Rle, Lle);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     // T3 classify
     int32_t* Dd = at<int32_t>(ws, L.Dd);
     int32_t* Sd = at<int32_t>(ws, L.Sd);
@@ -215,16 +273,16 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     Node* nodes = at<Node>(ws, L.nodes);
     tree_classify_kernel<0><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
                                                             spine, nodes, sum);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist, hoff, (int64_t)NPOW * nblocks, false, true,
                                                    at<uint32_t>(ws, L.scantmp_u32), htot, s)));
     tree_level_offsets_kernel<<<1, 128, 0, s>>>(hoff, htot, nblocks, sum);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     tree_classify_kernel<1><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
                                                             spine, nodes, sum);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     tree_spine_kernel<<<1, 1, 0, s>>>(b, r, k, strict, spine, nodes, Dd, sum);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Dd, Dd, (int64_t)r + 1, false, false,
                                                  at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
@@ -236,33 +294,33 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
     const int64_t cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
     tree_stack_max_kernel<<<grid_for(r, 256), 256, 0, s>>>(Sd, r, sum, (uint32_t)cap);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     if (leafpar) {
         tree_leaf_parity_kernel<<<grid_for(r, 256), 256, 0, s>>>(Dd, r, leafpar);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
     }
     if (nnodes) {
         tree_nodes_finalize_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, Dd, slack_mode, sum);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
         uint32_t* nch = at<uint32_t>(ws, L.nch);
         uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
         tree_nchunks_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, nch);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
         PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nnodes, false, true,
                                                        at<uint32_t>(ws, L.scantmp_u32), cb + nnodes, s)));
         tree_copy_chunk_base_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, cb, nnodes);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
         info.node_chunk.resize(nnodes + 1);
         PS_CUDA(cudaMemcpyAsync(info.node_chunk.data(), cb, (nnodes + 1) * 4, cudaMemcpyDeviceToHost, s));
     }
     PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
-    if (nnodes) {
+    if (nnodes && info.node_chunk[nnodes] > 0) {
         const uint32_t total = info.node_chunk[nnodes];
         if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
         tree_chunk_map_kernel<<<grid_for(total, 256), 256, 0, s>>>(nodes, nnodes, total,
                                                                    at<uint32_t>(ws, L.chunk2node));
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
     }
     if (info.s.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
     if (info.s.err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(info.s.err) + ")");
@@ -349,10 +407,13 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     uint32_t* b = at<uint32_t>(ws, L.b);
     uint32_t* nat = at<uint32_t>(ws, L.nat);
     const uint32_t ngroups = (uint32_t)L.ngroups;
+    const int64_t rec_bytes = (int64_t)sizeof(K) + 4;
+    Prof prof(s);
 
     // ---- N1 pass 1: run detection ------------------------------------------
+    const int ph_rd = prof.begin(0, -1, 0, 0, n * (int64_t)sizeof(K));
     rd_types_kernel<K><<<ngroups, 256, 0, s>>>(keys, (uint64_t)n, ty, cg);
-    PS_CUDA(cudaGetLastError());
+    PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpMin<uint32_t>>(cg, Fg, ngroups, true, false, at<uint32_t>(ws, L.scantmp_u32),
                                                    nullptr, s)));
     if (m <= MAX_M_TILED) {
@@ -362,7 +423,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         const size_t smem = (size_t)TILES_PER_GROUP * M1 * 8;
         rd_tables_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
                                                    err);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
         uint64_t span = GROUP;
         std::vector<uint64_t> spans(L.tab_levels);
         for (uint64_t l = 0; l < L.tab_levels; ++l) {
@@ -371,27 +432,28 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                 rd_compose_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
                     at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
                     at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
-                PS_CUDA(cudaGetLastError());
+                PS_LAUNCH_CHECK();
                 span *= TSCAN_FAN;
             }
         }
         const uint64_t top = L.tab_levels - 1;
         rd_top_kernel<<<1, 32, 0, s>>>(at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
                                        (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
         for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
             rd_down_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
                 at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
                 at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
-            PS_CUDA(cudaGetLastError());
+            PS_LAUNCH_CHECK();
         }
         rd_emit_kernel<<<ngroups, 256, 0, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
                                                at<uint64_t>(ws, L.lvl_ent[0]), b, nat, err);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
     } else {
         rd_serial_kernel<<<1, 32, 0, s>>>(ty, (uint64_t)n, m, b, nat, sum);
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
     }
+    prof.end(ph_rd);
     Summary h;
     PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
@@ -404,6 +466,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     TreeInfo info;
     memset(&info.s, 0, sizeof(info.s));
     uint32_t nnodes = 0;
+    const int ph_tree = prof.begin(1, -1, 0, 0, 0);
     if (r >= 2) {
         int rc = build_tree(ws, L, r, (uint64_t)n, cfg.k, cfg.strict_merge_down, slack_mode_of(cfg.variant), leafpar,
                             info, s);
@@ -412,6 +475,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     } else {
         PS_CUDA(cudaMemsetAsync(leafpar, 0, 1, s));
     }
+    prof.end(ph_tree);
 
     // ---- N1 pass 2: leaves -----------------------------------------------------
     Bufs<K> bufs;
@@ -422,6 +486,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     {
         const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M));
         const unsigned grid = grid_for((uint64_t)n, FORM_TILE);
+        const int ph = prof.begin(2, -1, r, 0, n * ((int64_t)sizeof(K) + rec_bytes));
         if (argsort) {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
@@ -433,7 +498,8 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             form_leaves_kernel<K, false><<<grid, FORM_THREADS, smem, s>>>(bufs, (uint64_t)n, b, nat, leafpar, r, ty,
                                                                           (uint32_t)m);
         }
-        PS_CUDA(cudaGetLastError());
+        PS_LAUNCH_CHECK();
+        prof.end(ph);
     }
 
     // ---- N3/N4: merges, stage by stage ------------------------------------------
@@ -441,31 +507,55 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         const Node* nodes = at<Node>(ws, L.nodes);
         const uint32_t* c2n = at<uint32_t>(ws, L.chunk2node);
         uint4* cuts = at<uint4>(ws, L.cuts);
-        const size_t msmem = merge_smem_bytes<K>();
-        PS_CUDA(cudaFuncSetAttribute(merge_chunks_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-        auto run_stage = [&](uint32_t nlo, uint32_t nhi) -> int {
+        const size_t psmem = merge_pipe_smem_bytes<K>();
+        const size_t ssmem = merge_small_smem_bytes<K>();
+        PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        PS_CUDA(cudaFuncSetAttribute(merge_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+        int dev = 0, sms = 148, occ = 1;
+        PS_CUDA(cudaGetDevice(&dev));
+        PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_pipe_kernel<K>, PIPE_THREADS, psmem));
+        const uint32_t pipe_grid_max = (uint32_t)std::max(1, sms * std::max(occ, 1));
+        int stage = 0;
+        auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint64_t cost, uint32_t nsmall) -> int {
             if (nhi <= nlo) return PS_OK;
             const uint32_t c0 = info.node_chunk[nlo], c1 = info.node_chunk[nhi];
-            if (c1 - c0 > nhi - nlo) {
-                merge_partition_kernel<K><<<grid_for(c1 - c0, 128), 128, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
-                PS_CUDA(cudaGetLastError());
+            const uint32_t nbig = (nhi - nlo) - nsmall;
+            const int ph = prof.begin(4, stage, nhi - nlo, c1 - c0, 2 * (int64_t)cost * rec_bytes);
+            if (nsmall) {
+                merge_small_kernel<K><<<grid_for(nhi - nlo, SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(bufs, nodes,
+                                                                                                        nlo, nhi);
+                PS_LAUNCH_CHECK();
             }
-            merge_chunks_kernel<K><<<c1 - c0, MERGE_THREADS, msmem, s>>>(bufs, nodes, c2n, cuts, c0, err);
-            PS_CUDA(cudaGetLastError());
+            if (c1 > c0) {
+                if (c1 - c0 > nbig) {
+                    const int pp = prof.begin(3, stage, nbig, c1 - c0, 0);
+                    merge_partition_kernel<K><<<grid_for(c1 - c0, 128), 128, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
+                    PS_LAUNCH_CHECK();
+                    prof.end(pp);
+                }
+                const uint32_t units = c1 - c0;
+                merge_pipe_kernel<K><<<std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s>>>(bufs, nodes, c2n, cuts,
+                                                                                                 c0, units, err);
+                PS_LAUNCH_CHECK();
+            }
+            prof.end(ph);
+            stage++;
             return PS_OK;
         };
         for (int p = (int)NPOW - 1; p >= 1; --p) {
-            int rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1]);
+            int rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p]);
             if (rc) return rc;
         }
         for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
-            int rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1);
+            int rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i]);
             if (rc) return rc;
         }
     }
     PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
     if (h.err) return fail(PS_EINVARIANT, "merge invariant violated (flags " + std::to_string(h.err) + ")");
+    prof.finish();
     int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
     if (rc) return rc;
 
@@ -496,6 +586,21 @@ extern "C" {
 const char* ps_last_error(void) { return g_last_error.c_str(); }
 
 const char* ps_version(void) { return "powersort-b200 0.1.0 (sm_100a)"; }
+
+int ps_profile_enable(int32_t on) {
+    g_prof_on = on != 0;
+    return PS_OK;
+}
+
+int ps_profile_read(ps_prof_entry* out, int32_t cap, int32_t* count) {
+    const int32_t n = (int32_t)g_prof_last.size();
+    if (count) *count = n;
+    if (out)
+        for (int32_t i = 0; i < n && i < cap; ++i) out[i] = g_prof_last[i];
+    return PS_OK;
+}
+
+int64_t ps_launch_count(void) { return launch_counter().load(); }
 
 size_t ps_workspace_size(int64_t n, int32_t dtype, const ps_config* cfg) {
     if (n < 0 || !cfg || cfg->min_run_len < 1) return 0;

@@ -22,6 +22,7 @@ constexpr uint32_t CHUNK_CAP = 4096;  // max records per merge chunk (k * cut sp
 constexpr uint32_t MERGE_THREADS = 256;
 constexpr uint32_t MERGE_VT = CHUNK_CAP / MERGE_THREADS;  // 16 records per thread
 constexpr uint32_t MAX_WAY = 4;
+constexpr uint32_t SMALL_NODE = 512;  // nodes up to this size: one warp each (no chunking)
 
 constexpr uint32_t INF32 = 0xFFFFFFFFu;
 constexpr uint32_t MAX_SPINE = 256;
@@ -67,6 +68,10 @@ struct Summary {
     unsigned long long merges[5];      // by arity
     unsigned long long scan_slack;     // sum of per-merge slack (variant-specific)
     unsigned long long buffer_cost;
+    unsigned long long level_cost[NPOW];     // merge cost per power bucket
+    unsigned long long spine_cost[MAX_SPINE]; // merge cost per merge_down node
+    uint32_t level_small[NPOW];               // nodes <= SMALL_NODE per power bucket
+    uint32_t spine_small[MAX_SPINE];
 };
 
 PS_DEV uint32_t lane_id() { return threadIdx.x & 31u; }

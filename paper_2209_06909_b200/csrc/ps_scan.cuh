@@ -3,9 +3,17 @@
 // Forward or reverse, inclusive or exclusive, any commutative monoid.
 #pragma once
 
+#include <atomic>
+
 #include "ps_common.cuh"
 
 namespace ps {
+
+// Host-side count of kernels launched by this library (bench evidence).
+inline std::atomic<int64_t>& launch_counter() {
+    static std::atomic<int64_t> c{0};
+    return c;
+}
 
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
@@ -134,11 +142,13 @@ cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclu
     int64_t nb = (n + SCAN_BLK - 1) / SCAN_BLK;
     if (nb == 1) {
         scan_apply_kernel<T, Op><<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr, reverse, exclusive, total_out);
+        launch_counter()++;
         return cudaGetLastError();
     }
     T* partial = tmp;
     T* rest = tmp + nb + 32;
     scan_reduce_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, partial, n, reverse);
+    launch_counter() += 2;
     cudaError_t e = device_scan<T, Op>(partial, partial, nb, false, true, rest, nullptr, s);
     if (e != cudaSuccess) return e;
     scan_apply_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, partial, reverse, exclusive,

@@ -366,7 +366,7 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         nd.parity = (uint8_t)(depth & 1);
         const uint32_t w = nd.arity;
         const uint32_t size = nd.pos[w] - nd.pos[0];
-        uint32_t nch = 1;
+        uint32_t nch = size <= SMALL_NODE ? 0 : 1;
         if (size > CHUNK_CAP) {
             const uint32_t spacing = CHUNK_CAP / w;
             for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / spacing;
@@ -379,6 +379,13 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         m4 = w == 4;
         slack = slack_mode == 0 ? w : (slack_mode == 1 ? (w == 2 ? 0 : 1) : 0);
         if (depth < 0) atomicOr(&sum->err, ERR_CHAIN);
+        if (nd.flags & 1) {
+            sum->spine_cost[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size;
+            sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_NODE;
+        } else {
+            atomicAdd(&sum->level_cost[nd.power], (unsigned long long)size);
+            if (size <= SMALL_NODE) atomicAdd(&sum->level_small[nd.power], 1u);
+        }
     }
     for (int d = 16; d; d >>= 1) {
         cost += __shfl_xor_sync(PS_FULL, cost, d);
