@@ -530,12 +530,12 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             if (c1 > c0) {
                 if (c1 - c0 > nbig) {
                     const int pp = prof.begin(3, stage, nbig, c1 - c0, 0);
-                    merge_partition_kernel<K><<<grid_for(c1 - c0, 128), 128, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
+                    merge_partition_kernel<K><<<grid_for(c1 - c0, 8), 256, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
                     PS_LAUNCH_CHECK();
                     prof.end(pp);
                 }
                 const uint32_t units = c1 - c0;
-                merge_pipe_kernel<K><<<std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s>>>(bufs, nodes, c2n, cuts,
+                merge_pipe_kernel<K><<<std::min((units + 1) / 2, pipe_grid_max), PIPE_THREADS, psmem, s>>>(bufs, nodes, c2n, cuts,
                                                                                                  c0, units, err);
                 PS_LAUNCH_CHECK();
             }
