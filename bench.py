@@ -399,7 +399,7 @@ def run_ours(args):
     traffic = load_traffic(args.config)
     roofline = {
         "bound": "hbm",
-        "kernel": "merge_chunks_kernel (all merge launches of a step)",
+        "kernel": "merge_pipe_kernel + merge_small_kernel (all merge launches of a step)",
         "achieved": achieved,
         "peak": peak,
         "unit": "GB/s",

@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpowersort_b200.so")
+LIB_PATH = os.environ.get("PS_LIB") or os.path.join(_HERE, "libpowersort_b200.so")
 
 PS_OK, PS_EINVAL, PS_ECUDA, PS_ENOMEM, PS_EINVARIANT, PS_EOVERFLOW = range(6)
 

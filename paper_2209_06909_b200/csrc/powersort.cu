@@ -142,7 +142,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.ngroups = std::max<uint64_t>(1, cdiv(n, GROUP));
     L.ntiles = L.ngroups * TILES_PER_GROUP;
     // total chunks <= nodes + merge_cost / (CHUNK_CAP / MAX_WAY); merge_cost <= 64 n
-    L.chunks_max = L.rmax + cdiv(64 * n, CHUNK_CAP / MAX_WAY) + 16;
+    L.chunks_max = L.rmax + cdiv(64 * n, CHUNK_CAP / 2 / MAX_WAY) + 16;
     // min tree levels over P (size rmax + 1)
     uint64_t s = align_up(L.rmax + 1, 32);
     L.nlev = 0;
@@ -227,7 +227,7 @@ inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)std::max<uin
 // Builds the merge tree of the run boundaries b[0..r] (device, already in
 // place) for an array of n elements.  Leaves leaf parities when leafpar != 0.
 int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int strict, int slack_mode,
-               uint8_t* leafpar, TreeInfo& info, cudaStream_t s) {
+               uint8_t* leafpar, TreeInfo& info, cudaStream_t s, uint32_t cap = CHUNK_CAP) {
     Summary* sum = at<Summary>(ws, L.sum);
     uint32_t* err = &sum->err;
     const uint32_t* b = at<uint32_t>(ws, L.b);
@@ -292,15 +292,15 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
     const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
-    const int64_t cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
-    tree_stack_max_kernel<<<grid_for(r, 256), 256, 0, s>>>(Sd, r, sum, (uint32_t)cap);
+    const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
+    tree_stack_max_kernel<<<grid_for(r, 256), 256, 0, s>>>(Sd, r, sum, (uint32_t)stack_cap);
     PS_LAUNCH_CHECK();
     if (leafpar) {
         tree_leaf_parity_kernel<<<grid_for(r, 256), 256, 0, s>>>(Dd, r, leafpar);
         PS_LAUNCH_CHECK();
     }
     if (nnodes) {
-        tree_nodes_finalize_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, Dd, slack_mode, sum);
+        tree_nodes_finalize_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, Dd, slack_mode, cap, sum);
         PS_LAUNCH_CHECK();
         uint32_t* nch = at<uint32_t>(ws, L.nch);
         uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
@@ -469,7 +469,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     const int ph_tree = prof.begin(1, -1, 0, 0, 0);
     if (r >= 2) {
         int rc = build_tree(ws, L, r, (uint64_t)n, cfg.k, cfg.strict_merge_down, slack_mode_of(cfg.variant), leafpar,
-                            info, s);
+                            info, s, chunk_cap<K>());
         if (rc) return rc;
         nnodes = info.s.nmain + info.s.nspine_nodes;
     } else {
@@ -776,3 +776,18 @@ int ps_shard_merge(int32_t, int32_t, const void* const*, const int32_t* const*, 
 }
 
 }  // extern "C"
+
+#ifdef PS_PIPE_TIMING
+// Diagnostics build only: clock64 phase counters of merge_pipe_kernel
+// (producer: batch, wait-empty, stage, units; consumer: wait-full, pass 1,
+// pass 2, store, units).
+extern "C" int ps_debug_pipe_timing(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, ps::g_pipe_tim, 16 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ps::g_pipe_tim, z, sizeof(z));
+    }
+    return PS_OK;
+}
+#endif

@@ -18,7 +18,16 @@ constexpr uint32_t MAX_M_TILED = 256;             // larger min_run_len -> seria
 constexpr uint32_t TSCAN_FAN = 32;                // tables composed per warp in the chain scan
 
 // ---- merge geometry ------------------------------------------------------
-constexpr uint32_t CHUNK_CAP = 4096;  // max records per merge chunk (k * cut spacing)
+constexpr uint32_t CHUNK_CAP = 4096;  // max records per merge chunk (k * cut spacing), 4-byte keys
+// per key width: 8-byte keys use half the records so two CTAs still fit per SM
+template <class K>
+__host__ __device__ constexpr uint32_t chunk_cap() {
+#ifdef PS_CAP4
+    return sizeof(K) == 4 ? PS_CAP4 : CHUNK_CAP / 2;
+#else
+    return sizeof(K) == 4 ? CHUNK_CAP : CHUNK_CAP / 2;
+#endif
+}
 constexpr uint32_t MERGE_THREADS = 256;
 constexpr uint32_t MERGE_VT = CHUNK_CAP / MERGE_THREADS;  // 16 records per thread
 constexpr uint32_t MAX_WAY = 4;

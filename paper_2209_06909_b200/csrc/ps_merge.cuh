@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     }
     q -= 1;
     const uint32_t w = nd.arity;
-    const uint32_t S = CHUNK_CAP / w;
+    const uint32_t S = chunk_cap<K>() / w;
     const K* src = bufs.k[nd.parity ^ 1];
     uint32_t L[4];
 #pragma unroll
@@ -161,7 +161,11 @@ PS_DEV void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, ui
         : "memory");
 }
 // named barrier 1 over the consumer warps only
-PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(256) : "memory"); }
+#ifndef PS_CONSUMERS
+#define PS_CONSUMERS 256
+#endif
+constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
+PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(PIPE_CONSUMERS) : "memory"); }
 
 // ---------------------------------------------------------------------------
 // Small nodes (size <= SMALL_NODE): one warp per node, straight from global.
@@ -224,24 +228,54 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
 }
 
 // ---------------------------------------------------------------------------
+// Optional clock64 phase counters of the pipe kernel (build with -DPS_PIPE_TIMING)
+#ifdef PS_PIPE_TIMING
+__device__ unsigned long long g_pipe_tim[16];
+#define PT_START(on) long long _pt0 = clock64(); const bool _pton = (on);
+#define PT_MARK(idx)                                                         \
+    if (_pton) {                                                             \
+        const long long _t = clock64();                                      \
+        atomicAdd(&g_pipe_tim[idx], (unsigned long long)(_t - _pt0));        \
+        _pt0 = _t;                                                           \
+    }
+#define PT_COUNT(idx) \
+    if (_pton) atomicAdd(&g_pipe_tim[idx], 1ull);
+#else
+#define PT_START(on)
+#define PT_MARK(idx)
+#define PT_COUNT(idx)
+#endif
+
+// ---------------------------------------------------------------------------
 // Big-node chunks: persistent, warp-specialized, TMA-bulk double-buffered.
-constexpr uint32_t PIPE_CONSUMERS = 256;
 constexpr uint32_t PIPE_THREADS = 32 + PIPE_CONSUMERS;
 
 PS_DEV __host__ constexpr uint32_t align16c(uint32_t x) { return (x + 15u) & ~15u; }
-PS_DEV uint32_t padi(uint32_t o) { return o + (o >> 5); }  // bank padding: one slot per 32
+PS_DEV __host__ constexpr uint32_t cmax(uint32_t a, uint32_t b) { return a > b ? a : b; }
+
+// (key, value) record in shared memory: 8 bytes for 4-byte keys, 16 for 8-byte
+template <class K>
+struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
+    K k;
+    int32_t v;
+};
+
+// bank padding of record arrays: two records per 16, which keeps every
+// 4-record group 16-byte aligned for the vector store phase
+PS_DEV uint32_t padr(uint32_t o) { return o + ((o >> 4) << 1); }
 
 template <class K>
 struct PipeLayout {
-    static constexpr uint32_t PADN = CHUNK_CAP + CHUNK_CAP / 32 + 8;
-    // slot = TMA landing zone for the k windows (with 16B alignment slack), and
-    // afterwards the padded output of the last pass
-    static constexpr uint32_t KEY_BYTES = align16c(PADN * (uint32_t)sizeof(K)) + MAX_WAY * 32u;
-    static constexpr uint32_t VAL_BYTES = align16c(PADN * 4u) + MAX_WAY * 32u;
-    static constexpr uint32_t SLOT = KEY_BYTES + VAL_BYTES;
-    // scratch for the first-pass results X || Y (padded)
-    static constexpr uint32_t SKEY = align16c(PADN * (uint32_t)sizeof(K));
-    static constexpr uint32_t SCRATCH = SKEY + align16c(PADN * 4u);
+    static constexpr uint32_t CAP = chunk_cap<K>();
+    static constexpr uint32_t PADN = CAP + CAP / 8 + 16;  // padded record capacity
+    static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
+    // slot = TMA landing zone of the k key windows + k value windows (SoA, 16B
+    // alignment slack each), and afterwards the padded records of the last pass
+    static constexpr uint32_t KEY_BYTES = align16c(CAP * (uint32_t)sizeof(K)) + MAX_WAY * 32u;
+    static constexpr uint32_t VAL_BYTES = align16c(CAP * 4u) + MAX_WAY * 32u;
+    static constexpr uint32_t SLOT = align16c(cmax(KEY_BYTES + VAL_BYTES, PADN * RECB));
+    // scratch: first-pass records X || Y (or the 2-way output)
+    static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
 };
 
 struct PipeDesc {
@@ -255,49 +289,194 @@ size_t merge_pipe_smem_bytes() {
     return 2 * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::SCRATCH + 2 * sizeof(PipeDesc) + 64;
 }
 
-// A read-only sorted sequence in shared memory (optionally bank-padded).
+// Merge-path cursors.  Every consumer thread advances two independent cursors
+// in lockstep, so two dependency chains (search and serial merge) overlap.
+// WinCur merges two TMA-landed SoA windows, RecCur two padded record runs;
+// ties always go to the A side.  Outputs go to padded records out[base + o].
 template <class K>
-struct SeqView {
+struct WinCur {
+    const K *ak, *bk;
+    const int32_t *av, *bv;
+    uint32_t la, lb, i, j, o, oe, base;
+    K a, b;
+    PS_DEV uint32_t ca(uint32_t x) const { return x < la ? x : (la ? la - 1 : 0); }
+    PS_DEV uint32_t cb(uint32_t x) const { return x < lb ? x : (lb ? lb - 1 : 0); }
+    PS_DEV K keyA(uint32_t x) const { return ak[ca(x)]; }
+    PS_DEV K keyB(uint32_t x) const { return bk[cb(x)]; }
+    PS_DEV void heads() {
+        a = ak[ca(i)];
+        b = bk[cb(j)];
+    }
+    PS_DEV void step(Rec<K>* out) {
+        if (o >= oe) return;
+        const bool takeA = i < la && (j >= lb || !(b < a));
+        Rec<K> r;
+        r.k = takeA ? a : b;
+        r.v = *(takeA ? av + i : bv + j);
+        out[padr(base + o)] = r;
+        ++o;
+        i += takeA;
+        j += !takeA;
+        const K nk = *(takeA ? ak + ca(i) : bk + cb(j));
+        a = takeA ? nk : a;
+        b = takeA ? b : nk;
+    }
+};
+
+template <class K>
+struct RecCur {
+    const Rec<K>* r;
+    uint32_t offa, offb, la, lb, i, j, o, oe, base;
+    Rec<K> a, b;
+    PS_DEV uint32_t ia(uint32_t x) const { return padr(offa + (x < la ? x : (la ? la - 1 : 0))); }
+    PS_DEV uint32_t ib(uint32_t x) const { return padr(offb + (x < lb ? x : (lb ? lb - 1 : 0))); }
+    PS_DEV K keyA(uint32_t x) const { return r[ia(x)].k; }
+    PS_DEV K keyB(uint32_t x) const { return r[ib(x)].k; }
+    PS_DEV void heads() {
+        a = r[ia(i)];
+        b = r[ib(j)];
+    }
+    PS_DEV void step(Rec<K>* out) {
+        if (o >= oe) return;
+        const bool takeA = i < la && (j >= lb || !(b.k < a.k));
+        out[padr(base + o)] = takeA ? a : b;
+        ++o;
+        i += takeA;
+        j += !takeA;
+        const Rec<K> nx = r[takeA ? ia(i) : ib(j)];
+        a = takeA ? nx : a;
+        b = takeA ? b : nx;
+    }
+};
+
+// Interleaved diagonal searches for both cursors, then the lockstep merge.
+template <class C0, class C1, class K>
+PS_DEV void dual_merge(C0& c0, C1& c1, Rec<K>* out) {
+    uint32_t lo0 = c0.o > c0.lb ? c0.o - c0.lb : 0, hi0 = c0.o < c0.la ? c0.o : c0.la;
+    uint32_t lo1 = c1.o > c1.lb ? c1.o - c1.lb : 0, hi1 = c1.o < c1.la ? c1.o : c1.la;
+    if (c0.o >= c0.oe) lo0 = hi0;
+    if (c1.o >= c1.oe) lo1 = hi1;
+    while (lo0 < hi0 || lo1 < hi1) {
+        const uint32_t m0 = (lo0 + hi0) >> 1, m1 = (lo1 + hi1) >> 1;
+        const bool act0 = lo0 < hi0, act1 = lo1 < hi1;
+        // A[mid] <= B[d-1-mid]  (indices are clamped, results used only when active)
+        const bool le0 = !(c0.keyB(c0.o - 1 - m0) < c0.keyA(m0));
+        const bool le1 = !(c1.keyB(c1.o - 1 - m1) < c1.keyA(m1));
+        if (act0) {
+            lo0 = le0 ? m0 + 1 : lo0;
+            hi0 = le0 ? hi0 : m0;
+        }
+        if (act1) {
+            lo1 = le1 ? m1 + 1 : lo1;
+            hi1 = le1 ? hi1 : m1;
+        }
+    }
+    c0.i = lo0;
+    c0.j = c0.o - lo0;
+    c1.i = lo1;
+    c1.j = c1.o - lo1;
+    c0.heads();
+    c1.heads();
+    const uint32_t n0 = c0.oe > c0.o ? c0.oe - c0.o : 0, n1 = c1.oe > c1.o ? c1.oe - c1.o : 0;
+    const uint32_t nmax = n0 > n1 ? n0 : n1;
+#pragma unroll 2
+    for (uint32_t t = 0; t < nmax; ++t) {
+        c0.step(out);
+        c1.step(out);
+    }
+}
+
+// One cursor: diagonal search, then the serial branch-free merge.
+template <class C, class K>
+PS_DEV void single_merge(C& c, Rec<K>* out) {
+    if (c.o >= c.oe) return;
+    uint32_t lo = c.o > c.lb ? c.o - c.lb : 0, hi = c.o < c.la ? c.o : c.la;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        const bool le = !(c.keyB(c.o - 1 - m) < c.keyA(m));
+        lo = le ? m + 1 : lo;
+        hi = le ? hi : m;
+    }
+    c.i = lo;
+    c.j = c.o - lo;
+    c.heads();
+    const uint32_t n = c.oe - c.o;
+#pragma unroll 4
+    for (uint32_t t = 0; t < n; ++t) c.step(out);
+}
+
+// A TMA-landed input window: SoA keys / values, unpadded.
+template <class K>
+struct Win {
     const K* k;
     const int32_t* v;
     uint32_t len;
-    bool pad;
-    PS_DEV uint32_t at(uint32_t i) const { return pad ? padi(i) : i; }
+    PS_DEV uint32_t cl(uint32_t i) const { return i < len ? i : (len ? len - 1 : 0); }
+};
+// A padded record sequence: element i at r[padr(off + i)].
+template <class K>
+struct RecSeq {
+    const Rec<K>* r;
+    uint32_t len, off;
+    PS_DEV const Rec<K>& at(uint32_t i) const { return r[padr(off + (i < len ? i : (len ? len - 1 : 0)))]; }
 };
 
-// Merge-path: produce outputs [o0, o1) of merge(A, B) (ties to A) into the
-// padded arrays ok/ov at positions base + o.
-template <class K>
-PS_DEV void merge_range(const SeqView<K>& A, const SeqView<K>& B, K* ok, int32_t* ov, uint32_t base, uint32_t o0,
-                        uint32_t o1) {
-    if (o0 >= o1) return;
-    // diagonal search: i = # of A among the first o0 outputs
-    uint32_t lo = o0 > B.len ? o0 - B.len : 0;
-    uint32_t hi = o0 < A.len ? o0 : A.len;
+// Merge-path diagonal: # of A among the first d outputs of merge(A, B), ties to A.
+template <class K, class GA, class GB>
+PS_DEV uint32_t diag_search(uint32_t d, uint32_t la, uint32_t lb, GA ka, GB kb) {
+    uint32_t lo = d > lb ? d - lb : 0;
+    uint32_t hi = d < la ? d : la;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (!(B.k[B.at(o0 - 1 - mid)] < A.k[A.at(mid)]))  // A[mid] <= B[o0-1-mid]
-            lo = mid + 1;
-        else
-            hi = mid;
+        const bool le = !(kb(d - 1 - mid) < ka(mid));  // A[mid] <= B[d-1-mid]
+        lo = le ? mid + 1 : lo;
+        hi = le ? hi : mid;
     }
-    uint32_t i = lo, j = o0 - lo;
-    K a = i < A.len ? A.k[A.at(i)] : K(0);
-    K b = j < B.len ? B.k[B.at(j)] : K(0);
+    return lo;
+}
+
+// outputs [o0, o1) of merge(A, B) of two SoA windows -> padded records out[base + o]
+template <class K>
+PS_DEV void merge_win(const Win<K>& A, const Win<K>& B, Rec<K>* out, uint32_t base, uint32_t o0, uint32_t o1) {
+    if (o0 >= o1) return;
+    uint32_t i = diag_search<K>(o0, A.len, B.len, [&](uint32_t x) { return A.k[x]; },
+                                [&](uint32_t x) { return B.k[x]; });
+    uint32_t j = o0 - i;
+    K a = A.k[A.cl(i)];
+    K b = B.k[B.cl(j)];
+#pragma unroll 4
     for (uint32_t o = o0; o < o1; ++o) {
-        const bool takeA = j >= B.len || (i < A.len && !(b < a));
-        const uint32_t po = padi(base + o);
-        if (takeA) {
-            ok[po] = a;
-            ov[po] = A.v[A.at(i)];
-            ++i;
-            if (i < A.len) a = A.k[A.at(i)];
-        } else {
-            ok[po] = b;
-            ov[po] = B.v[B.at(j)];
-            ++j;
-            if (j < B.len) b = B.k[B.at(j)];
-        }
+        const bool takeA = i < A.len && (j >= B.len || !(b < a));
+        Rec<K> rec;
+        rec.k = takeA ? a : b;
+        rec.v = *(takeA ? A.v + i : B.v + j);
+        out[padr(base + o)] = rec;
+        i += takeA;
+        j += !takeA;
+        const K nk = *(takeA ? A.k + A.cl(i) : B.k + B.cl(j));
+        a = takeA ? nk : a;
+        b = takeA ? b : nk;
+    }
+}
+
+// outputs [o0, o1) of merge(X, Y) of two padded record sequences
+template <class K>
+PS_DEV void merge_rec(const RecSeq<K>& X, const RecSeq<K>& Y, Rec<K>* out, uint32_t o0, uint32_t o1) {
+    if (o0 >= o1) return;
+    uint32_t i = diag_search<K>(o0, X.len, Y.len, [&](uint32_t x) { return X.r[padr(X.off + x)].k; },
+                                [&](uint32_t x) { return Y.r[padr(Y.off + x)].k; });
+    uint32_t j = o0 - i;
+    Rec<K> a = X.at(i);
+    Rec<K> b = Y.at(j);
+#pragma unroll 4
+    for (uint32_t o = o0; o < o1; ++o) {
+        const bool takeA = i < X.len && (j >= Y.len || !(b.k < a.k));
+        out[padr(o)] = takeA ? a : b;
+        i += takeA;
+        j += !takeA;
+        const Rec<K> nx = takeA ? X.at(i) : Y.at(j);
+        a = takeA ? nx : a;
+        b = takeA ? b : nx;
     }
 }
 
@@ -329,6 +508,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         const uint32_t cbeg = c0 + (uint32_t)(((uint64_t)nchunks * blockIdx.x) / gridDim.x);
         const uint32_t cend = c0 + (uint32_t)(((uint64_t)nchunks * (blockIdx.x + 1)) / gridDim.x);
         uint32_t unit = 0;
+        PT_START(lane == 0)
         for (uint32_t c = cbeg; c < cend;) {
             // batch descriptors of chunks c .. c+31 (lane l <-> chunk c+l)
             const uint32_t x = c + lane;
@@ -352,6 +532,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 nid = INF32;
             }
             const uint32_t nvalid = min(32u, cend - c);
+            PT_MARK(0)
             uint32_t u = 0;
             while (u < nvalid) {
                 // unit = lanes u..V of the same node with total <= CHUNK_CAP
@@ -359,7 +540,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 const uint32_t sx = __shfl_sync(PS_FULL, st.x, u), sy = __shfl_sync(PS_FULL, st.y, u);
                 const uint32_t sz = __shfl_sync(PS_FULL, st.z, u), sw = __shfl_sync(PS_FULL, st.w, u);
                 const uint32_t tot = (en.x - sx) + (en.y - sy) + (en.z - sz) + (en.w - sw);
-                const bool ok = lane >= u && lane < nvalid && nid == nid_u && tot <= CHUNK_CAP;
+                const bool ok = lane >= u && lane < nvalid && nid == nid_u && tot <= LY::CAP;
                 uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
                 // contiguous run of ok lanes starting at u
                 const uint32_t runlen = __ffs(~bal) ? __ffs(~bal) - 1 : 32 - u;
@@ -375,6 +556,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 // ---- stage the unit into slot (unit & 1) ----
                 const uint32_t slot = unit & 1;
                 if (unit >= 2) mbar_wait(&empty[slot], ((unit >> 1) - 1) & 1);
+                PT_MARK(1)
                 uint8_t* sbase = smem + slot * LY::SLOT;
                 const uint32_t sv4[4] = {sx, sy, sz, sw};
                 const uint32_t ev4[4] = {ex, ey, ez, ew};
@@ -441,9 +623,11 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     d.w = w;
                     d.par = par;
                     d.done = 0;
-                    if (total > CHUNK_CAP) atomicOr(err, ERR_CUT);
+                    if (total > LY::CAP) atomicOr(err, ERR_CUT);
                     mbar_arrive_tx(&full[slot], txs);
                 }
+                PT_MARK(2)
+                PT_COUNT(3)
                 unit++;
                 u = V + 1;
             }
@@ -462,118 +646,108 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     // ------------------------------ consumers ---------------------------------
     const uint32_t ctid = tid - 32;
     const uint32_t clane = ctid & 31;
-    K* const xk = reinterpret_cast<K*>(scratch);
-    int32_t* const xv = reinterpret_cast<int32_t*>(scratch + LY::SKEY);
+    Rec<K>* const xr = reinterpret_cast<Rec<K>*>(scratch);
+    PT_START(ctid == 0)
     for (uint32_t i = 0;; ++i) {
         const uint32_t slot = i & 1;
         mbar_wait(&full[slot], (i >> 1) & 1);
+        PT_MARK(4)
         const PipeDesc& d = desc[slot];
         if (d.done) break;
         const uint32_t T = d.T, w = d.w, par = d.par;
         const uint64_t out = d.out;
         uint8_t* sbase = smem + slot * LY::SLOT;
-        SeqView<K> win[4];
+        Win<K> win[4];
 #pragma unroll
         for (uint32_t a = 0; a < 4; ++a) {
             win[a].k = reinterpret_cast<const K*>(sbase + d.koff[a]);
             win[a].v = reinterpret_cast<const int32_t*>(sbase + d.voff[a]);
             win[a].len = a < w ? d.len[a] : 0;
-            win[a].pad = false;
         }
-        const uint32_t o0 = (uint32_t)(((uint64_t)T * ctid) / PIPE_CONSUMERS);
-        const uint32_t o1 = (uint32_t)(((uint64_t)T * (ctid + 1)) / PIPE_CONSUMERS);
-        K* ok;
-        int32_t* ov;
+        auto wincur = [&](uint32_t a, uint32_t b, uint32_t base, uint32_t o0, uint32_t o1) {
+            WinCur<K> c;
+            c.ak = win[a].k;
+            c.bk = win[b].k;
+            c.av = win[a].v;
+            c.bv = win[b].v;
+            c.la = win[a].len;
+            c.lb = win[b].len;
+            c.o = o0;
+            c.oe = o1;
+            c.base = base;
+            return c;
+        };
+        Rec<K>* orec;
+        constexpr uint32_t NC = PIPE_CONSUMERS;
+        // final records are placed with the global 16-byte phase of the
+        // destination so the store phase moves aligned 16-byte vectors
+        constexpr uint32_t ER = sizeof(K) == 4 ? 4 : 2;  // records per store group
+        const uint32_t al = (uint32_t)(out % ER);
+        const uint32_t o0 = (uint32_t)((uint64_t)T * ctid / NC), o1 = (uint32_t)((uint64_t)T * (ctid + 1) / NC);
         if (w >= 3) {
-            // pass 1: X = merge(A, B) -> scratch[0, LA+LB); Y = merge(C, D) (or C) -> scratch[LA+LB, T)
-            const uint32_t LX = win[0].len + win[1].len;
-            merge_range<K>(win[0], win[1], xk, xv, 0, o0, min(o1, LX));
-            merge_range<K>(win[2], win[3], xk, xv, LX, o0 > LX ? o0 - LX : 0, o1 > LX ? o1 - LX : 0);
+            // pass 1: X = merge(A, B) -> xr[0, LX);  Y = merge(C, D) (3-way: C) -> xr[LX, T)
+            // (thread t takes the t-th 1/NC of the concatenated X || Y output)
+            const uint32_t LX = win[0].len + win[1].len, LYn = T - LX;
+            WinCur<K> cx = wincur(0, 1, 0, o0, min(o1, LX));
+            single_merge(cx, xr);
+            WinCur<K> cy = wincur(2, 3, LX, o0 > LX ? o0 - LX : 0, o1 > LX ? o1 - LX : 0);
+            single_merge(cy, xr);
             consumer_sync();
-            // pass 2: merge X (scratch[0, LX)) and Y (scratch[LX, T)) into the
-            // slot, whose input windows are fully consumed
-            ok = reinterpret_cast<K*>(sbase);
-            ov = reinterpret_cast<int32_t*>(sbase + LY::KEY_BYTES);
-            // merge X and Y where Y element j lives at padded index LX + j
-            {
-                uint32_t lo = o0 > (T - LX) ? o0 - (T - LX) : 0;
-                uint32_t hi = o0 < LX ? o0 : LX;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (!(xk[padi(LX + o0 - 1 - mid)] < xk[padi(mid)]))
-                        lo = mid + 1;
-                    else
-                        hi = mid;
-                }
-                uint32_t ii = lo, jj = o0 - lo;
-                const uint32_t LY_ = T - LX;
-                K a = ii < LX ? xk[padi(ii)] : K(0);
-                K b = jj < LY_ ? xk[padi(LX + jj)] : K(0);
-                for (uint32_t o = o0; o < o1; ++o) {
-                    const bool takeA = jj >= LY_ || (ii < LX && !(b < a));
-                    const uint32_t po = padi(o);
-                    if (takeA) {
-                        ok[po] = a;
-                        ov[po] = xv[padi(ii)];
-                        ++ii;
-                        if (ii < LX) a = xk[padi(ii)];
-                    } else {
-                        ok[po] = b;
-                        ov[po] = xv[padi(LX + jj)];
-                        ++jj;
-                        if (jj < LY_) b = xk[padi(LX + jj)];
-                    }
-                }
-            }
+            PT_MARK(5)
+            // pass 2: merge X and Y into the slot (its input windows are consumed)
+            orec = reinterpret_cast<Rec<K>*>(sbase);
+            RecCur<K> p0;
+            p0.r = xr;
+            p0.offa = 0;
+            p0.offb = LX;
+            p0.la = LX;
+            p0.lb = LYn;
+            p0.base = al;
+            p0.o = o0;
+            p0.oe = o1;
+            single_merge(p0, orec);
         } else {
             // 2-way: merge(A, B) straight into scratch
-            ok = xk;
-            ov = xv;
-            merge_range<K>(win[0], win[1], ok, ov, 0, o0, o1);
+            orec = xr;
+            WinCur<K> c0 = wincur(0, 1, al, o0, o1);
+            single_merge(c0, orec);
         }
         consumer_sync();
-        // 16-byte stores aligned in global memory
+        PT_MARK(6)
+        // store: group j = records [ER*j, ER*j + ER) of the phase-shifted layout
         K* __restrict__ dstK = bufs.k[par];
         int32_t* __restrict__ dstV = bufs.v[par];
         {
-            constexpr uint32_t E = 16 / sizeof(K);
-            const uint32_t al = (uint32_t)(out % E);
-            const uint32_t ng = (al + T + E - 1) / E;
-            for (uint32_t j = ctid; j < ng; j += PIPE_CONSUMERS) {
-                const int32_t g0 = (int32_t)(j * E) - (int32_t)al;
-                if (g0 >= 0 && g0 + (int32_t)E <= (int32_t)T) {
-                    uint4 vv;
-                    K* pv = reinterpret_cast<K*>(&vv);
-#pragma unroll
-                    for (uint32_t t = 0; t < E; ++t) pv[t] = ok[padi(g0 + t)];
-                    *reinterpret_cast<uint4*>(dstK + out + g0) = vv;
-                } else {
-                    for (uint32_t t = 0; t < E; ++t) {
-                        const int32_t o = g0 + (int32_t)t;
-                        if (o >= 0 && o < (int32_t)T) dstK[out + o] = ok[padi(o)];
+            const uint32_t ng = (al + T + ER - 1) / ER;
+            const uint64_t gbase = out - al;  // global element of record index 0
+            for (uint32_t j = ctid; j < ng; j += NC) {
+                const uint32_t r0 = j * ER;
+                if (r0 >= al && r0 + ER <= al + T) {
+                    const uint4* src = reinterpret_cast<const uint4*>(orec + padr(r0));
+                    if (sizeof(K) == 4) {
+                        const uint4 q0 = src[0], q1 = src[1];  // (k0,v0,k1,v1) (k2,v2,k3,v3)
+                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.z, q1.x, q1.z);
+                        *reinterpret_cast<uint4*>(dstV + gbase + r0) = make_uint4(q0.y, q0.w, q1.y, q1.w);
+                    } else {
+                        const uint4 q0 = src[0], q1 = src[1];  // (k0 lo, k0 hi, v0, pad) (k1 lo, k1 hi, v1, pad)
+                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.y, q1.x, q1.y);
+                        *reinterpret_cast<uint2*>(dstV + gbase + r0) = make_uint2(q0.z, q1.z);
                     }
-                }
-            }
-            const uint32_t alv = (uint32_t)(out % 4);
-            const uint32_t ngv = (alv + T + 3) / 4;
-            for (uint32_t j = ctid; j < ngv; j += PIPE_CONSUMERS) {
-                const int32_t g0 = (int32_t)(j * 4) - (int32_t)alv;
-                if (g0 >= 0 && g0 + 4 <= (int32_t)T) {
-                    int4 vv;
-                    vv.x = ov[padi(g0)];
-                    vv.y = ov[padi(g0 + 1)];
-                    vv.z = ov[padi(g0 + 2)];
-                    vv.w = ov[padi(g0 + 3)];
-                    *reinterpret_cast<int4*>(dstV + out + g0) = vv;
                 } else {
-                    for (int32_t t = 0; t < 4; ++t) {
-                        const int32_t o = g0 + t;
-                        if (o >= 0 && o < (int32_t)T) dstV[out + o] = ov[padi(o)];
+                    for (uint32_t t = 0; t < ER; ++t) {
+                        const uint32_t rr = r0 + t;
+                        if (rr >= al && rr < al + T) {
+                            const Rec<K> rec = orec[padr(rr)];
+                            dstK[gbase + rr] = rec.k;
+                            dstV[gbase + rr] = rec.v;
+                        }
                     }
                 }
             }
         }
         consumer_sync();  // scratch / slot reads done before the next unit
+        PT_MARK(7)
+        PT_COUNT(8)
         if (clane == 0) mbar_arrive(&empty[slot]);
     }
 }

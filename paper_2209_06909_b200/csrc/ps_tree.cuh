@@ -357,7 +357,7 @@ __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, ui
 // slack_mode: 0 -> slack = arity ("4way"/"2way" sentinel kernels),
 //             1 -> 2-way 0, 3/4-way 1 ("4way-nosentinel"), 2 -> 0.
 __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nnodes, const int32_t* __restrict__ S,
-                                           int slack_mode, Summary* sum) {
+                                           int slack_mode, uint32_t cap, Summary* sum) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
     if (i < nnodes) {
@@ -367,8 +367,8 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         const uint32_t w = nd.arity;
         const uint32_t size = nd.pos[w] - nd.pos[0];
         uint32_t nch = size <= SMALL_NODE ? 0 : 1;
-        if (size > CHUNK_CAP) {
-            const uint32_t spacing = CHUNK_CAP / w;
+        if (size > cap) {
+            const uint32_t spacing = cap / w;
             for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / spacing;
         }
         nd.nchunks = nch;
