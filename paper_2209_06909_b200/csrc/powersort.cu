@@ -24,6 +24,7 @@
 #include "ps_merge.cuh"
 #include "ps_runs.cuh"
 #include "ps_scan.cuh"
+#include "ps_shard.cuh"
 #include "ps_tree.cuh"
 
 using namespace ps;
@@ -327,6 +328,62 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     return PS_OK;
 }
 
+// Runs one batch of disjoint merge nodes [nlo, nhi) whose chunks are
+// [c0, c1): small nodes by warps, big ones by partition + the TMA pipeline.
+template <class K>
+struct MergeRunner {
+    Bufs<K> bufs;
+    const Node* nodes;
+    const uint32_t* c2n;
+    uint4* cuts;
+    uint32_t* err;
+    cudaStream_t s;
+    size_t psmem, ssmem;
+    uint32_t pipe_grid_max;
+
+    int init(Bufs<K> b, const Node* nd, const uint32_t* chunk2node, uint4* ct, uint32_t* e, cudaStream_t st) {
+        bufs = b;
+        nodes = nd;
+        c2n = chunk2node;
+        cuts = ct;
+        err = e;
+        s = st;
+        psmem = merge_pipe_smem_bytes<K>();
+        ssmem = merge_small_smem_bytes<K>();
+        PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        PS_CUDA(cudaFuncSetAttribute(merge_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+        int dev = 0, sms = 148, occ = 1;
+        PS_CUDA(cudaGetDevice(&dev));
+        PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_pipe_kernel<K>, PIPE_THREADS, psmem));
+        pipe_grid_max = (uint32_t)std::max(1, sms * std::max(occ, 1));
+        return PS_OK;
+    }
+
+    int stage(uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint32_t nsmall, Prof* prof, int stage_id) {
+        if (nhi <= nlo) return PS_OK;
+        const uint32_t nbig = (nhi - nlo) - nsmall;
+        if (nsmall) {
+            merge_small_kernel<K><<<grid_for(nhi - nlo, SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(bufs, nodes, nlo,
+                                                                                                    nhi);
+            PS_LAUNCH_CHECK();
+        }
+        if (c1 > c0) {
+            if (c1 - c0 > nbig) {
+                const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
+                merge_partition_kernel<K><<<grid_for(c1 - c0, 8), 256, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
+                PS_LAUNCH_CHECK();
+                if (prof) prof->end(pp);
+            }
+            const uint32_t units = c1 - c0;
+            merge_pipe_kernel<K><<<std::min((units + 1) / 2, pipe_grid_max), PIPE_THREADS, psmem, s>>>(
+                bufs, nodes, c2n, cuts, c0, units, err);
+            PS_LAUNCH_CHECK();
+        }
+        return PS_OK;
+    }
+};
+
 int write_header(uint8_t* ws, const Layout& L, int64_t n, int64_t m, int k, int dtype, uint32_t r, uint32_t nmain,
                  uint32_t nspine, cudaStream_t s) {
     WsHeader h;
@@ -504,51 +561,25 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
 
     // ---- N3/N4: merges, stage by stage ------------------------------------------
     if (nnodes) {
-        const Node* nodes = at<Node>(ws, L.nodes);
-        const uint32_t* c2n = at<uint32_t>(ws, L.chunk2node);
-        uint4* cuts = at<uint4>(ws, L.cuts);
-        const size_t psmem = merge_pipe_smem_bytes<K>();
-        const size_t ssmem = merge_small_smem_bytes<K>();
-        PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-        PS_CUDA(cudaFuncSetAttribute(merge_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-        int dev = 0, sms = 148, occ = 1;
-        PS_CUDA(cudaGetDevice(&dev));
-        PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_pipe_kernel<K>, PIPE_THREADS, psmem));
-        const uint32_t pipe_grid_max = (uint32_t)std::max(1, sms * std::max(occ, 1));
+        MergeRunner<K> mr;
+        int rc = mr.init(bufs, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts), err, s);
+        if (rc) return rc;
         int stage = 0;
         auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint64_t cost, uint32_t nsmall) -> int {
             if (nhi <= nlo) return PS_OK;
             const uint32_t c0 = info.node_chunk[nlo], c1 = info.node_chunk[nhi];
-            const uint32_t nbig = (nhi - nlo) - nsmall;
             const int ph = prof.begin(4, stage, nhi - nlo, c1 - c0, 2 * (int64_t)cost * rec_bytes);
-            if (nsmall) {
-                merge_small_kernel<K><<<grid_for(nhi - nlo, SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(bufs, nodes,
-                                                                                                        nlo, nhi);
-                PS_LAUNCH_CHECK();
-            }
-            if (c1 > c0) {
-                if (c1 - c0 > nbig) {
-                    const int pp = prof.begin(3, stage, nbig, c1 - c0, 0);
-                    merge_partition_kernel<K><<<grid_for(c1 - c0, 8), 256, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
-                    PS_LAUNCH_CHECK();
-                    prof.end(pp);
-                }
-                const uint32_t units = c1 - c0;
-                merge_pipe_kernel<K><<<std::min((units + 1) / 2, pipe_grid_max), PIPE_THREADS, psmem, s>>>(bufs, nodes, c2n, cuts,
-                                                                                                 c0, units, err);
-                PS_LAUNCH_CHECK();
-            }
+            int rc2 = mr.stage(nlo, nhi, c0, c1, nsmall, &prof, stage);
             prof.end(ph);
             stage++;
-            return PS_OK;
+            return rc2;
         };
         for (int p = (int)NPOW - 1; p >= 1; --p) {
-            int rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p]);
+            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p]);
             if (rc) return rc;
         }
         for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
-            int rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i]);
+            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i]);
             if (rc) return rc;
         }
     }
@@ -575,6 +606,200 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     st->moves = -1;
     st->comparisons_valid = 0;
     st->moves_valid = 0;
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// N6 cross-shard merge (ps_shard_merge)
+struct ShardLayout {
+    uint64_t bounds, targets, err, lk, lv, tk, tv, nodes, c2n, cuts, chunks_max, total;
+};
+
+ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
+    ShardLayout L;
+    memset(&L, 0, sizeof(L));
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t o = off;
+        off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
+        return o;
+    };
+    L.chunks_max = 16 + cdiv(8 * slab_n, CHUNK_CAP / 2 / MAX_WAY);
+    L.bounds = take(2 * 2 * MAX_SHARDS * 8);
+    L.targets = take(16);
+    L.err = take(16);
+    L.lk = take(slab_n * kb);
+    L.lv = take(slab_n * 4);
+    L.tk = take(slab_n * kb);
+    L.tv = take(slab_n * 4);
+    L.nodes = take(4 * sizeof(Node));
+    L.c2n = take(L.chunks_max * 4);
+    L.cuts = take(L.chunks_max * 16);
+    L.total = off;
+    return L;
+}
+
+template <class K>
+int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* const* shard_vals,
+                     const int64_t* shard_n, int64_t t0, int64_t t1, K* out_k, int32_t* out_v, uint8_t* ws,
+                     size_t wsb, cudaStream_t s) {
+    if (G < 1 || G > (int32_t)MAX_SHARDS) return fail(PS_EINVAL, "nshards must be in 1..8");
+    if (!shard_keys || !shard_vals || !shard_n || !ws) return fail(PS_EINVAL, "NULL pointer argument");
+    ShardSet<K> S;
+    memset(&S, 0, sizeof(S));
+    S.G = (uint32_t)G;
+    uint64_t N = 0;
+    for (int32_t h = 0; h < G; ++h) {
+        if (shard_n[h] < 0) return fail(PS_EINVAL, "negative shard length");
+        S.k[h] = reinterpret_cast<const K*>(shard_keys[h]);
+        S.v[h] = shard_vals[h];
+        S.n[h] = (uint64_t)shard_n[h];
+        S.off[h] = N;
+        N += (uint64_t)shard_n[h];
+    }
+    if (t0 < 0 || t1 < t0 || (uint64_t)t1 > N) return fail(PS_EINVAL, "slab range outside [0, sum(shard_n)]");
+    const uint64_t slab = (uint64_t)(t1 - t0);
+    if (slab > ((uint64_t)1 << 31)) return fail(PS_EINVAL, "slab longer than 2^31");
+    const ShardLayout L = shard_layout(slab, sizeof(K));
+    if (wsb < L.total) return fail(PS_ENOMEM, "shard-merge workspace too small");
+    if (slab == 0) return PS_OK;
+    const uint32_t cap = chunk_cap<K>();
+
+    // ---- co-ranks of t0 and t1 by parallel bracketing ---------------------------
+    unsigned long long hb[2][2][MAX_SHARDS];
+    uint64_t tg[2] = {(uint64_t)t0, (uint64_t)t1};
+    for (int t = 0; t < 2; ++t)
+        for (uint32_t h = 0; h < MAX_SHARDS; ++h) {
+            uint64_t lo = 0, hi = 0;
+            if (h < (uint32_t)G) {
+                const uint64_t rest = N - S.n[h];
+                lo = tg[t] > rest ? tg[t] - rest : 0;
+                hi = std::min<uint64_t>(S.n[h], tg[t]);
+            }
+            hb[t][0][h] = lo;
+            hb[t][1][h] = hi;
+        }
+    unsigned long long* bounds = at<unsigned long long>(ws, L.bounds);
+    uint64_t* targets = at<uint64_t>(ws, L.targets);
+    PS_CUDA(cudaMemcpyAsync(bounds, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(targets, tg, sizeof(tg), cudaMemcpyHostToDevice, s));
+    uint64_t maxw = 1;
+    for (int32_t h = 0; h < G; ++h) maxw = std::max<uint64_t>(maxw, S.n[h]);
+    int rounds = 2;
+    for (uint64_t w = maxw; w > 1; w = w / (SEL_CANDIDATES + 1) + 1) rounds++;
+    const dim3 sgrid(cdiv((uint64_t)G * SEL_CANDIDATES, 8), 2);
+    for (int pass = 0; pass < 4; ++pass) {
+        for (int it = 0; it < rounds; ++it) {
+            shard_select_kernel<K><<<sgrid, 256, 0, s>>>(S, targets, bounds);
+            PS_LAUNCH_CHECK();
+        }
+        PS_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaStreamSynchronize(s));
+        bool conv = true;
+        for (int t = 0; t < 2; ++t)
+            for (int32_t h = 0; h < G; ++h) conv &= hb[t][0][h] == hb[t][1][h];
+        if (conv) break;
+        if (pass == 3) return fail(PS_EINVARIANT, "shard co-rank selection did not converge");
+    }
+    uint64_t run_len[MAX_SHARDS], tot = 0;
+    for (int32_t h = 0; h < G; ++h) {
+        if (hb[1][0][h] < hb[0][0][h]) return fail(PS_EINVARIANT, "shard co-ranks not monotone");
+        run_len[h] = hb[1][0][h] - hb[0][0][h];
+        tot += run_len[h];
+    }
+    if (tot != slab) return fail(PS_EINVARIANT, "shard co-ranks do not sum to the slab");
+
+    // ---- gather the windows (peer loads over NVLink) into Lk/Lv ------------------
+    K* lk = at<K>(ws, L.lk);
+    int32_t* lv = at<int32_t>(ws, L.lv);
+    shard_gather_kernel<K><<<(unsigned)std::min<uint64_t>(cdiv(slab, 256), 148 * 16), 256, 0, s>>>(
+        S, bounds, bounds + 2 * MAX_SHARDS, lk, lv, slab);
+    PS_LAUNCH_CHECK();
+
+    // ---- local merge of the nonempty windows -------------------------------------
+    std::vector<uint32_t> runs_off;  // boundaries of nonempty runs in L
+    uint64_t acc = 0;
+    for (int32_t h = 0; h < G; ++h) {
+        if (run_len[h]) runs_off.push_back((uint32_t)acc);
+        acc += run_len[h];
+    }
+    runs_off.push_back((uint32_t)acc);
+    const uint32_t R = (uint32_t)runs_off.size() - 1;
+    if (R <= 1) {
+        PS_CUDA(cudaMemcpyAsync(out_k, lk, slab * sizeof(K), cudaMemcpyDeviceToDevice, s));
+        PS_CUDA(cudaMemcpyAsync(out_v, lv, slab * 4, cudaMemcpyDeviceToDevice, s));
+        PS_CUDA(cudaStreamSynchronize(s));
+        return PS_OK;
+    }
+    auto make_node = [&](const uint32_t* pos, uint32_t arity, uint32_t parity) {
+        Node nd;
+        memset(&nd, 0, sizeof(nd));
+        for (uint32_t a = 0; a <= arity; ++a) nd.pos[a] = pos[a];
+        nd.arity = (uint8_t)arity;
+        nd.parity = (uint8_t)parity;
+        nd.probe = 0;
+        const uint32_t size = pos[arity] - pos[0];
+        uint32_t nch = size <= SMALL_NODE ? 0 : 1;
+        if (size > cap)
+            for (uint32_t a = 0; a < arity; ++a) nch += (pos[a + 1] - pos[a] - 1) / (cap / arity);
+        nd.nchunks = nch;
+        return nd;
+    };
+    std::vector<std::vector<Node>> levels;
+    if (R <= MAX_WAY) {
+        levels.push_back({make_node(runs_off.data(), R, 0)});
+    } else {
+        const uint32_t left = (R + 1) / 2;
+        levels.push_back({make_node(runs_off.data(), left, 1), make_node(runs_off.data() + left, R - left, 1)});
+        const uint32_t p2[3] = {runs_off[0], runs_off[left], runs_off[R]};
+        levels.push_back({make_node(p2, 2, 0)});
+    }
+    Node* d_nodes = at<Node>(ws, L.nodes);
+    uint32_t* d_c2n = at<uint32_t>(ws, L.c2n);
+    uint4* d_cuts = at<uint4>(ws, L.cuts);
+    uint32_t* d_err = at<uint32_t>(ws, L.err);
+    PS_CUDA(cudaMemsetAsync(d_err, 0, 4, s));
+    for (size_t lvl = 0; lvl < levels.size(); ++lvl) {
+        std::vector<Node>& nds = levels[lvl];
+        std::vector<uint32_t> c2n;
+        uint32_t nsmall = 0;
+        for (uint32_t i = 0; i < nds.size(); ++i) {
+            nds[i].chunk_base = (uint32_t)c2n.size();
+            for (uint32_t c = 0; c < nds[i].nchunks; ++c) c2n.push_back(i);
+            nsmall += nds[i].nchunks == 0;
+        }
+        if (c2n.size() > L.chunks_max) return fail(PS_ENOMEM, "shard-merge chunk table too small");
+        PS_CUDA(cudaMemcpyAsync(d_nodes, nds.data(), nds.size() * sizeof(Node), cudaMemcpyHostToDevice, s));
+        if (!c2n.empty())
+            PS_CUDA(cudaMemcpyAsync(d_c2n, c2n.data(), c2n.size() * 4, cudaMemcpyHostToDevice, s));
+        Bufs<K> b;
+        if (levels.size() == 1) {  // L -> out
+            b.k[0] = out_k;
+            b.v[0] = out_v;
+            b.k[1] = lk;
+            b.v[1] = lv;
+        } else if (lvl == 0) {  // L -> T
+            b.k[0] = lk;
+            b.v[0] = lv;
+            b.k[1] = at<K>(ws, L.tk);
+            b.v[1] = at<int32_t>(ws, L.tv);
+        } else {  // T -> out
+            b.k[0] = out_k;
+            b.v[0] = out_v;
+            b.k[1] = at<K>(ws, L.tk);
+            b.v[1] = at<int32_t>(ws, L.tv);
+        }
+        MergeRunner<K> mr;
+        int rc = mr.init(b, d_nodes, d_c2n, d_cuts, d_err, s);
+        if (rc) return rc;
+        rc = mr.stage(0, (uint32_t)nds.size(), 0, (uint32_t)c2n.size(), nsmall, nullptr, (int)lvl);
+        if (rc) return rc;
+        PS_CUDA(cudaStreamSynchronize(s));  // host node/chunk tables are reused by the next level
+    }
+    uint32_t herr = 0;
+    PS_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    if (herr) return fail(PS_EINVARIANT, "shard merge invariant violated (flags " + std::to_string(herr) + ")");
     return PS_OK;
 }
 
@@ -765,14 +990,33 @@ int64_t ps_run_stack_capacity(int64_t k, int64_t n) {
 }
 
 size_t ps_shard_merge_workspace_size(int32_t nshards, int64_t slab_n) {
-    (void)nshards;
-    (void)slab_n;
-    return 0;
+    if (nshards < 1 || nshards > (int32_t)MAX_SHARDS || slab_n < 0) return 0;
+    return (size_t)shard_layout((uint64_t)slab_n, 8).total;
 }
 
-int ps_shard_merge(int32_t, int32_t, const void* const*, const int32_t* const*, const int64_t*, int64_t, int64_t,
-                   void*, int32_t*, void*, size_t, void*) {
-    return fail(PS_EINVAL, "ps_shard_merge: not implemented yet");
+int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys, const int32_t* const* shard_vals,
+                   const int64_t* shard_n, int64_t out_begin, int64_t out_end, void* out_keys, int32_t* out_vals,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+    switch (dtype) {
+        case PS_INT32:
+            return shard_merge_impl<int32_t>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
+                                             (int32_t*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
+                                             (cudaStream_t)stream);
+        case PS_INT64:
+            return shard_merge_impl<int64_t>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
+                                             (int64_t*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
+                                             (cudaStream_t)stream);
+        case PS_FLOAT32:
+            return shard_merge_impl<float>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
+                                           (float*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
+                                           (cudaStream_t)stream);
+        case PS_FLOAT64:
+            return shard_merge_impl<double>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
+                                            (double*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
+                                            (cudaStream_t)stream);
+        default:
+            return fail(PS_EINVAL, "unsupported dtype " + std::to_string(dtype));
+    }
 }
 
 }  // extern "C"

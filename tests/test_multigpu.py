@@ -1,0 +1,205 @@
+"""Multi-GPU mode.
+
+CPU tests cover the host logic: the slab plan exchanged over a world-size-2
+gloo group, and a pure-Python restatement of the parallel bracketing co-rank
+selection that ps_shard_merge runs on the device (shard_select_kernel).
+GPU tests run ps_shard_merge with G shards emulated on one device, and a
+two-process sort_distributed over CUDA IPC on one GPU (gloo for plumbing).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2209_06909_b200 import multigpu
+
+SEL_CANDIDATES = 64
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _plan_worker(rank, world, port, sizes, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    got = [None] * world
+    dist.all_gather_object(got, sizes[rank])
+    q.put((rank, multigpu.plan(got, rank)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_slab_plan_over_gloo_world2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    sizes = [1000, 777]
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, 2, port, sizes, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0]["offsets"] == [0, 1000] and res[1]["total"] == 1777
+    assert res[0]["slab"] == (0, 888) and res[1]["slab"] == (888, 1777)
+
+
+@pytest.mark.parametrize("total,world", [(0, 1), (10, 3), (2**31, 8), (12345, 7)])
+def test_slabs_partition_the_ranks(total, world):
+    slabs = [multigpu.slab_bounds(total, world, g) for g in range(world)]
+    assert slabs[0][0] == 0 and slabs[-1][1] == total
+    assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+
+
+def bracket_select(shards, t, rounds=None):
+    """Restatement of shard_select_kernel: co-rank of global rank t in the
+    stable merge of sorted shards (order (key, shard, position))."""
+    G = len(shards)
+    n = [len(s) for s in shards]
+    N = sum(n)
+    lo = [max(0, t - (N - n[h])) for h in range(G)]
+    hi = [min(n[h], t) for h in range(G)]
+    for _ in range(rounds or 64):
+        if lo == hi:
+            break
+        cur_lo, cur_hi = list(lo), list(hi)
+        for g in range(G):
+            w = cur_hi[g] - cur_lo[g]
+            if w <= 0:
+                continue
+            for ci in range(SEL_CANDIDATES):
+                p = cur_lo[g] + (w * (ci + 1)) // (SEL_CANDIDATES + 1)
+                if p >= cur_hi[g]:
+                    continue
+                y = shards[g][p]
+                r = []
+                for h in range(G):
+                    if h == g:
+                        r.append(p)
+                        continue
+                    side = "right" if h < g else "left"  # <= for earlier shards, < for later
+                    pos = int(np.searchsorted(shards[h][cur_lo[h]:cur_hi[h]], y, side=side)) + cur_lo[h]
+                    r.append(pos)
+                R = sum(r)
+                for h in range(G):
+                    if R < t:
+                        lo[h] = max(lo[h], p + 1 if h == g else r[h])
+                    else:
+                        hi[h] = min(hi[h], p if h == g else r[h])
+    assert lo == hi
+    return lo
+
+
+def test_bracketing_selection_matches_stable_merge():
+    rng = np.random.default_rng(4)
+    for trial in range(60):
+        G = int(rng.integers(1, 9))
+        shards = []
+        for _ in range(G):
+            m = int(rng.integers(0, 400))
+            hi = int(rng.choice([3, 50, 10**6]))
+            shards.append(np.sort(rng.integers(0, hi, size=m)))
+        allk = np.concatenate(shards) if shards else np.array([])
+        shard_id = np.concatenate([np.full(len(s), h) for h, s in enumerate(shards)])
+        order = np.lexsort((shard_id, allk))  # stable (key, shard, position)
+        N = len(allk)
+        for t in sorted(set([0, N, N // 2, int(rng.integers(0, N + 1))])):
+            c = bracket_select(shards, t)
+            first_t = shard_id[order[:t]]
+            expect = [int(np.sum(first_t == h)) for h in range(G)]
+            assert c == expect, (trial, t)
+
+
+# --------------------------------------------------------------------- GPU
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("kind", ["cfg2", "dups", "disjoint"])
+def test_shard_merge_emulated_on_one_gpu(G, kind):
+    from paper_2209_06909_b200 import SortConfig, stable_sort_with, workloads
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(G * 7 + len(kind))
+    n = 200_000 + int(rng.integers(0, 1000))
+    if kind == "cfg2":
+        keys = workloads.cfg2(n=n, seed=G)
+    elif kind == "dups":
+        keys = rng.integers(0, 5, size=n).astype(np.int32)
+    else:
+        keys = np.arange(n, dtype=np.int32)[::-1].copy()  # each shard's keys disjoint from the others
+    cuts = np.sort(rng.integers(0, n, size=G - 1)) if G > 1 else np.array([], dtype=np.int64)
+    bounds = [0] + cuts.tolist() + [n]
+    sk, sv = [], []
+    for g in range(G):
+        a, b = bounds[g], bounds[g + 1]
+        k = torch.from_numpy(keys[a:b].copy()).to(dev)
+        v = torch.arange(a, b, dtype=torch.int32, device=dev)
+        if k.numel():
+            stable_sort_with(k, SortConfig(), values=v)
+        sk.append(k)
+        sv.append(v)
+    out_k, out_v = [], []
+    for g in range(G):
+        t0, t1 = multigpu.slab_bounds(n, G, g)
+        k, v = multigpu.shard_merge(sk, sv, t0, t1)
+        out_k.append(k.cpu().numpy())
+        out_v.append(v.cpu().numpy())
+    perm = np.argsort(keys, kind="stable")
+    assert np.array_equal(np.concatenate(out_v), perm)
+    assert np.array_equal(np.concatenate(out_k), keys[perm])
+
+
+def _dist_worker(rank, world, port, n, q):
+    import torch.distributed as dist
+
+    from paper_2209_06909_b200 import workloads
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)  # both ranks share the single test GPU (host barriers only)
+    keys = workloads.cfg5(n=n, seed=1)
+    a, b = multigpu.slab_bounds(n, world, rank)
+    shard = torch.from_numpy(keys[a:b].copy()).cuda()
+    k, v = multigpu.sort_distributed(shard)
+    q.put((rank, k.cpu().numpy(), v.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sort_distributed_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+
+    from paper_2209_06909_b200 import workloads
+
+    n = 300_000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (k, v)) for r, k, v in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    keys = workloads.cfg5(n=n, seed=1)
+    perm = np.argsort(keys, kind="stable")
+    assert np.array_equal(np.concatenate([res[0][1], res[1][1]]), perm)
+    assert np.array_equal(np.concatenate([res[0][0], res[1][0]]).view(np.uint32), keys[perm].view(np.uint32))
