@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--n", type=int, default=None, help="override the config size (default: BASELINE size)")
+    ap.add_argument("--keys", dest="n", type=int, default=None,
+                    help="override the config size (default: the BASELINE size)")
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -338,6 +339,114 @@ def run_e2e(args, torch, dist, dev, keys_np, cfg, world, expect_keys):
     }
 
 
+def run_distributed(args):
+    """N > 1: the global input is world x n keys; rank g owns shard g (the
+    config recipe with seed + g).  One step = local sort of the shard plus the
+    NVLink cross-shard merge of this rank's slab (paper_2209_06909_b200.multigpu
+    .sort_distributed).  Weak scaling; time = max over ranks of the device
+    time between barriers."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_06909_b200 import SortConfig, _lib, multigpu, workloads
+
+    rank, local, world = dist_env()
+    backend = os.environ.get("PS_BENCH_BACKEND", "nccl")  # gloo: test mode, ranks may share a GPU
+    dist.init_process_group(backend)
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    dev = torch.device("cuda", torch.cuda.current_device())
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
+    lib = _lib.load()
+    n = args.n or workloads.FULL_N[args.config]
+    keys_np = workloads.generate(args.config, n=n, seed=args.seed + rank)
+    cfg = SortConfig(k=args.k, variant="4way" if args.k == 4 else "2way")
+    src = torch.from_numpy(keys_np).to(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    work = torch.empty_like(src)
+
+    def step():
+        work.copy_(src)
+        flush.fill_(1)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        out = multigpu.sort_distributed(work, cfg)
+        t1.record()
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1), out
+
+    for _ in range(max(args.warmup, 1)):
+        _, out = step()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    launches0 = lib.ps_launch_count()
+    total = 0.0
+    for _ in range(args.steps):
+        ms, out = step()
+        total += ms
+    launches = lib.ps_launch_count() - launches0
+    clocks = sampler.stop()
+    t = torch.tensor([total], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    # e2e: pinned H2D of the shard, distributed sort, D2H of the slab (keys + global indices)
+    h_in = torch.from_numpy(keys_np).pin_memory()
+    e_total = 0.0
+    d2h = 0
+    for i in range(max(args.warmup, 1) + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        work.copy_(h_in, non_blocking=True)
+        ek, ev = multigpu.sort_distributed(work, cfg)
+        hk = ek.to("cpu", non_blocking=True)
+        hv = ev.to("cpu", non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= max(args.warmup, 1):
+            e_total += a.elapsed_time(b)
+        d2h = hk.numel() * hk.element_size() + hv.numel() * 4
+    te = torch.tensor([e_total], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e_total = float(te.item())
+    e2e = {"value": world * n * args.steps / (e_total / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(keys_np.nbytes), "d2h_bytes_per_step": int(d2h),
+           "ms_per_step": e_total / args.steps,
+           "api": "paper_2209_06909_b200.multigpu.sort_distributed"}
+    # certify this rank's slab: sorted, and its boundary with the next slab ordered
+    k, v = out
+    assert bool((k[:-1] <= k[1:]).all()), "slab not sorted"
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": world * n * args.steps / (total / 1e3),
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": total / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": str(keys_np.dtype),
+            "data": "synthetic (seeded %s recipe per shard, SURVEY 8d)" % args.config,
+            "config": config_dict(args, n * world, {
+                "key_dtype": str(keys_np.dtype),
+                "parallelism": "%d shards: local sort + NVLink P2P cross-shard merge (no NCCL on data)" % world}),
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -487,6 +596,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if dist_env()[2] > 1:
+        return run_distributed(args)
     return run_ours(args)
 
 
