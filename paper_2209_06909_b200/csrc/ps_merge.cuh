@@ -165,6 +165,10 @@ PS_DEV void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, ui
 #define PS_CONSUMERS 256
 #endif
 constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
+#ifndef PS_SLOTS
+#define PS_SLOTS 2
+#endif
+constexpr uint32_t PIPE_SLOTS = PS_SLOTS;  // input slots per CTA (TMA multi-buffering)
 PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(PIPE_CONSUMERS) : "memory"); }
 
 // ---------------------------------------------------------------------------
@@ -262,7 +266,11 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
 
 // bank padding of record arrays: two records per 16, which keeps every
 // 4-record group 16-byte aligned for the vector store phase
+#ifdef PS_NOPAD
+PS_DEV uint32_t padr(uint32_t o) { return o; }
+#else
 PS_DEV uint32_t padr(uint32_t o) { return o + ((o >> 4) << 1); }
+#endif
 
 template <class K>
 struct PipeLayout {
@@ -286,7 +294,7 @@ struct PipeDesc {
 
 template <class K>
 size_t merge_pipe_smem_bytes() {
-    return 2 * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::SCRATCH + 2 * sizeof(PipeDesc) + 64;
+    return PIPE_SLOTS * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::SCRATCH + PIPE_SLOTS * sizeof(PipeDesc) + 64;
 }
 
 // Merge-path cursors.  Every consumer thread advances two independent cursors
@@ -299,8 +307,10 @@ struct WinCur {
     const int32_t *av, *bv;
     uint32_t la, lb, i, j, o, oe, base;
     K a, b;
-    PS_DEV uint32_t ca(uint32_t x) const { return x < la ? x : (la ? la - 1 : 0); }
-    PS_DEV uint32_t cb(uint32_t x) const { return x < lb ? x : (lb ? lb - 1 : 0); }
+    // one-past-the-end reads stay inside shared memory (the next window, the
+    // slot's alignment slack or the padded capacity), so no clamping is needed
+    PS_DEV uint32_t ca(uint32_t x) const { return x; }
+    PS_DEV uint32_t cb(uint32_t x) const { return x; }
     PS_DEV K keyA(uint32_t x) const { return ak[ca(x)]; }
     PS_DEV K keyB(uint32_t x) const { return bk[cb(x)]; }
     PS_DEV void heads() {
@@ -328,8 +338,8 @@ struct RecCur {
     const Rec<K>* r;
     uint32_t offa, offb, la, lb, i, j, o, oe, base;
     Rec<K> a, b;
-    PS_DEV uint32_t ia(uint32_t x) const { return padr(offa + (x < la ? x : (la ? la - 1 : 0))); }
-    PS_DEV uint32_t ib(uint32_t x) const { return padr(offb + (x < lb ? x : (lb ? lb - 1 : 0))); }
+    PS_DEV uint32_t ia(uint32_t x) const { return padr(offa + x); }
+    PS_DEV uint32_t ib(uint32_t x) const { return padr(offb + x); }
     PS_DEV K keyA(uint32_t x) const { return r[ia(x)].k; }
     PS_DEV K keyB(uint32_t x) const { return r[ib(x)].k; }
     PS_DEV void heads() {
@@ -487,17 +497,17 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                                                                   uint32_t nchunks, uint32_t* err) {
     using LY = PipeLayout<K>;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* scratch = smem + 2 * LY::SLOT;
+    uint8_t* scratch = smem + PIPE_SLOTS * LY::SLOT;
     PipeDesc* desc = reinterpret_cast<PipeDesc*>(scratch + LY::SCRATCH);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(desc + 2);
-    uint64_t* full = bars;       // [2]
-    uint64_t* empty = bars + 2;  // [2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(desc + PIPE_SLOTS);
+    uint64_t* full = bars;                // [PIPE_SLOTS]
+    uint64_t* empty = bars + PIPE_SLOTS;  // [PIPE_SLOTS]
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], PIPE_CONSUMERS / 32);
-        mbar_init(&empty[1], PIPE_CONSUMERS / 32);
+        for (uint32_t sl = 0; sl < PIPE_SLOTS; ++sl) {
+            mbar_init(&full[sl], 1);
+            mbar_init(&empty[sl], PIPE_CONSUMERS / 32);
+        }
         mbar_fence_init();
     }
     __syncthreads();
@@ -554,8 +564,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 const uint32_t w = __shfl_sync(PS_FULL, (uint32_t)nd.arity, u);
                 const uint32_t par = __shfl_sync(PS_FULL, (uint32_t)nd.parity, u);
                 // ---- stage the unit into slot (unit & 1) ----
-                const uint32_t slot = unit & 1;
-                if (unit >= 2) mbar_wait(&empty[slot], ((unit >> 1) - 1) & 1);
+                const uint32_t slot = unit % PIPE_SLOTS;
+                if (unit >= PIPE_SLOTS) mbar_wait(&empty[slot], ((unit / PIPE_SLOTS) - 1) & 1);
                 PT_MARK(1)
                 uint8_t* sbase = smem + slot * LY::SLOT;
                 const uint32_t sv4[4] = {sx, sy, sz, sw};
@@ -634,8 +644,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             c += nvalid;
         }
         // termination marker
-        const uint32_t slot = unit & 1;
-        if (unit >= 2) mbar_wait(&empty[slot], ((unit >> 1) - 1) & 1);
+        const uint32_t slot = unit % PIPE_SLOTS;
+        if (unit >= PIPE_SLOTS) mbar_wait(&empty[slot], ((unit / PIPE_SLOTS) - 1) & 1);
         if (lane == 0) {
             desc[slot].done = 1;
             mbar_arrive(&full[slot]);
@@ -649,8 +659,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     Rec<K>* const xr = reinterpret_cast<Rec<K>*>(scratch);
     PT_START(ctid == 0)
     for (uint32_t i = 0;; ++i) {
-        const uint32_t slot = i & 1;
-        mbar_wait(&full[slot], (i >> 1) & 1);
+        const uint32_t slot = i % PIPE_SLOTS;
+        mbar_wait(&full[slot], (i / PIPE_SLOTS) & 1);
         PT_MARK(4)
         const PipeDesc& d = desc[slot];
         if (d.done) break;

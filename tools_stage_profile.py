@@ -28,3 +28,6 @@ for e in prof:
     print('%-15s stage %3d nodes %8d chunks %8d  %8.3f ms  %9.1f MB  %7.0f GB/s' % (
         e['kind'], e['stage'], e['nodes'], e['chunks'], e['ms'], e['bytes'] / 1e6, gbs))
 print('sum of entries %.3f ms' % tot)
+import numpy as np
+ok = np.array_equal(perm.cpu().numpy(), np.argsort(keys_np, kind='stable'))
+print('parity vs numpy stable argsort:', 'OK' if ok else 'MISMATCH')
