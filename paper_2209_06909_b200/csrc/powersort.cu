@@ -143,7 +143,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.ngroups = std::max<uint64_t>(1, cdiv(n, GROUP));
     L.ntiles = L.ngroups * TILES_PER_GROUP;
     // total chunks <= nodes + merge_cost / (CHUNK_CAP / MAX_WAY); merge_cost <= 64 n
-    L.chunks_max = L.rmax + cdiv(64 * n, CHUNK_CAP / 2 / MAX_WAY) + 16;
+    L.chunks_max = L.rmax + cdiv(64 * n, (CHUNK_CAP / 2 - 16) / MAX_WAY) + 16;
     // min tree levels over P (size rmax + 1)
     uint64_t s = align_up(L.rmax + 1, 32);
     L.nlev = 0;
@@ -376,7 +376,7 @@ struct MergeRunner {
                 if (prof) prof->end(pp);
             }
             const uint32_t units = c1 - c0;
-            merge_pipe_kernel<K><<<std::min((units + 1) / 2, pipe_grid_max), PIPE_THREADS, psmem, s>>>(
+            merge_pipe_kernel<K><<<std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s>>>(
                 bufs, nodes, c2n, cuts, c0, units, err);
             PS_LAUNCH_CHECK();
         }
@@ -478,6 +478,12 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         uint64_t* tile_tab = at<uint64_t>(ws, L.tile_tab);
         uint64_t* gtab = at<uint64_t>(ws, L.lvl_tab[0]);
         const size_t smem = (size_t)TILES_PER_GROUP * M1 * 8;
+        const size_t fan_smem = (size_t)TSCAN_FAN * M1 * 8;  // up to 64.3 KB at m = 256
+        if (fan_smem > 48 * 1024) {
+            PS_CUDA(cudaFuncSetAttribute(rd_compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
+            PS_CUDA(cudaFuncSetAttribute(rd_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
+            PS_CUDA(cudaFuncSetAttribute(rd_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
+        }
         rd_tables_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
                                                    err);
         PS_LAUNCH_CHECK();
@@ -486,7 +492,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         for (uint64_t l = 0; l < L.tab_levels; ++l) {
             spans[l] = span;
             if (l + 1 < L.tab_levels) {
-                rd_compose_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
+                rd_compose_kernel<<<(unsigned)L.lvlP[l + 1], 32, fan_smem, s>>>(
                     at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
                     at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
                 PS_LAUNCH_CHECK();
@@ -494,16 +500,16 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             }
         }
         const uint64_t top = L.tab_levels - 1;
-        rd_top_kernel<<<1, 32, 0, s>>>(at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
+        rd_top_kernel<<<1, 32, fan_smem, s>>>(at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
                                        (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
         PS_LAUNCH_CHECK();
         for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
-            rd_down_kernel<<<(unsigned)L.lvlP[l + 1], 32, TSCAN_FAN * M1 * 8, s>>>(
+            rd_down_kernel<<<(unsigned)L.lvlP[l + 1], 32, fan_smem, s>>>(
                 at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
                 at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
             PS_LAUNCH_CHECK();
         }
-        rd_emit_kernel<<<ngroups, 256, 0, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
+        rd_emit_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
                                                at<uint64_t>(ws, L.lvl_ent[0]), b, nat, err);
         PS_LAUNCH_CHECK();
     } else {
@@ -526,7 +532,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     const int ph_tree = prof.begin(1, -1, 0, 0, 0);
     if (r >= 2) {
         int rc = build_tree(ws, L, r, (uint64_t)n, cfg.k, cfg.strict_merge_down, slack_mode_of(cfg.variant), leafpar,
-                            info, s, chunk_cap<K>());
+                            info, s, cut_cap<K>());
         if (rc) return rc;
         nnodes = info.s.nmain + info.s.nspine_nodes;
     } else {
@@ -624,7 +630,7 @@ ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
         off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
         return o;
     };
-    L.chunks_max = 16 + cdiv(8 * slab_n, CHUNK_CAP / 2 / MAX_WAY);
+    L.chunks_max = 16 + cdiv(8 * slab_n, (CHUNK_CAP / 2 - 16) / MAX_WAY);
     L.bounds = take(2 * 2 * MAX_SHARDS * 8);
     L.targets = take(16);
     L.err = take(16);
@@ -663,7 +669,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
     const ShardLayout L = shard_layout(slab, sizeof(K));
     if (wsb < L.total) return fail(PS_ENOMEM, "shard-merge workspace too small");
     if (slab == 0) return PS_OK;
-    const uint32_t cap = chunk_cap<K>();
+    const uint32_t cap = cut_cap<K>();
 
     // ---- co-ranks of t0 and t1 by parallel bracketing ---------------------------
     unsigned long long hb[2][2][MAX_SHARDS];
@@ -1027,9 +1033,9 @@ int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys
 // pass 2, store, units).
 extern "C" int ps_debug_pipe_timing(unsigned long long* out, int reset) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, ps::g_pipe_tim, 16 * sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out, ps::g_pipe_tim, 40 * sizeof(unsigned long long));
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[40] = {0};
         cudaMemcpyToSymbol(ps::g_pipe_tim, z, sizeof(z));
     }
     return PS_OK;

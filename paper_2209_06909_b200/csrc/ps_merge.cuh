@@ -30,6 +30,28 @@
 
 namespace ps {
 
+// consumer threads per merge_pipe_kernel CTA
+#ifndef PS_CONSUMERS
+#define PS_CONSUMERS 256
+#endif
+constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
+
+// Consumer thread t produces the VT outputs [VT*t, VT*t + VT) of every merge
+// pass.  Record arrays get one pad record per VT, so the k-th output of all
+// lanes lands at (VT+1)*t + k: 2 wavefronts per warp store (bank-conflict free).
+template <class K>
+PS_DEV __host__ constexpr uint32_t pipe_vt() {
+    return chunk_cap<K>() / PIPE_CONSUMERS;
+}
+// Cut spacing budget: units hold <= CAP - VT records, so pass 1 can start Y
+// at a VT-aligned offset (no thread straddles X and Y) within NC threads.
+template <class K>
+PS_DEV __host__ constexpr uint32_t cut_cap() {
+    return chunk_cap<K>() - pipe_vt<K>();
+}
+static_assert((pipe_vt<int32_t>() & (pipe_vt<int32_t>() - 1)) == 0, "VT must be a power of two");
+static_assert((pipe_vt<int64_t>() & (pipe_vt<int64_t>() - 1)) == 0, "VT must be a power of two");
+
 // # of a[0..len) that are <= x (LE) or < x (!LE)
 template <class K, bool LE>
 PS_DEV uint32_t count_pred(const K* __restrict__ a, uint32_t len, K x) {
@@ -77,6 +99,50 @@ PS_DEV uint32_t warp_count_pred(const K* __restrict__ a, uint32_t len, K x) {
     return lo + __popc(__ballot_sync(PS_FULL, p));
 }
 
+// Up to three counts at once (one per other run): lanes 10g..10g+9 run an
+// 11-ary search in array g, all groups in the same rounds (~8 rounds for 2^22
+// elements instead of three sequential searches).  le[g]: count <= x, else < x.
+template <class K>
+PS_DEV void warp_count3(const K* r0, const K* r1, const K* r2, uint32_t l0, uint32_t l1, uint32_t l2, bool le0,
+                        bool le1, bool le2, uint32_t nsearch, K x, uint32_t* out) {
+    const uint32_t lane = lane_id();
+    const uint32_t grp = lane / 10, sub = lane % 10;
+    const bool active = grp < nsearch;
+    const K* run = grp == 0 ? r0 : (grp == 1 ? r1 : r2);
+    const bool le = grp == 0 ? le0 : (grp == 1 ? le1 : le2);
+    uint32_t lo = 0, hi = active ? (grp == 0 ? l0 : (grp == 1 ? l1 : l2)) : 0;
+    const uint32_t gshift = grp < 3 ? grp * 10 : 0;
+    while (__any_sync(PS_FULL, hi - lo > 10)) {
+        const uint32_t span = hi - lo;
+        const bool probing = span > 10;
+        bool p = false;
+        if (probing) {
+            const uint32_t probe = lo + (uint32_t)(((uint64_t)span * (sub + 1)) / 11);
+            const K y = run[probe];
+            p = le ? !(x < y) : (y < x);
+        }
+        const uint32_t bal = __ballot_sync(PS_FULL, p);
+        if (probing) {
+            const uint32_t c = __popc((bal >> gshift) & 0x3FFu);
+            const uint32_t nlo = c ? lo + (uint32_t)(((uint64_t)span * c) / 11) + 1 : lo;
+            const uint32_t nhi = c < 10 ? lo + (uint32_t)(((uint64_t)span * (c + 1)) / 11) : hi;
+            lo = nlo;
+            hi = nhi;
+        }
+    }
+    const uint32_t idx = lo + sub;
+    bool p = false;
+    if (active && idx < hi) {
+        const K y = run[idx];
+        p = le ? !(x < y) : (y < x);
+    }
+    const uint32_t bal = __ballot_sync(PS_FULL, p);
+    const uint32_t res = lo + __popc((bal >> gshift) & 0x3FFu);
+    out[0] = __shfl_sync(PS_FULL, res, 0);
+    out[1] = __shfl_sync(PS_FULL, res, 10);
+    out[2] = __shfl_sync(PS_FULL, res, 20);
+}
+
 // Partition: one warp per chunk of the stage [c0, c1); the first chunk of each
 // node gets the zero cut.
 template <class K>
@@ -94,7 +160,7 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     }
     q -= 1;
     const uint32_t w = nd.arity;
-    const uint32_t S = chunk_cap<K>() / w;
+    const uint32_t S = cut_cap<K>() / w;
     const K* src = bufs.k[nd.parity ^ 1];
     uint32_t L[4];
 #pragma unroll
@@ -107,18 +173,20 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     }
     const uint32_t j = q + 1;
     const K y = src[(uint64_t)nd.pos[a] + (uint64_t)j * S];
+    // the other runs, in order: o = index among them, run bb = o + (o >= a)
+    const uint32_t b0 = a == 0 ? 1 : 0, b1 = a <= 1 ? 2 : 1, b2 = a == 3 ? 2 : 3;
+    uint32_t got[3];
+    warp_count3<K>(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
+                   b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < a, b1 < a, b2 < a, w - 1, y, got);
     uint32_t rk[4] = {0, 0, 0, 0};
+    rk[a] = j * S;
     uint32_t mm = j - 1;
 #pragma unroll
-    for (uint32_t bb = 0; bb < 4; ++bb) {
-        if (bb >= w) break;
-        if (bb == a) {
-            rk[bb] = j * S;
-            continue;
-        }
-        const K* run = src + nd.pos[bb];
-        rk[bb] = bb < a ? warp_count_pred<K, true>(run, L[bb], y) : warp_count_pred<K, false>(run, L[bb], y);
-        mm += rk[bb] ? (rk[bb] - 1) / S : 0;
+    for (uint32_t o = 0; o < 3; ++o) {
+        if (o + 1 >= w) break;
+        const uint32_t bb = o + (o >= a ? 1 : 0);
+        rk[bb] = got[o];
+        mm += got[o] ? (got[o] - 1) / S : 0;
     }
     if (lane == 0) cuts[nd.chunk_base + 1 + mm] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
 }
@@ -161,10 +229,6 @@ PS_DEV void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, ui
         : "memory");
 }
 // named barrier 1 over the consumer warps only
-#ifndef PS_CONSUMERS
-#define PS_CONSUMERS 256
-#endif
-constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
 #ifndef PS_SLOTS
 #define PS_SLOTS 2
 #endif
@@ -234,7 +298,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
 // ---------------------------------------------------------------------------
 // Optional clock64 phase counters of the pipe kernel (build with -DPS_PIPE_TIMING)
 #ifdef PS_PIPE_TIMING
-__device__ unsigned long long g_pipe_tim[16];
+__device__ unsigned long long g_pipe_tim[40];
 #define PT_START(on) long long _pt0 = clock64(); const bool _pton = (on);
 #define PT_MARK(idx)                                                         \
     if (_pton) {                                                             \
@@ -244,7 +308,13 @@ __device__ unsigned long long g_pipe_tim[16];
     }
 #define PT_COUNT(idx) \
     if (_pton) atomicAdd(&g_pipe_tim[idx], 1ull);
+// per-consumer-warp work time since the unit started (before the barrier)
+#define PT_USTART long long _ptu = clock64();
+#define PT_WARP(idx) \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_pipe_tim[(idx) + ((threadIdx.x - 32) >> 5)], clock64() - _ptu);
 #else
+#define PT_USTART
+#define PT_WARP(idx)
 #define PT_START(on)
 #define PT_MARK(idx)
 #define PT_COUNT(idx)
@@ -264,18 +334,18 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
     int32_t v;
 };
 
-// bank padding of record arrays: two records per 16, which keeps every
-// 4-record group 16-byte aligned for the vector store phase
 #ifdef PS_NOPAD
+template <class K>
 PS_DEV uint32_t padr(uint32_t o) { return o; }
 #else
-PS_DEV uint32_t padr(uint32_t o) { return o + ((o >> 4) << 1); }
+template <class K>
+PS_DEV uint32_t padr(uint32_t o) { return o + o / pipe_vt<K>(); }
 #endif
 
 template <class K>
 struct PipeLayout {
     static constexpr uint32_t CAP = chunk_cap<K>();
-    static constexpr uint32_t PADN = CAP + CAP / 8 + 16;  // padded record capacity
+    static constexpr uint32_t PADN = CAP + CAP / pipe_vt<K>() + 16;  // padded record capacity
     static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
     // slot = TMA landing zone of the k key windows + k value windows (SoA, 16B
     // alignment slack each), and afterwards the padded records of the last pass
@@ -297,9 +367,7 @@ size_t merge_pipe_smem_bytes() {
     return PIPE_SLOTS * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::SCRATCH + PIPE_SLOTS * sizeof(PipeDesc) + 64;
 }
 
-// Merge-path cursors.  Every consumer thread advances two independent cursors
-// in lockstep, so two dependency chains (search and serial merge) overlap.
-// WinCur merges two TMA-landed SoA windows, RecCur two padded record runs;
+// Merge-path cursors.  WinCur merges two TMA-landed SoA windows, RecCur two padded record runs;
 // ties always go to the A side.  Outputs go to padded records out[base + o].
 template <class K>
 struct WinCur {
@@ -323,7 +391,7 @@ struct WinCur {
         Rec<K> r;
         r.k = takeA ? a : b;
         r.v = *(takeA ? av + i : bv + j);
-        out[padr(base + o)] = r;
+        out[padr<K>(base + o)] = r;
         ++o;
         i += takeA;
         j += !takeA;
@@ -338,8 +406,8 @@ struct RecCur {
     const Rec<K>* r;
     uint32_t offa, offb, la, lb, i, j, o, oe, base;
     Rec<K> a, b;
-    PS_DEV uint32_t ia(uint32_t x) const { return padr(offa + x); }
-    PS_DEV uint32_t ib(uint32_t x) const { return padr(offb + x); }
+    PS_DEV uint32_t ia(uint32_t x) const { return padr<K>(offa + x); }
+    PS_DEV uint32_t ib(uint32_t x) const { return padr<K>(offb + x); }
     PS_DEV K keyA(uint32_t x) const { return r[ia(x)].k; }
     PS_DEV K keyB(uint32_t x) const { return r[ib(x)].k; }
     PS_DEV void heads() {
@@ -349,7 +417,7 @@ struct RecCur {
     PS_DEV void step(Rec<K>* out) {
         if (o >= oe) return;
         const bool takeA = i < la && (j >= lb || !(b.k < a.k));
-        out[padr(base + o)] = takeA ? a : b;
+        out[padr<K>(base + o)] = takeA ? a : b;
         ++o;
         i += takeA;
         j += !takeA;
@@ -358,43 +426,6 @@ struct RecCur {
         b = takeA ? b : nx;
     }
 };
-
-// Interleaved diagonal searches for both cursors, then the lockstep merge.
-template <class C0, class C1, class K>
-PS_DEV void dual_merge(C0& c0, C1& c1, Rec<K>* out) {
-    uint32_t lo0 = c0.o > c0.lb ? c0.o - c0.lb : 0, hi0 = c0.o < c0.la ? c0.o : c0.la;
-    uint32_t lo1 = c1.o > c1.lb ? c1.o - c1.lb : 0, hi1 = c1.o < c1.la ? c1.o : c1.la;
-    if (c0.o >= c0.oe) lo0 = hi0;
-    if (c1.o >= c1.oe) lo1 = hi1;
-    while (lo0 < hi0 || lo1 < hi1) {
-        const uint32_t m0 = (lo0 + hi0) >> 1, m1 = (lo1 + hi1) >> 1;
-        const bool act0 = lo0 < hi0, act1 = lo1 < hi1;
-        // A[mid] <= B[d-1-mid]  (indices are clamped, results used only when active)
-        const bool le0 = !(c0.keyB(c0.o - 1 - m0) < c0.keyA(m0));
-        const bool le1 = !(c1.keyB(c1.o - 1 - m1) < c1.keyA(m1));
-        if (act0) {
-            lo0 = le0 ? m0 + 1 : lo0;
-            hi0 = le0 ? hi0 : m0;
-        }
-        if (act1) {
-            lo1 = le1 ? m1 + 1 : lo1;
-            hi1 = le1 ? hi1 : m1;
-        }
-    }
-    c0.i = lo0;
-    c0.j = c0.o - lo0;
-    c1.i = lo1;
-    c1.j = c1.o - lo1;
-    c0.heads();
-    c1.heads();
-    const uint32_t n0 = c0.oe > c0.o ? c0.oe - c0.o : 0, n1 = c1.oe > c1.o ? c1.oe - c1.o : 0;
-    const uint32_t nmax = n0 > n1 ? n0 : n1;
-#pragma unroll 2
-    for (uint32_t t = 0; t < nmax; ++t) {
-        c0.step(out);
-        c1.step(out);
-    }
-}
 
 // One cursor: diagonal search, then the serial branch-free merge.
 template <class C, class K>
@@ -421,74 +452,7 @@ struct Win {
     const K* k;
     const int32_t* v;
     uint32_t len;
-    PS_DEV uint32_t cl(uint32_t i) const { return i < len ? i : (len ? len - 1 : 0); }
 };
-// A padded record sequence: element i at r[padr(off + i)].
-template <class K>
-struct RecSeq {
-    const Rec<K>* r;
-    uint32_t len, off;
-    PS_DEV const Rec<K>& at(uint32_t i) const { return r[padr(off + (i < len ? i : (len ? len - 1 : 0)))]; }
-};
-
-// Merge-path diagonal: # of A among the first d outputs of merge(A, B), ties to A.
-template <class K, class GA, class GB>
-PS_DEV uint32_t diag_search(uint32_t d, uint32_t la, uint32_t lb, GA ka, GB kb) {
-    uint32_t lo = d > lb ? d - lb : 0;
-    uint32_t hi = d < la ? d : la;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const bool le = !(kb(d - 1 - mid) < ka(mid));  // A[mid] <= B[d-1-mid]
-        lo = le ? mid + 1 : lo;
-        hi = le ? hi : mid;
-    }
-    return lo;
-}
-
-// outputs [o0, o1) of merge(A, B) of two SoA windows -> padded records out[base + o]
-template <class K>
-PS_DEV void merge_win(const Win<K>& A, const Win<K>& B, Rec<K>* out, uint32_t base, uint32_t o0, uint32_t o1) {
-    if (o0 >= o1) return;
-    uint32_t i = diag_search<K>(o0, A.len, B.len, [&](uint32_t x) { return A.k[x]; },
-                                [&](uint32_t x) { return B.k[x]; });
-    uint32_t j = o0 - i;
-    K a = A.k[A.cl(i)];
-    K b = B.k[B.cl(j)];
-#pragma unroll 4
-    for (uint32_t o = o0; o < o1; ++o) {
-        const bool takeA = i < A.len && (j >= B.len || !(b < a));
-        Rec<K> rec;
-        rec.k = takeA ? a : b;
-        rec.v = *(takeA ? A.v + i : B.v + j);
-        out[padr(base + o)] = rec;
-        i += takeA;
-        j += !takeA;
-        const K nk = *(takeA ? A.k + A.cl(i) : B.k + B.cl(j));
-        a = takeA ? nk : a;
-        b = takeA ? b : nk;
-    }
-}
-
-// outputs [o0, o1) of merge(X, Y) of two padded record sequences
-template <class K>
-PS_DEV void merge_rec(const RecSeq<K>& X, const RecSeq<K>& Y, Rec<K>* out, uint32_t o0, uint32_t o1) {
-    if (o0 >= o1) return;
-    uint32_t i = diag_search<K>(o0, X.len, Y.len, [&](uint32_t x) { return X.r[padr(X.off + x)].k; },
-                                [&](uint32_t x) { return Y.r[padr(Y.off + x)].k; });
-    uint32_t j = o0 - i;
-    Rec<K> a = X.at(i);
-    Rec<K> b = Y.at(j);
-#pragma unroll 4
-    for (uint32_t o = o0; o < o1; ++o) {
-        const bool takeA = i < X.len && (j >= Y.len || !(b.k < a.k));
-        out[padr(o)] = takeA ? a : b;
-        i += takeA;
-        j += !takeA;
-        const Rec<K> nx = takeA ? X.at(i) : Y.at(j);
-        a = takeA ? nx : a;
-        b = takeA ? b : nx;
-    }
-}
 
 template <class K>
 __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
@@ -550,7 +514,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 const uint32_t sx = __shfl_sync(PS_FULL, st.x, u), sy = __shfl_sync(PS_FULL, st.y, u);
                 const uint32_t sz = __shfl_sync(PS_FULL, st.z, u), sw = __shfl_sync(PS_FULL, st.w, u);
                 const uint32_t tot = (en.x - sx) + (en.y - sy) + (en.z - sz) + (en.w - sw);
-                const bool ok = lane >= u && lane < nvalid && nid == nid_u && tot <= LY::CAP;
+                const bool ok = lane >= u && lane < nvalid && nid == nid_u && tot <= cut_cap<K>();
                 uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
                 // contiguous run of ok lanes starting at u
                 const uint32_t runlen = __ffs(~bal) ? __ffs(~bal) - 1 : 32 - u;
@@ -633,7 +597,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     d.w = w;
                     d.par = par;
                     d.done = 0;
-                    if (total > LY::CAP) atomicOr(err, ERR_CUT);
+                    if (total > cut_cap<K>()) atomicOr(err, ERR_CUT);
                     mbar_arrive_tx(&full[slot], txs);
                 }
                 PT_MARK(2)
@@ -662,6 +626,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         const uint32_t slot = i % PIPE_SLOTS;
         mbar_wait(&full[slot], (i / PIPE_SLOTS) & 1);
         PT_MARK(4)
+        PT_USTART
         const PipeDesc& d = desc[slot];
         if (d.done) break;
         const uint32_t T = d.T, w = d.w, par = d.par;
@@ -693,15 +658,28 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         // destination so the store phase moves aligned 16-byte vectors
         constexpr uint32_t ER = sizeof(K) == 4 ? 4 : 2;  // records per store group
         const uint32_t al = (uint32_t)(out % ER);
-        const uint32_t o0 = (uint32_t)((uint64_t)T * ctid / NC), o1 = (uint32_t)((uint64_t)T * (ctid + 1) / NC);
+        constexpr uint32_t VT = pipe_vt<K>();
+        const uint32_t o0 = min(T, VT * ctid), o1 = min(T, VT * ctid + VT);
         if (w >= 3) {
-            // pass 1: X = merge(A, B) -> xr[0, LX);  Y = merge(C, D) (3-way: C) -> xr[LX, T)
-            // (thread t takes the t-th 1/NC of the concatenated X || Y output)
+            // pass 1: X = merge(A, B) -> xr[0, LX);  Y = merge(C, D) (3-way: C) -> xr[LXp, LXp + LY)
+            // with LXp = LX rounded up to VT: thread t takes outputs [VT*t, VT*t + VT)
+            // of that layout, so every warp runs one merge (no X/Y divergence)
             const uint32_t LX = win[0].len + win[1].len, LYn = T - LX;
-            WinCur<K> cx = wincur(0, 1, 0, o0, min(o1, LX));
-            single_merge(cx, xr);
-            WinCur<K> cy = wincur(2, 3, LX, o0 > LX ? o0 - LX : 0, o1 > LX ? o1 - LX : 0);
-            single_merge(cy, xr);
+            const uint32_t LXp = (LX + VT - 1) / VT * VT;
+            const uint32_t ob = VT * ctid;
+            const bool isY = ob >= LXp;
+            WinCur<K> c;
+            c.ak = isY ? win[2].k : win[0].k;
+            c.bk = isY ? win[3].k : win[1].k;
+            c.av = isY ? win[2].v : win[0].v;
+            c.bv = isY ? win[3].v : win[1].v;
+            c.la = isY ? win[2].len : win[0].len;
+            c.lb = isY ? win[3].len : win[1].len;
+            c.o = isY ? ob - LXp : ob;
+            c.oe = isY ? min(ob + VT - LXp, LYn) : min(ob + VT, LX);
+            c.base = isY ? LXp : 0;
+            single_merge(c, xr);
+            PT_WARP(16)
             consumer_sync();
             PT_MARK(5)
             // pass 2: merge X and Y into the slot (its input windows are consumed)
@@ -709,7 +687,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             RecCur<K> p0;
             p0.r = xr;
             p0.offa = 0;
-            p0.offb = LX;
+            p0.offb = LXp;
             p0.la = LX;
             p0.lb = LYn;
             p0.base = al;
@@ -722,6 +700,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             WinCur<K> c0 = wincur(0, 1, al, o0, o1);
             single_merge(c0, orec);
         }
+        PT_WARP(24)
         consumer_sync();
         PT_MARK(6)
         // store: group j = records [ER*j, ER*j + ER) of the phase-shifted layout
@@ -733,13 +712,18 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             for (uint32_t j = ctid; j < ng; j += NC) {
                 const uint32_t r0 = j * ER;
                 if (r0 >= al && r0 + ER <= al + T) {
-                    const uint4* src = reinterpret_cast<const uint4*>(orec + padr(r0));
+                    // an ER-group never straddles a pad record (ER divides VT)
+                    const Rec<K>* src = orec + padr<K>(r0);
                     if (sizeof(K) == 4) {
-                        const uint4 q0 = src[0], q1 = src[1];  // (k0,v0,k1,v1) (k2,v2,k3,v3)
-                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.z, q1.x, q1.z);
-                        *reinterpret_cast<uint4*>(dstV + gbase + r0) = make_uint4(q0.y, q0.w, q1.y, q1.w);
+                        const uint2 q0 = *reinterpret_cast<const uint2*>(src + 0);
+                        const uint2 q1 = *reinterpret_cast<const uint2*>(src + 1);
+                        const uint2 q2 = *reinterpret_cast<const uint2*>(src + 2);
+                        const uint2 q3 = *reinterpret_cast<const uint2*>(src + 3);
+                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q1.x, q2.x, q3.x);
+                        *reinterpret_cast<uint4*>(dstV + gbase + r0) = make_uint4(q0.y, q1.y, q2.y, q3.y);
                     } else {
-                        const uint4 q0 = src[0], q1 = src[1];  // (k0 lo, k0 hi, v0, pad) (k1 lo, k1 hi, v1, pad)
+                        const uint4 q0 = *reinterpret_cast<const uint4*>(src + 0);  // (k0 lo, k0 hi, v0, pad)
+                        const uint4 q1 = *reinterpret_cast<const uint4*>(src + 1);
                         *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.y, q1.x, q1.y);
                         *reinterpret_cast<uint2*>(dstV + gbase + r0) = make_uint2(q0.z, q1.z);
                     }
@@ -747,7 +731,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     for (uint32_t t = 0; t < ER; ++t) {
                         const uint32_t rr = r0 + t;
                         if (rr >= al && rr < al + T) {
-                            const Rec<K> rec = orec[padr(rr)];
+                            const Rec<K> rec = orec[padr<K>(rr)];
                             dstK[gbase + rr] = rec.k;
                             dstV[gbase + rr] = rec.v;
                         }

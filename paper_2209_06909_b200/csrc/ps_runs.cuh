@@ -256,26 +256,36 @@ __global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restri
 
 // ---------------------------------------------------------------------------
 // Chain scan over tables (hierarchical, fan-out TSCAN_FAN).  Level-L table j
-// spans [j*span, (j+1)*span); F at its start is Ft[j*span/TILE].
-// compose: one warp per output table; dynamic smem TSCAN_FAN*(m+1) uint64.
+// spans [j*span, (j+1)*span); F at its start is Ft[j*span/TILE].  Every kernel
+// stages its tables and F values in shared memory first, so the serial walks
+// below only pay shared-memory latency.
+// Dynamic smem of compose/top/down: TSCAN_FAN*(m+1) uint64.
+PS_DEV uint32_t stage_tables(const uint64_t* __restrict__ in, uint32_t j0, uint32_t cnt, uint32_t M1,
+                             uint64_t span, const uint32_t* __restrict__ Ft, uint64_t* s_tab, uint64_t* s_F) {
+    for (uint32_t i = threadIdx.x; i < cnt * M1; i += blockDim.x) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) s_F[k] = Ft[((uint64_t)(j0 + k) * span) / TILE];
+    return cnt;
+}
+
+// compose: one warp per output table.
 __global__ void __launch_bounds__(32) rd_compose_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
                                                         const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
                                                         uint64_t* __restrict__ out, uint32_t* err) {
     extern __shared__ uint64_t s_tab[];
+    __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t o = blockIdx.x;
     const uint32_t j0 = o * TSCAN_FAN;
     const uint32_t cnt = min(TSCAN_FAN, P - j0);
     const uint32_t M1 = m + 1;
-    for (uint32_t i = threadIdx.x; i < cnt * M1; i += 32) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    stage_tables(in, j0, cnt, M1, span, Ft, s_tab, s_F);
     __syncwarp();
     const uint64_t t0 = (uint64_t)j0 * span;
-    const uint64_t F0 = Ft[t0 / TILE];
     for (uint32_t e = threadIdx.x; e < M1; e += 32) {
-        uint64_t x = e < m ? t0 + e : F0;
+        uint64_t x = e < m ? t0 + e : s_F[0];
         uint64_t c = 0;
         for (uint32_t k = 0; k < cnt; ++k) {
             const uint64_t tk = t0 + (uint64_t)k * span;
-            tab_apply(s_tab + k * M1, tk, tk + span, Ft[tk / TILE], m, n, x, c, err);
+            tab_apply(s_tab + k * M1, tk, tk + span, s_F[k], m, n, x, c, err);
         }
         out[(uint64_t)o * M1 + e] = pack_xc((uint32_t)x, (uint32_t)c);
     }
@@ -283,16 +293,21 @@ __global__ void __launch_bounds__(32) rd_compose_kernel(const uint64_t* __restri
 
 // top: P <= TSCAN_FAN tables, entry (0, 0); writes each table's entry and the
 // total run count r (b[r] = n).
-__global__ void rd_top_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
-                              const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
-                              uint64_t* __restrict__ entries, uint32_t* __restrict__ b, Summary* sum, uint32_t* err) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(32) rd_top_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
+                                                    const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
+                                                    uint64_t* __restrict__ entries, uint32_t* __restrict__ b,
+                                                    Summary* sum, uint32_t* err) {
+    extern __shared__ uint64_t s_tab[];
+    __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t M1 = m + 1;
+    stage_tables(in, 0, P, M1, span, Ft, s_tab, s_F);
+    __syncwarp();
+    if (threadIdx.x != 0) return;
     uint64_t x = 0, c = 0;
     for (uint32_t j = 0; j < P; ++j) {
         entries[j] = pack_xc((uint32_t)x, (uint32_t)c);
         const uint64_t tj = (uint64_t)j * span;
-        tab_apply(in + (uint64_t)j * M1, tj, tj + span, Ft[tj / TILE], m, n, x, c, err);
+        tab_apply(s_tab + j * M1, tj, tj + span, s_F[j], m, n, x, c, err);
     }
     if (x != n) atomicOr(err, ERR_CHAIN);
     sum->r = (uint32_t)c;
@@ -305,11 +320,12 @@ __global__ void __launch_bounds__(32) rd_down_kernel(const uint64_t* __restrict_
                                                      const uint64_t* __restrict__ up_entries,
                                                      uint64_t* __restrict__ entries, uint32_t* err) {
     extern __shared__ uint64_t s_tab[];
+    __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t o = blockIdx.x;
     const uint32_t j0 = o * TSCAN_FAN;
     const uint32_t cnt = min(TSCAN_FAN, P - j0);
     const uint32_t M1 = m + 1;
-    for (uint32_t i = threadIdx.x; i < cnt * M1; i += 32) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    stage_tables(in, j0, cnt, M1, span, Ft, s_tab, s_F);
     __syncwarp();
     if (threadIdx.x != 0) return;
     const uint64_t v = up_entries[o];
@@ -317,12 +333,13 @@ __global__ void __launch_bounds__(32) rd_down_kernel(const uint64_t* __restrict_
     for (uint32_t k = 0; k < cnt; ++k) {
         entries[j0 + k] = pack_xc((uint32_t)x, (uint32_t)c);
         const uint64_t tk = (uint64_t)(j0 + k) * span;
-        tab_apply(s_tab + k * M1, tk, tk + span, Ft[tk / TILE], m, n, x, c, err);
+        tab_apply(s_tab + k * M1, tk, tk + span, s_F[k], m, n, x, c, err);
     }
 }
 
 // ---------------------------------------------------------------------------
 // RD2c: emit the run boundaries b[c] and natural lengths nat[c].
+// Dynamic smem: TILES_PER_GROUP * (m+1) uint64 (the group's tile tables).
 __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
                                                       const uint32_t* __restrict__ Fg, uint32_t ngroups,
                                                       const uint64_t* __restrict__ tile_tab,
@@ -333,18 +350,23 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
     __shared__ uint32_t s_chg[GROUP_WORDS + 1];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
     __shared__ uint64_t s_entry[TILES_PER_GROUP];
+    __shared__ uint64_t s_F[TILES_PER_GROUP];
+    extern __shared__ uint64_t s_tab[];  // [TILES_PER_GROUP][m+1]
     const uint32_t g = blockIdx.x;
     ChainView cv;
     build_chain_view(ty, n, g, ngroups, Fg, s_chg, s_nzn, cv, m);
     const uint32_t M1 = m + 1;
     const uint64_t tile0 = (uint64_t)g * TILES_PER_GROUP;
+    for (uint32_t i = threadIdx.x; i < TILES_PER_GROUP * M1; i += blockDim.x) s_tab[i] = tile_tab[tile0 * M1 + i];
+    if (threadIdx.x < TILES_PER_GROUP) s_F[threadIdx.x] = Ft[tile0 + threadIdx.x];
+    __syncthreads();
     if (threadIdx.x == 0) {
         const uint64_t v = group_entries[g];
         uint64_t x = unpack_x(v), c = unpack_c(v);
         for (uint32_t k = 0; k < TILES_PER_GROUP; ++k) {
             s_entry[k] = pack_xc((uint32_t)x, (uint32_t)c);
             const uint64_t tk = cv.G + (uint64_t)k * TILE;
-            tab_apply(tile_tab + (tile0 + k) * M1, tk, tk + TILE, Ft[tile0 + k], m, n, x, c, err);
+            tab_apply(s_tab + k * M1, tk, tk + TILE, s_F[k], m, n, x, c, err);
         }
     }
     __syncthreads();

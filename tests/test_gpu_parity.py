@@ -118,6 +118,19 @@ def test_min_run_len_sweep(mrl, dev):
         assert read_trace(device=dev) == ref.trace
 
 
+@pytest.mark.parametrize("mrl", [5, 24, 200, 256])
+def test_min_run_len_multilevel_chain_scan(mrl, dev):
+    # > TSCAN_FAN groups of 16384 keys: the run-boundary chain scan goes
+    # through compose/top/down levels (64 KB of staged tables at m = 256)
+    n = 1_300_000 + 4 * mrl  # cfg4 needs n % 4 == 0
+    keys = workloads.cfg4(n=n, seed=mrl)
+    ref = oracle.sort(keys, min_run_len=mrl)
+    out, perm, stats = gpu_sort(keys, dev, min_run_len=mrl)
+    assert np.array_equal(perm, ref.values), mrl
+    assert stats.run_lengths == ref.run_lengths
+    assert stats.merge_cost == ref.stats["merge_cost"]
+
+
 def test_values_payload_permuted(dev):
     keys_np = workloads.cfg3(n=1 << 16, seed=5)
     vals_np = np.random.default_rng(1).integers(-1000, 1000, size=keys_np.size).astype(np.int32)

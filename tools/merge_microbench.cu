@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT) bench64_kernel(const int* __restrict__ gk,
 #pragma unroll 4
         for (uint32_t o = o0; o < o1; ++o) {
             const bool takeA = i < la && (j >= lb || a < b);
-            out[padr(o)] = takeA ? a : b;
+            out[padr<int>(o)] = takeA ? a : b;
             i += takeA;
             j += !takeA;
             const uint64_t nx = takeA ? A[i < la ? i : la - 1] : B[j < lb ? j : lb - 1];

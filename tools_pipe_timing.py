@@ -14,7 +14,7 @@ dev = torch.device('cuda', 0)
 src = torch.from_numpy(keys_np).to(dev)
 keys = torch.empty_like(src)
 perm = torch.empty(src.numel(), dtype=torch.int32, device=dev)
-buf = np.zeros(16, dtype=np.uint64)
+buf = np.zeros(40, dtype=np.uint64)
 for it in range(2):
     keys.copy_(src)
     lib.ps_debug_pipe_timing(buf.ctypes.data, 1)
@@ -26,3 +26,5 @@ for i, nm in enumerate(names):
     v = int(buf[i])
     per = v / (pu if nm.startswith('P') else cu)
     print('%-14s total %14d   per unit %10.1f cycles' % (nm, v, per))
+print('per-warp pass1 work (cycles/unit, to the barrier):', ' '.join('%6.0f' % (int(buf[16 + w]) / cu) for w in range(8)))
+print('per-warp pass2 work (cycles/unit, since unit start):', ' '.join('%6.0f' % (int(buf[24 + w]) / cu) for w in range(8)))
