@@ -142,8 +142,8 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.rmax = rmax + 2;
     L.ngroups = std::max<uint64_t>(1, cdiv(n, GROUP));
     L.ntiles = L.ngroups * TILES_PER_GROUP;
-    // total chunks <= nodes + merge_cost / (CHUNK_CAP / MAX_WAY); merge_cost <= 64 n
-    L.chunks_max = L.rmax + cdiv(64 * n, (CHUNK_CAP / 2 - 16) / MAX_WAY) + 16;
+    // total chunks <= nodes + merge_cost / (cut spacing); merge_cost <= 64 n
+    L.chunks_max = L.rmax + cdiv(64 * n, MIN_CUT_SPACING) + 16;
     // min tree levels over P (size rmax + 1)
     uint64_t s = align_up(L.rmax + 1, 32);
     L.nlev = 0;
@@ -630,7 +630,7 @@ ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
         off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
         return o;
     };
-    L.chunks_max = 16 + cdiv(8 * slab_n, (CHUNK_CAP / 2 - 16) / MAX_WAY);
+    L.chunks_max = 16 + cdiv(8 * slab_n, MIN_CUT_SPACING);
     L.bounds = take(2 * 2 * MAX_SHARDS * 8);
     L.targets = take(16);
     L.err = take(16);

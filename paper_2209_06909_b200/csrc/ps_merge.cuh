@@ -5,14 +5,14 @@
 // merges.py:1-8), i.e. the merge under the strict order (key, run, position).
 //
 // Big nodes are cut into chunks: cut (a, j) is the record at position j*S of
-// run a (S = CHUNK_CAP / arity); its rank in every other run b is a search
+// run a (S = cut_cap / arity); its rank in every other run b is a search
 // (<= for b < a, < for b > a) and its index in the merged cut order follows
 // directly from those ranks.  Between consecutive cuts there are at most S
-// records of each run, so every chunk holds <= CHUNK_CAP records.
+// records of each run, so every chunk holds <= cut_cap records.
 //
 // merge_pipe_kernel (persistent, warp-specialized):
 //   producer warp  -- reads the descriptors of 32 chunks at once, packs
-//                     consecutive chunks of a node into units of <= CHUNK_CAP
+//                     consecutive chunks of a node into units of <= cut_cap
 //                     records and stages each unit's k input windows (keys
 //                     and values) into a free smem slot with TMA bulk copies
 //                     (cp.async.bulk + mbarrier complete_tx), double-buffered;
@@ -37,20 +37,34 @@ namespace ps {
 constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
 
 // Consumer thread t produces the VT outputs [VT*t, VT*t + VT) of every merge
-// pass.  Record arrays get one pad record per VT, so the k-th output of all
-// lanes lands at (VT+1)*t + k: 2 wavefronts per warp store (bank-conflict free).
+// pass.  VT is odd (17 records of 8 bytes, 9 of 16 bytes): the k-th output of
+// the lanes of a warp lands in distinct banks (2 or 4 wavefronts per warp
+// store, the minimum), and the data-dependent read positions of balanced
+// merges (~VT/2 * t) spread over all banks as well.  No padding is needed.
+#ifndef PS_VT4
+#define PS_VT4 17
+#endif
+#ifndef PS_VT8
+#define PS_VT8 9
+#endif
 template <class K>
 PS_DEV __host__ constexpr uint32_t pipe_vt() {
-    return chunk_cap<K>() / PIPE_CONSUMERS;
+    return sizeof(K) == 4 ? PS_VT4 : PS_VT8;
+}
+// records per unit (smem slot capacity)
+template <class K>
+PS_DEV __host__ constexpr uint32_t pipe_cap() {
+    return pipe_vt<K>() * PIPE_CONSUMERS;
 }
 // Cut spacing budget: units hold <= CAP - VT records, so pass 1 can start Y
 // at a VT-aligned offset (no thread straddles X and Y) within NC threads.
 template <class K>
 PS_DEV __host__ constexpr uint32_t cut_cap() {
-    return chunk_cap<K>() - pipe_vt<K>();
+    return pipe_cap<K>() - pipe_vt<K>();
 }
-static_assert((pipe_vt<int32_t>() & (pipe_vt<int32_t>() - 1)) == 0, "VT must be a power of two");
-static_assert((pipe_vt<int64_t>() & (pipe_vt<int64_t>() - 1)) == 0, "VT must be a power of two");
+// smallest cut spacing of any key type (bounds the chunk count)
+constexpr uint32_t MIN_CUT_SPACING =
+    (cut_cap<int32_t>() < cut_cap<int64_t>() ? cut_cap<int32_t>() : cut_cap<int64_t>()) / MAX_WAY;
 
 // # of a[0..len) that are <= x (LE) or < x (!LE)
 template <class K, bool LE>
@@ -334,18 +348,12 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
     int32_t v;
 };
 
-#ifdef PS_NOPAD
-template <class K>
-PS_DEV uint32_t padr(uint32_t o) { return o; }
-#else
-template <class K>
-PS_DEV uint32_t padr(uint32_t o) { return o + o / pipe_vt<K>(); }
-#endif
 
 template <class K>
 struct PipeLayout {
-    static constexpr uint32_t CAP = chunk_cap<K>();
-    static constexpr uint32_t PADN = CAP + CAP / pipe_vt<K>() + 16;  // padded record capacity
+    static constexpr uint32_t CAP = pipe_cap<K>();
+    static constexpr uint32_t PADN = CAP + 16;  // record capacity (+ over-read / don't-care slack)
+    static_assert(PADN >= CAP + pipe_vt<K>() - 1, "record slack must hold a thread's don't-care outputs");
     static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
     // slot = TMA landing zone of the k key windows + k value windows (SoA, 16B
     // alignment slack each), and afterwards the padded records of the last pass
@@ -385,14 +393,13 @@ struct WinCur {
         a = ak[ca(i)];
         b = bk[cb(j)];
     }
-    PS_DEV void step(Rec<K>* out) {
-        if (o >= oe) return;
+    // one output to outp[t]; no end check (see single_merge)
+    PS_DEV void step(Rec<K>* outp, uint32_t t) {
         const bool takeA = i < la && (j >= lb || !(b < a));
         Rec<K> r;
         r.k = takeA ? a : b;
         r.v = *(takeA ? av + i : bv + j);
-        out[padr<K>(base + o)] = r;
-        ++o;
+        outp[t] = r;
         i += takeA;
         j += !takeA;
         const K nk = *(takeA ? ak + ca(i) : bk + cb(j));
@@ -406,19 +413,17 @@ struct RecCur {
     const Rec<K>* r;
     uint32_t offa, offb, la, lb, i, j, o, oe, base;
     Rec<K> a, b;
-    PS_DEV uint32_t ia(uint32_t x) const { return padr<K>(offa + x); }
-    PS_DEV uint32_t ib(uint32_t x) const { return padr<K>(offb + x); }
+    PS_DEV uint32_t ia(uint32_t x) const { return (offa + x); }
+    PS_DEV uint32_t ib(uint32_t x) const { return (offb + x); }
     PS_DEV K keyA(uint32_t x) const { return r[ia(x)].k; }
     PS_DEV K keyB(uint32_t x) const { return r[ib(x)].k; }
     PS_DEV void heads() {
         a = r[ia(i)];
         b = r[ib(j)];
     }
-    PS_DEV void step(Rec<K>* out) {
-        if (o >= oe) return;
+    PS_DEV void step(Rec<K>* outp, uint32_t t) {
         const bool takeA = i < la && (j >= lb || !(b.k < a.k));
-        out[padr<K>(base + o)] = takeA ? a : b;
-        ++o;
+        outp[t] = takeA ? a : b;
         i += takeA;
         j += !takeA;
         const Rec<K> nx = r[takeA ? ia(i) : ib(j)];
@@ -427,7 +432,12 @@ struct RecCur {
     }
 };
 
-// One cursor: diagonal search, then the serial branch-free merge.
+// One cursor: diagonal search, then the serial branch-free merge of exactly
+// VT steps (fully unrolled, no per-step end check).  A thread with fewer than
+// VT outputs (the last one of a merge) writes up to VT - 1 don't-care records
+// past its range: they land in the slack between X and Y (Y starts VT-aligned)
+// or past the unit's last output, inside the record capacity (PADN >= CAP + VT
+// - 1), and are never read.  Its extra reads stay inside shared memory too.
 template <class C, class K>
 PS_DEV void single_merge(C& c, Rec<K>* out) {
     if (c.o >= c.oe) return;
@@ -441,9 +451,9 @@ PS_DEV void single_merge(C& c, Rec<K>* out) {
     c.i = lo;
     c.j = c.o - lo;
     c.heads();
-    const uint32_t n = c.oe - c.o;
-#pragma unroll 4
-    for (uint32_t t = 0; t < n; ++t) c.step(out);
+    Rec<K>* outp = out + c.base + c.o;
+#pragma unroll
+    for (uint32_t t = 0; t < pipe_vt<K>(); ++t) c.step(outp, t);
 }
 
 // A TMA-landed input window: SoA keys / values, unpadded.
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             PT_MARK(0)
             uint32_t u = 0;
             while (u < nvalid) {
-                // unit = lanes u..V of the same node with total <= CHUNK_CAP
+                // unit = lanes u..V of the same node with total <= cut_cap
                 const uint32_t nid_u = __shfl_sync(PS_FULL, nid, u);
                 const uint32_t sx = __shfl_sync(PS_FULL, st.x, u), sy = __shfl_sync(PS_FULL, st.y, u);
                 const uint32_t sz = __shfl_sync(PS_FULL, st.z, u), sw = __shfl_sync(PS_FULL, st.w, u);
@@ -712,18 +722,13 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             for (uint32_t j = ctid; j < ng; j += NC) {
                 const uint32_t r0 = j * ER;
                 if (r0 >= al && r0 + ER <= al + T) {
-                    // an ER-group never straddles a pad record (ER divides VT)
-                    const Rec<K>* src = orec + padr<K>(r0);
+                    const uint4* src = reinterpret_cast<const uint4*>(orec + r0);
                     if (sizeof(K) == 4) {
-                        const uint2 q0 = *reinterpret_cast<const uint2*>(src + 0);
-                        const uint2 q1 = *reinterpret_cast<const uint2*>(src + 1);
-                        const uint2 q2 = *reinterpret_cast<const uint2*>(src + 2);
-                        const uint2 q3 = *reinterpret_cast<const uint2*>(src + 3);
-                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q1.x, q2.x, q3.x);
-                        *reinterpret_cast<uint4*>(dstV + gbase + r0) = make_uint4(q0.y, q1.y, q2.y, q3.y);
+                        const uint4 q0 = src[0], q1 = src[1];  // (k0,v0,k1,v1) (k2,v2,k3,v3)
+                        *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.z, q1.x, q1.z);
+                        *reinterpret_cast<uint4*>(dstV + gbase + r0) = make_uint4(q0.y, q0.w, q1.y, q1.w);
                     } else {
-                        const uint4 q0 = *reinterpret_cast<const uint4*>(src + 0);  // (k0 lo, k0 hi, v0, pad)
-                        const uint4 q1 = *reinterpret_cast<const uint4*>(src + 1);
+                        const uint4 q0 = src[0], q1 = src[1];  // (k0 lo, k0 hi, v0, pad) (k1 lo, k1 hi, v1, pad)
                         *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.y, q1.x, q1.y);
                         *reinterpret_cast<uint2*>(dstV + gbase + r0) = make_uint2(q0.z, q1.z);
                     }
@@ -731,7 +736,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     for (uint32_t t = 0; t < ER; ++t) {
                         const uint32_t rr = r0 + t;
                         if (rr >= al && rr < al + T) {
-                            const Rec<K> rec = orec[padr<K>(rr)];
+                            const Rec<K> rec = orec[(rr)];
                             dstK[gbase + rr] = rec.k;
                             dstV[gbase + rr] = rec.v;
                         }
