@@ -24,6 +24,10 @@ template <class K>
 struct Bufs {
     K* k[2];
     int32_t* v[2];
+    // select, not an indexed access: a runtime index into the by-value kernel
+    // parameter would spill the struct to local memory
+    PS_DEV K* kb(uint32_t p) const { return p ? k[1] : k[0]; }
+    PS_DEV int32_t* vb(uint32_t p) const { return p ? v[1] : v[0]; }
 };
 
 // shared layout: sb[FORM_TILE+2] u32, snat[FORM_TILE+1] u32, spar[FORM_TILE+1] u8,
@@ -103,8 +107,8 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         const uint32_t len = (uint32_t)(ej - bj);
         if (snat[lo] < len) continue;  // extended window, below
         const uint32_t par = spar[lo];
-        K* dk = bufs.k[par];
-        int32_t* dv = bufs.v[par];
+        K* dk = bufs.kb(par);
+        int32_t* dv = bufs.vb(par);
         bool desc = false;
         if (len >= 2) {
             const uint64_t q = bj + 1;
@@ -195,8 +199,8 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         const uint32_t leaf = wlist[lo];
         const uint32_t par = spar[leaf];
         const uint64_t dst = (uint64_t)sb[leaf] + rank;
-        bufs.k[par][dst] = x;
-        bufs.v[par][dst] = wv[e];
+        bufs.kb(par)[dst] = x;
+        bufs.vb(par)[dst] = wv[e];
     }
 }
 

@@ -32,7 +32,7 @@ namespace ps {
 
 // consumer threads per merge_pipe_kernel CTA
 #ifndef PS_CONSUMERS
-#define PS_CONSUMERS 256
+#define PS_CONSUMERS 512
 #endif
 constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
 
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     q -= 1;
     const uint32_t w = nd.arity;
     const uint32_t S = cut_cap<K>() / w;
-    const K* src = bufs.k[nd.parity ^ 1];
+    const K* src = bufs.kb(nd.parity ^ 1);
     uint32_t L[4];
 #pragma unroll
     for (uint32_t a = 0; a < 4; ++a) L[a] = a < w ? nd.pos[a + 1] - nd.pos[a] : 0;
@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
     K* ok = sk + SMALL_NODE;
     int32_t* sv = reinterpret_cast<int32_t*>(ok + SMALL_NODE);
     int32_t* ov = sv + SMALL_NODE;
-    const K* __restrict__ srcK = bufs.k[nd.parity ^ 1];
-    const int32_t* __restrict__ srcV = bufs.v[nd.parity ^ 1];
+    const K* __restrict__ srcK = bufs.kb(nd.parity ^ 1);
+    const int32_t* __restrict__ srcV = bufs.vb(nd.parity ^ 1);
     for (uint32_t i = lane; i < size; i += 32) {
         sk[i] = srcK[(uint64_t)p0 + i];
         sv[i] = srcV[(uint64_t)p0 + i];
@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
         ov[rank] = sv[i];
     }
     __syncwarp();
-    K* __restrict__ dstK = bufs.k[nd.parity];
-    int32_t* __restrict__ dstV = bufs.v[nd.parity];
+    K* __restrict__ dstK = bufs.kb(nd.parity);
+    int32_t* __restrict__ dstV = bufs.vb(nd.parity);
     for (uint32_t i = lane; i < size; i += 32) {
         dstK[(uint64_t)p0 + i] = ok[i];
         dstV[(uint64_t)p0 + i] = ov[i];
@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 }
                 const uint32_t region = (is_val ? LY::KEY_BYTES : 0u) + pre;
                 if (lane < 8 && wa < w && len) {
-                    const uint8_t* src = is_val ? reinterpret_cast<const uint8_t*>(bufs.v[par ^ 1])
-                                                : reinterpret_cast<const uint8_t*>(bufs.k[par ^ 1]);
+                    const uint8_t* src = is_val ? reinterpret_cast<const uint8_t*>(bufs.vb(par ^ 1))
+                                                : reinterpret_cast<const uint8_t*>(bufs.kb(par ^ 1));
                     const uint64_t b0 = e0 * ebytes, b1 = (e0 + len) * ebytes;
                     const uint64_t a0 = b0 & ~15ull, a1 = b1 & ~15ull;
                     if (a1 > a0) {
@@ -711,17 +711,21 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             single_merge(c0, orec);
         }
         PT_WARP(24)
-        consumer_sync();
+        // store: every warp moves its own outputs [VT*32*w, VT*32*(w+1)) as soon as
+        // they are written (no CTA barrier): full ER-groups of the phase-shifted
+        // layout as 16-byte vectors, the partial groups at both ends record by record
+        __syncwarp();
         PT_MARK(6)
-        // store: group j = records [ER*j, ER*j + ER) of the phase-shifted layout
-        K* __restrict__ dstK = bufs.k[par];
-        int32_t* __restrict__ dstV = bufs.v[par];
+        K* __restrict__ dstK = bufs.kb(par);
+        int32_t* __restrict__ dstV = bufs.vb(par);
         {
-            const uint32_t ng = (al + T + ER - 1) / ER;
+            const uint32_t wid = ctid >> 5;
+            const uint32_t rs = al + min(T, VT * 32 * wid), re = al + min(T, VT * 32 * (wid + 1));
             const uint64_t gbase = out - al;  // global element of record index 0
-            for (uint32_t j = ctid; j < ng; j += NC) {
-                const uint32_t r0 = j * ER;
-                if (r0 >= al && r0 + ER <= al + T) {
+            if (rs < re) {
+                const uint32_t g0 = (rs + ER - 1) / ER, g1 = re / ER;
+                for (uint32_t j = g0 + clane; j < g1; j += 32) {
+                    const uint32_t r0 = j * ER;
                     const uint4* src = reinterpret_cast<const uint4*>(orec + r0);
                     if (sizeof(K) == 4) {
                         const uint4 q0 = src[0], q1 = src[1];  // (k0,v0,k1,v1) (k2,v2,k3,v3)
@@ -732,22 +736,28 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                         *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.y, q1.x, q1.y);
                         *reinterpret_cast<uint2*>(dstV + gbase + r0) = make_uint2(q0.z, q1.z);
                     }
-                } else {
-                    for (uint32_t t = 0; t < ER; ++t) {
-                        const uint32_t rr = r0 + t;
-                        if (rr >= al && rr < al + T) {
-                            const Rec<K> rec = orec[(rr)];
-                            dstK[gbase + rr] = rec.k;
-                            dstV[gbase + rr] = rec.v;
-                        }
-                    }
+                }
+                // head [rs, min(re, g0*ER)) on lanes 0..ER-1, tail [max(rs, g1*ER), re) on lanes 16..
+                // (a range inside one group is written twice, with the same data)
+                uint32_t rr = INF32;
+                if (clane < ER) rr = rs + clane < min(re, g0 * ER) ? rs + clane : INF32;
+                if (clane >= 16 && clane < 16 + ER) {
+                    const uint32_t t0 = max(rs, g1 * ER) + (clane - 16);
+                    rr = t0 < re ? t0 : INF32;
+                }
+                if (rr != INF32) {
+                    const Rec<K> rec = orec[rr];
+                    dstK[gbase + rr] = rec.k;
+                    dstV[gbase + rr] = rec.v;
                 }
             }
         }
-        consumer_sync();  // scratch / slot reads done before the next unit
+        __syncwarp();
+        if (clane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+        // scratch xr is rewritten by the next unit's first pass
+        consumer_sync();
         PT_MARK(7)
         PT_COUNT(8)
-        if (clane == 0) mbar_arrive(&empty[slot]);
     }
 }
 
