@@ -352,7 +352,7 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
 template <class K>
 struct PipeLayout {
     static constexpr uint32_t CAP = pipe_cap<K>();
-    static constexpr uint32_t PADN = CAP + 16;  // record capacity (+ over-read / don't-care slack)
+    static constexpr uint32_t PADN = CAP + pipe_vt<K>() + 16;  // record capacity (+ over-read / don't-care slack)
     static_assert(PADN >= CAP + pipe_vt<K>() - 1, "record slack must hold a thread's don't-care outputs");
     static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
     // slot = TMA landing zone of the k key windows + k value windows (SoA, 16B
