@@ -48,6 +48,26 @@ size_t form_smem_bytes(uint32_t m) {
     return s;
 }
 
+// Largest j in [0, r) with b[j] <= x (b ascending, b[0] = 0 <= x), by a warp
+// (33-ary search: one probe per lane and round; all lanes return j).
+PS_DEV uint32_t warp_last_le(const uint32_t* __restrict__ b, uint32_t r, uint32_t x) {
+    const uint32_t lane = lane_id();
+    uint32_t lo = 0, hi = r;  // b[lo] <= x, answer in [lo, hi)
+    while (hi - lo > 32) {
+        const uint32_t span = hi - lo;
+        const uint32_t probe = lo + (uint32_t)(((uint64_t)span * (lane + 1)) / 33);
+        const uint32_t c = __popc(__ballot_sync(PS_FULL, b[probe] <= x));
+        // probes 0..c-1 satisfy b <= x
+        const uint32_t nlo = c ? lo + (uint32_t)(((uint64_t)span * c) / 33) : lo;
+        const uint32_t nhi = c < 32 ? lo + (uint32_t)(((uint64_t)span * (c + 1)) / 33) : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const uint32_t idx = lo + lane;
+    const bool p = idx < hi && b[idx] <= x;
+    return lo + __popc(__ballot_sync(PS_FULL, p)) - 1;
+}
+
 template <class K, bool ARGSORT>
 __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs, uint64_t n,
                                                                    const uint32_t* __restrict__ b,
@@ -72,20 +92,14 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     const uint64_t t0 = (uint64_t)blockIdx.x * FORM_TILE;
     const uint64_t t1 = min(t0 + FORM_TILE, n);
     const uint32_t tid = threadIdx.x;
-    if (tid == 0) {
-        // last leaf with b <= t0, last leaf with b <= t1-1
-        uint32_t lo = 0, hi = r;  // b[lo] <= t0 < b[hi]
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (b[mid] <= t0) lo = mid; else hi = mid;
+    if (tid < 32) {
+        // last leaf with b <= t0 and last leaf with b <= t1-1: 32-ary warp searches
+        const uint32_t lo = warp_last_le(b, r, (uint32_t)t0);
+        const uint32_t lo2 = warp_last_le(b, r, (uint32_t)(t1 - 1));
+        if (tid == 0) {
+            s_first = lo;
+            s_cnt = lo2 - lo + 1;
         }
-        uint32_t lo2 = lo, hi2 = r;
-        while (hi2 - lo2 > 1) {
-            uint32_t mid = (lo2 + hi2) >> 1;
-            if (b[mid] <= t1 - 1) lo2 = mid; else hi2 = mid;
-        }
-        s_first = lo;
-        s_cnt = lo2 - lo + 1;
     }
     __syncthreads();
     const uint32_t first = s_first, cnt = s_cnt;
@@ -97,47 +111,73 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     __syncthreads();
 
     // ---- natural leaves: copy / mirrored swap ------------------------------
-    for (uint64_t pos = t0 + tid; pos < t1; pos += FORM_THREADS) {
-        uint32_t lo = 0, hi = cnt;  // sb[lo] <= pos < sb[hi]
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (sb[mid] <= pos) lo = mid; else hi = mid;
-        }
-        const uint64_t bj = sb[lo], ej = sb[lo + 1];
-        const uint32_t len = (uint32_t)(ej - bj);
-        if (snat[lo] < len) continue;  // extended window, below
-        const uint32_t par = spar[lo];
-        K* dk = bufs.kb(par);
-        int32_t* dv = bufs.vb(par);
-        bool desc = false;
-        if (len >= 2) {
-            const uint64_t q = bj + 1;
-            desc = !((ty[q >> 5] >> (q & 31)) & 1u);
-        }
-        if (!desc) {
-            if (par) {
-                dk[pos] = K0[pos];
-                dv[pos] = ARGSORT ? (int32_t)pos : V0[pos];
-            } else if (ARGSORT) {
-                V0[pos] = (int32_t)pos;
+    // Positions are handled FORM_BATCH at a time per thread: all loads of a
+    // batch are issued before its stores (memory-level parallelism).  Every
+    // address a thread reads is written only by that thread (a mirrored pair
+    // belongs to the owner of its lower position), so the reordering is safe.
+    constexpr uint32_t FORM_BATCH = 4;
+    enum : uint8_t { F_NONE = 0, F_COPY = 1, F_ARGV = 2, F_SWAP = 3 };
+    for (uint64_t pos0 = t0 + tid; pos0 < t1; pos0 += FORM_THREADS * FORM_BATCH) {
+        uint8_t act[FORM_BATCH];
+        uint8_t parb[FORM_BATCH];
+        uint64_t mir[FORM_BATCH];
+        K ka[FORM_BATCH], kb[FORM_BATCH];
+        int32_t va[FORM_BATCH], vb[FORM_BATCH];
+#pragma unroll
+        for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+            const uint64_t pos = pos0 + (uint64_t)u * FORM_THREADS;
+            act[u] = F_NONE;
+            parb[u] = 0;
+            mir[u] = pos;
+            if (pos >= t1) continue;
+            uint32_t lo = 0, hi = cnt;  // sb[lo] <= pos < sb[hi]
+            while (hi - lo > 1) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (sb[mid] <= pos) lo = mid; else hi = mid;
             }
-        } else {
-            const uint64_t mirror = bj + ej - 1 - pos;
+            const uint64_t bj = sb[lo], ej = sb[lo + 1];
+            const uint32_t len = (uint32_t)(ej - bj);
+            if (snat[lo] < len) continue;  // extended window, below
+            const uint32_t par = spar[lo];
+            parb[u] = (uint8_t)par;
+            bool desc = false;
+            if (len >= 2) {
+                const uint64_t q = bj + 1;
+                desc = !((ty[q >> 5] >> (q & 31)) & 1u);
+            }
+            const uint64_t mirror = desc ? bj + ej - 1 - pos : pos;
+            mir[u] = mirror;
             if (pos < mirror) {
-                const K ka = K0[pos], kb = K0[mirror];
-                const int32_t va = ARGSORT ? (int32_t)pos : V0[pos];
-                const int32_t vb = ARGSORT ? (int32_t)mirror : V0[mirror];
-                dk[pos] = kb;
-                dv[pos] = vb;
-                dk[mirror] = ka;
-                dv[mirror] = va;
+                act[u] = F_SWAP;
+                ka[u] = K0[pos];
+                kb[u] = K0[mirror];
+                va[u] = ARGSORT ? (int32_t)pos : V0[pos];
+                vb[u] = ARGSORT ? (int32_t)mirror : V0[mirror];
             } else if (pos == mirror) {
                 if (par) {
-                    dk[pos] = K0[pos];
-                    dv[pos] = ARGSORT ? (int32_t)pos : V0[pos];
+                    act[u] = F_COPY;
+                    ka[u] = K0[pos];
+                    va[u] = ARGSORT ? (int32_t)pos : V0[pos];
                 } else if (ARGSORT) {
-                    V0[pos] = (int32_t)pos;
+                    act[u] = F_ARGV;
                 }
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+            const uint64_t pos = pos0 + (uint64_t)u * FORM_THREADS;
+            K* dk = bufs.kb(parb[u]);
+            int32_t* dv = bufs.vb(parb[u]);
+            if (act[u] == F_SWAP) {
+                dk[pos] = kb[u];
+                dv[pos] = vb[u];
+                dk[mir[u]] = ka[u];
+                dv[mir[u]] = va[u];
+            } else if (act[u] == F_COPY) {
+                dk[pos] = ka[u];
+                dv[pos] = va[u];
+            } else if (act[u] == F_ARGV) {
+                V0[pos] = (int32_t)pos;
             }
         }
     }
@@ -172,15 +212,30 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     if (tid == 0) woff[nwin] = wtot;
     __syncthreads();
     // stage
-    for (uint32_t e = tid; e < wtot; e += FORM_THREADS) {
-        uint32_t lo = 0, hi = nwin;
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (woff[mid] <= e) lo = mid; else hi = mid;
+    for (uint32_t e0 = tid; e0 < wtot; e0 += FORM_THREADS * 4) {
+        K kk[4];
+        int32_t vv[4];
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+            const uint32_t e = e0 + u * FORM_THREADS;
+            if (e >= wtot) continue;
+            uint32_t lo = 0, hi = nwin;
+            while (hi - lo > 1) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (woff[mid] <= e) lo = mid; else hi = mid;
+            }
+            const uint64_t p = (uint64_t)sb[wlist[lo]] + (e - woff[lo]);
+            kk[u] = K0[p];
+            vv[u] = ARGSORT ? (int32_t)p : V0[p];
         }
-        const uint64_t p = (uint64_t)sb[wlist[lo]] + (e - woff[lo]);
-        wk[e] = K0[p];
-        wv[e] = ARGSORT ? (int32_t)p : V0[p];
+#pragma unroll
+        for (uint32_t u = 0; u < 4; ++u) {
+            const uint32_t e = e0 + u * FORM_THREADS;
+            if (e < wtot) {
+                wk[e] = kk[u];
+                wv[e] = vv[u];
+            }
+        }
     }
     __syncthreads();
     for (uint32_t e = tid; e < wtot; e += FORM_THREADS) {

@@ -278,14 +278,33 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
     int32_t* ov = sv + SMALL_NODE;
     const K* __restrict__ srcK = bufs.kb(nd.parity ^ 1);
     const int32_t* __restrict__ srcV = bufs.vb(nd.parity ^ 1);
-    for (uint32_t i = lane; i < size; i += 32) {
-        sk[i] = srcK[(uint64_t)p0 + i];
-        sv[i] = srcV[(uint64_t)p0 + i];
+    {
+        // all loads issued before the shared-memory stores
+        constexpr uint32_t PER = SMALL_NODE / 32;
+        K kk[PER];
+        int32_t vv[PER];
+#pragma unroll
+        for (uint32_t u = 0; u < PER; ++u) {
+            const uint32_t i = lane + 32 * u;
+            if (i < size) {
+                kk[u] = srcK[(uint64_t)p0 + i];
+                vv[u] = srcV[(uint64_t)p0 + i];
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < PER; ++u) {
+            const uint32_t i = lane + 32 * u;
+            if (i < size) {
+                sk[i] = kk[u];
+                sv[i] = vv[u];
+            }
+        }
     }
     if (lane < 5) s_off[warp][lane] = lane <= w ? nd.pos[lane] - p0 : size;
     __syncwarp();
     const uint32_t* off = s_off[warp];
     const uint32_t o1 = off[1], o2 = w > 2 ? off[2] : size, o3 = w > 3 ? off[3] : size;
+#pragma unroll 4
     for (uint32_t i = lane; i < size; i += 32) {
         const uint32_t a = (i >= o1) + (i >= o2) + (i >= o3);
         const K x = sk[i];

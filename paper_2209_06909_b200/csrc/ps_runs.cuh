@@ -262,7 +262,23 @@ __global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restri
 // Dynamic smem of compose/top/down: TSCAN_FAN*(m+1) uint64.
 PS_DEV uint32_t stage_tables(const uint64_t* __restrict__ in, uint32_t j0, uint32_t cnt, uint32_t M1,
                              uint64_t span, const uint32_t* __restrict__ Ft, uint64_t* s_tab, uint64_t* s_F) {
-    for (uint32_t i = threadIdx.x; i < cnt * M1; i += blockDim.x) s_tab[i] = in[(uint64_t)j0 * M1 + i];
+    // batches of 8 independent loads per thread (a plain load->store loop would
+    // wait one memory latency per element)
+    const uint32_t tot = cnt * M1;
+    const uint64_t* src = in + (uint64_t)j0 * M1;
+    for (uint32_t base = 0; base < tot; base += 8 * blockDim.x) {
+        uint64_t v[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * blockDim.x + threadIdx.x;
+            v[u] = i < tot ? src[i] : 0;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < tot) s_tab[i] = v[u];
+        }
+    }
     for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) s_F[k] = Ft[((uint64_t)(j0 + k) * span) / TILE];
     return cnt;
 }
@@ -357,7 +373,7 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
     build_chain_view(ty, n, g, ngroups, Fg, s_chg, s_nzn, cv, m);
     const uint32_t M1 = m + 1;
     const uint64_t tile0 = (uint64_t)g * TILES_PER_GROUP;
-    for (uint32_t i = threadIdx.x; i < TILES_PER_GROUP * M1; i += blockDim.x) s_tab[i] = tile_tab[tile0 * M1 + i];
+    for (uint32_t i = threadIdx.x; i < TILES_PER_GROUP * M1; i += blockDim.x) s_tab[i] = tile_tab[tile0 * M1 + i];  // <= 8 per thread
     if (threadIdx.x < TILES_PER_GROUP) s_F[threadIdx.x] = Ft[tile0 + threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -382,9 +382,25 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         if (nd.flags & 1) {
             sum->spine_cost[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size;
             sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_NODE;
-        } else {
-            atomicAdd(&sum->level_cost[nd.power], (unsigned long long)size);
-            if (size <= SMALL_NODE) atomicAdd(&sum->level_small[nd.power], 1u);
+        }
+    }
+    // per-level cost / small counts: one atomic per distinct power per warp
+    // (main nodes are level-sorted, so a warp mostly holds one power)
+    {
+        uint32_t key = 0xFFFFFFFFu, sz = 0, sm = 0;
+        if (i < nnodes) {
+            const Node& nd = nodes[i];
+            if (!(nd.flags & 1)) {
+                key = nd.power;
+                sz = nd.pos[nd.arity] - nd.pos[0];
+                sm = sz <= SMALL_NODE;
+            }
+        }
+        const uint32_t grp = __match_any_sync(PS_FULL, key);
+        const uint32_t gsz = __reduce_add_sync(grp, sz), gsm = __reduce_add_sync(grp, sm);
+        if (key != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(grp) - 1)) {
+            atomicAdd(&sum->level_cost[key], (unsigned long long)gsz);
+            if (gsm) atomicAdd(&sum->level_small[key], gsm);
         }
     }
     for (int d = 16; d; d >>= 1) {
@@ -394,12 +410,26 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         m4 += __shfl_xor_sync(PS_FULL, m4, d);
         slack += __shfl_xor_sync(PS_FULL, slack, d);
     }
-    if (lane_id() == 0 && cost) {
-        atomicAdd(&sum->merge_cost, cost);
-        atomicAdd(&sum->merges[2], m2);
-        atomicAdd(&sum->merges[3], m3);
-        atomicAdd(&sum->merges[4], m4);
-        atomicAdd(&sum->scan_slack, slack);
+    // block reduction, then one set of atomics per block
+    __shared__ unsigned long long s_red[5][32];
+    const uint32_t wv = threadIdx.x >> 5;
+    if (lane_id() == 0) {
+        s_red[0][wv] = cost;
+        s_red[1][wv] = m2;
+        s_red[2][wv] = m3;
+        s_red[3][wv] = m4;
+        s_red[4][wv] = slack;
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        unsigned long long t = 0;
+        for (uint32_t q = 0; q < (blockDim.x + 31) / 32; ++q) t += s_red[threadIdx.x][q];
+        if (t) {
+            unsigned long long* dst = threadIdx.x == 0 ? &sum->merge_cost
+                                    : threadIdx.x == 4 ? &sum->scan_slack
+                                                       : &sum->merges[threadIdx.x + 1];
+            atomicAdd(dst, t);
+        }
     }
 }
 
