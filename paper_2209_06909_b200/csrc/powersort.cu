@@ -341,8 +341,12 @@ struct MergeRunner {
     size_t psmem, ssmem;
     uint32_t pipe_grid_max;
 
-    int init(Bufs<K> b, const Node* nd, const uint32_t* chunk2node, uint4* ct, uint32_t* e, cudaStream_t st) {
+    uint64_t nelem;  // elements in each buffer
+
+    int init(Bufs<K> b, uint64_t n, const Node* nd, const uint32_t* chunk2node, uint4* ct, uint32_t* e,
+             cudaStream_t st) {
         bufs = b;
+        nelem = n;
         nodes = nd;
         c2n = chunk2node;
         cuts = ct;
@@ -360,12 +364,14 @@ struct MergeRunner {
         return PS_OK;
     }
 
-    int stage(uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint32_t nsmall, Prof* prof, int stage_id) {
+    int stage(uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint32_t nsmall, uint32_t small_max, Prof* prof,
+              int stage_id) {
         if (nhi <= nlo) return PS_OK;
         const uint32_t nbig = (nhi - nlo) - nsmall;
         if (nsmall) {
-            merge_small_kernel<K><<<grid_for(nhi - nlo, SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(bufs, nodes, nlo,
-                                                                                                    nhi);
+            const uint32_t G = small_group(small_max);
+            merge_small_kernel<K><<<grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(
+                bufs, nodes, nlo, nhi, G);
             PS_LAUNCH_CHECK();
         }
         if (c1 > c0) {
@@ -377,7 +383,7 @@ struct MergeRunner {
             }
             const uint32_t units = c1 - c0;
             merge_pipe_kernel<K><<<std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s>>>(
-                bufs, nodes, c2n, cuts, c0, units, err);
+                bufs, nelem, nodes, c2n, cuts, c0, units, err);
             PS_LAUNCH_CHECK();
         }
         return PS_OK;
@@ -568,24 +574,26 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     // ---- N3/N4: merges, stage by stage ------------------------------------------
     if (nnodes) {
         MergeRunner<K> mr;
-        int rc = mr.init(bufs, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts), err, s);
+        int rc = mr.init(bufs, (uint64_t)n, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts),
+                         err, s);
         if (rc) return rc;
         int stage = 0;
-        auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint64_t cost, uint32_t nsmall) -> int {
+        auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint64_t cost, uint32_t nsmall, uint32_t small_max) -> int {
             if (nhi <= nlo) return PS_OK;
             const uint32_t c0 = info.node_chunk[nlo], c1 = info.node_chunk[nhi];
             const int ph = prof.begin(4, stage, nhi - nlo, c1 - c0, 2 * (int64_t)cost * rec_bytes);
-            int rc2 = mr.stage(nlo, nhi, c0, c1, nsmall, &prof, stage);
+            int rc2 = mr.stage(nlo, nhi, c0, c1, nsmall, small_max, &prof, stage);
             prof.end(ph);
             stage++;
             return rc2;
         };
         for (int p = (int)NPOW - 1; p >= 1; --p) {
-            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p]);
+            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p],
+                           info.s.level_small_max[p]);
             if (rc) return rc;
         }
         for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
-            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i]);
+            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i], SMALL_NODE);
             if (rc) return rc;
         }
     }
@@ -745,7 +753,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
         nd.parity = (uint8_t)parity;
         nd.probe = 0;
         const uint32_t size = pos[arity] - pos[0];
-        uint32_t nch = size <= SMALL_NODE ? 0 : 1;
+        uint32_t nch = size <= SMALL_KERNEL_MAX ? 0 : 1;
         if (size > cap)
             for (uint32_t a = 0; a < arity; ++a) nch += (pos[a + 1] - pos[a] - 1) / (cap / arity);
         nd.nchunks = nch;
@@ -796,9 +804,9 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
             b.v[1] = at<int32_t>(ws, L.tv);
         }
         MergeRunner<K> mr;
-        int rc = mr.init(b, d_nodes, d_c2n, d_cuts, d_err, s);
+        int rc = mr.init(b, slab, d_nodes, d_c2n, d_cuts, d_err, s);
         if (rc) return rc;
-        rc = mr.stage(0, (uint32_t)nds.size(), 0, (uint32_t)c2n.size(), nsmall, nullptr, (int)lvl);
+        rc = mr.stage(0, (uint32_t)nds.size(), 0, (uint32_t)c2n.size(), nsmall, SMALL_NODE, nullptr, (int)lvl);
         if (rc) return rc;
         PS_CUDA(cudaStreamSynchronize(s));  // host node/chunk tables are reused by the next level
     }

@@ -32,6 +32,15 @@ constexpr uint32_t MERGE_THREADS = 256;
 constexpr uint32_t MERGE_VT = CHUNK_CAP / MERGE_THREADS;  // 16 records per thread
 constexpr uint32_t MAX_WAY = 4;
 constexpr uint32_t SMALL_NODE = 512;  // nodes up to this size: one warp each (no chunking)
+// nodes of at most SMALL_KERNEL_MAX records are merged by merge_small_kernel
+// (<= SMALL_NODE); all others by the TMA pipeline (0: the pipeline takes all).
+// Tiny nodes stay on the warp kernel: a pipeline unit holds at most MAXSEG of
+// them and its producer then dominates.
+#ifndef PS_SMALL_MAX
+#define PS_SMALL_MAX 256
+#endif
+constexpr uint32_t SMALL_KERNEL_MAX = PS_SMALL_MAX;
+static_assert(SMALL_KERNEL_MAX <= SMALL_NODE, "small-kernel threshold exceeds its capacity");
 
 constexpr uint32_t INF32 = 0xFFFFFFFFu;
 constexpr uint32_t MAX_SPINE = 256;
@@ -80,6 +89,7 @@ struct Summary {
     unsigned long long level_cost[NPOW];     // merge cost per power bucket
     unsigned long long spine_cost[MAX_SPINE]; // merge cost per merge_down node
     uint32_t level_small[NPOW];               // nodes <= SMALL_NODE per power bucket
+    uint32_t level_small_max[NPOW];           // largest small node per power bucket
     uint32_t spine_small[MAX_SPINE];
 };
 

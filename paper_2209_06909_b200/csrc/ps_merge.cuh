@@ -250,82 +250,123 @@ constexpr uint32_t PIPE_SLOTS = PS_SLOTS;  // input slots per CTA (TMA multi-buf
 PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(PIPE_CONSUMERS) : "memory"); }
 
 // ---------------------------------------------------------------------------
-// Small nodes (size <= SMALL_NODE): one warp per node, straight from global.
+// Small nodes (size <= SMALL_NODE): one warp per group of G consecutive nodes
+// of the batch (G * largest small node <= SMALL_NODE, chosen by the host per
+// level), packed into the warp's shared-memory window.  Loads are batched;
+// each record's output index is its index in its run plus its rank in every
+// other run of its node (<= for earlier runs, < for later: the stable order).
 constexpr uint32_t SMALL_WARPS = 8;
 
 template <class K>
 size_t merge_small_smem_bytes() {
-    return (size_t)SMALL_WARPS * SMALL_NODE * 2 * (sizeof(K) + 4);
+    return (size_t)SMALL_WARPS * SMALL_NODE * (2 * (sizeof(K) + 4) + 1);
 }
 
 template <class K>
 __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
-                                                                       uint32_t nlo, uint32_t nhi) {
+                                                                       uint32_t nlo, uint32_t nhi, uint32_t G) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ uint32_t s_off[SMALL_WARPS][8];
+    // per node of the group: packed start, global start, run starts (relative), size, parity
+    __shared__ uint32_t s_pre[SMALL_WARPS][33];
+    __shared__ uint32_t s_p0[SMALL_WARPS][32];
+    __shared__ uint32_t s_off[SMALL_WARPS][32][4];
+    __shared__ uint8_t s_par[SMALL_WARPS][32];
     const uint32_t warp = warp_id(), lane = lane_id();
-    const uint32_t idx = nlo + blockIdx.x * SMALL_WARPS + warp;
-    if (idx >= nhi) return;
-    const Node nd = nodes[idx];
-    const uint32_t w = nd.arity;
-    const uint32_t p0 = nd.pos[0];
-    const uint32_t size = nd.pos[w] - p0;
-    if (size > SMALL_NODE) return;
-    uint8_t* base = smem + (size_t)warp * SMALL_NODE * 2 * (sizeof(K) + 4);
+    const uint64_t first64 = (uint64_t)nlo + ((uint64_t)blockIdx.x * SMALL_WARPS + warp) * G;
+    if (first64 >= nhi) return;
+    const uint32_t first = (uint32_t)first64;
+    const uint32_t cnt = min(G, nhi - first);
+    uint8_t* base = smem + (size_t)warp * SMALL_NODE * (2 * (sizeof(K) + 4) + 1);
     K* sk = reinterpret_cast<K*>(base);
     K* ok = sk + SMALL_NODE;
     int32_t* sv = reinterpret_cast<int32_t*>(ok + SMALL_NODE);
     int32_t* ov = sv + SMALL_NODE;
-    const K* __restrict__ srcK = bufs.kb(nd.parity ^ 1);
-    const int32_t* __restrict__ srcV = bufs.vb(nd.parity ^ 1);
+    uint8_t* snid = reinterpret_cast<uint8_t*>(ov + SMALL_NODE);
+    uint32_t sz = 0;
+    if (lane < cnt) {
+        const Node nd = nodes[first + lane];
+        const uint32_t w = nd.arity, p0 = nd.pos[0], size = nd.pos[w] - p0;
+        if (size <= SMALL_KERNEL_MAX) {  // bigger nodes of the batch belong to the pipe kernel
+            sz = size;
+            s_p0[warp][lane] = p0;
+            s_par[warp][lane] = nd.parity;
+#pragma unroll
+            for (uint32_t a = 0; a < 4; ++a) s_off[warp][lane][a] = a < w ? nd.pos[a] - p0 : size;
+        }
+    }
+    uint32_t inc = sz;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(PS_FULL, inc, d);
+        if (lane >= (uint32_t)d) inc += y;
+    }
+    s_pre[warp][lane + 1] = inc;
+    if (lane == 0) s_pre[warp][0] = 0;
+    const uint32_t total = __shfl_sync(PS_FULL, inc, 31);
+    __syncwarp();
+    const uint32_t* pre = s_pre[warp];
+    if (total > SMALL_NODE) return;  // host chose G too large (cannot happen)
+    constexpr uint32_t PER = SMALL_NODE / 32;
     {
-        // all loads issued before the shared-memory stores
-        constexpr uint32_t PER = SMALL_NODE / 32;
         K kk[PER];
         int32_t vv[PER];
 #pragma unroll
         for (uint32_t u = 0; u < PER; ++u) {
             const uint32_t i = lane + 32 * u;
-            if (i < size) {
-                kk[u] = srcK[(uint64_t)p0 + i];
-                vv[u] = srcV[(uint64_t)p0 + i];
+            if (i < total) {
+                uint32_t lo = 0, hi = cnt;  // pre[lo] <= i < pre[hi]
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (pre[mid] <= i) lo = mid; else hi = mid;
+                }
+                snid[i] = (uint8_t)lo;
+                const uint64_t p = (uint64_t)s_p0[warp][lo] + (i - pre[lo]);
+                const uint32_t sp = s_par[warp][lo] ^ 1u;
+                kk[u] = bufs.kb(sp)[p];
+                vv[u] = bufs.vb(sp)[p];
             }
         }
 #pragma unroll
         for (uint32_t u = 0; u < PER; ++u) {
             const uint32_t i = lane + 32 * u;
-            if (i < size) {
+            if (i < total) {
                 sk[i] = kk[u];
                 sv[i] = vv[u];
             }
         }
     }
-    if (lane < 5) s_off[warp][lane] = lane <= w ? nd.pos[lane] - p0 : size;
     __syncwarp();
-    const uint32_t* off = s_off[warp];
-    const uint32_t o1 = off[1], o2 = w > 2 ? off[2] : size, o3 = w > 3 ? off[3] : size;
 #pragma unroll 4
-    for (uint32_t i = lane; i < size; i += 32) {
-        const uint32_t a = (i >= o1) + (i >= o2) + (i >= o3);
+    for (uint32_t i = lane; i < total; i += 32) {
+        const uint32_t j = snid[i];
+        const uint32_t nb = pre[j], q = i - nb;
+        const uint32_t* off = s_off[warp][j];
+        const uint32_t o1 = off[1], o2 = off[2], o3 = off[3], oe = pre[j + 1] - nb;
+        const uint32_t a = (q >= o1) + (q >= o2) + (q >= o3);
         const K x = sk[i];
-        uint32_t rank = i - off[a];
-#pragma unroll
-        for (uint32_t b = 0; b < 4; ++b) {
-            if (b < w && b != a) {
-                const uint32_t ob = off[b], lb = off[b + 1] - ob;
-                rank += b < a ? count_pred<K, true>(sk + ob, lb, x) : count_pred<K, false>(sk + ob, lb, x);
-            }
-        }
-        ok[rank] = x;
-        ov[rank] = sv[i];
+        uint32_t rank = q - (a == 0 ? 0u : a == 1 ? o1 : a == 2 ? o2 : o3);
+        const K* nk = sk + nb;
+        if (a != 0) rank += count_pred<K, true>(nk, o1, x);
+        if (a != 1) rank += a > 1 ? count_pred<K, true>(nk + o1, o2 - o1, x) : count_pred<K, false>(nk + o1, o2 - o1, x);
+        if (a != 2) rank += a > 2 ? count_pred<K, true>(nk + o2, o3 - o2, x) : count_pred<K, false>(nk + o2, o3 - o2, x);
+        if (a != 3) rank += count_pred<K, false>(nk + o3, oe - o3, x);
+        ok[nb + rank] = x;
+        ov[nb + rank] = sv[i];
     }
     __syncwarp();
-    K* __restrict__ dstK = bufs.kb(nd.parity);
-    int32_t* __restrict__ dstV = bufs.vb(nd.parity);
-    for (uint32_t i = lane; i < size; i += 32) {
-        dstK[(uint64_t)p0 + i] = ok[i];
-        dstV[(uint64_t)p0 + i] = ov[i];
+#pragma unroll 4
+    for (uint32_t i = lane; i < total; i += 32) {
+        const uint32_t j = snid[i];
+        const uint64_t p = (uint64_t)s_p0[warp][j] + (i - pre[j]);
+        bufs.kb(s_par[warp][j])[p] = ok[i];
+        bufs.vb(s_par[warp][j])[p] = ov[i];
     }
+}
+
+// nodes per warp for a batch whose largest small node has `maxsz` records
+inline uint32_t small_group(uint32_t maxsz) {
+    if (maxsz == 0) return 1;
+    const uint32_t g = SMALL_NODE / maxsz;
+    return g < 1 ? 1 : (g > 32 ? 32 : g);
 }
 
 // ---------------------------------------------------------------------------
@@ -368,25 +409,38 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
 };
 
 
+// Units hold up to MAXSEG segments; a segment is a contiguous chunk range of
+// one node (a unit of one segment may be several chunks of one node; several
+// segments pack consecutive whole small-to-mid nodes or chunk ranges).
+constexpr uint32_t MAXSEG = 32;
+
 template <class K>
 struct PipeLayout {
     static constexpr uint32_t CAP = pipe_cap<K>();
     static constexpr uint32_t PADN = CAP + pipe_vt<K>() + 16;  // record capacity (+ over-read / don't-care slack)
     static_assert(PADN >= CAP + pipe_vt<K>() - 1, "record slack must hold a thread's don't-care outputs");
     static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
-    // slot = TMA landing zone of the k key windows + k value windows (SoA, 16B
-    // alignment slack each), and afterwards the padded records of the last pass
-    static constexpr uint32_t KEY_BYTES = align16c(CAP * (uint32_t)sizeof(K)) + MAX_WAY * 32u;
-    static constexpr uint32_t VAL_BYTES = align16c(CAP * 4u) + MAX_WAY * 32u;
+    // slot = TMA landing zone of the key windows + value windows of all segments
+    // (SoA, <= 31 bytes of 16-byte alignment slack per window), and afterwards
+    // the records of the last pass
+    static constexpr uint32_t KEY_BYTES = align16c(CAP * (uint32_t)sizeof(K)) + MAXSEG * MAX_WAY * 32u;
+    static constexpr uint32_t VAL_BYTES = align16c(CAP * 4u) + MAXSEG * MAX_WAY * 32u;
     static constexpr uint32_t SLOT = align16c(cmax(KEY_BYTES + VAL_BYTES, PADN * RECB));
-    // scratch: first-pass records X || Y (or the 2-way output)
+    // scratch: first-pass records X || Y of every segment (or the 2-way output)
     static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
 };
 
+struct PipeSeg {
+    uint64_t out;  // global element index of the segment's first output
+    uint32_t koff[4], voff[4], len[4];  // window byte offsets in the slot, lengths (0 past the arity)
+    uint32_t w, par, T, lx;             // arity, output parity, records, |X| = len[0] + len[1]
+};
+
 struct PipeDesc {
-    uint64_t out;  // global element index of the unit's first output
-    uint32_t koff[4], voff[4], len[4];
-    uint32_t T, w, par, done;
+    uint32_t nseg, done, end1, end2;
+    uint32_t s1[2 * MAXSEG];  // pass-1 layout: X of segment s at s1[2s], Y at s1[2s+1] (VT-aligned)
+    uint32_t s2[MAXSEG];      // pass-2 layout: output of segment s at s2[s] (VT-aligned)
+    PipeSeg seg[MAXSEG];
 };
 
 template <class K>
@@ -483,18 +537,31 @@ struct Win {
     uint32_t len;
 };
 
+// largest p in [0, n) with tab[p] <= x (tab ascending, tab[0] == 0 <= x)
+PS_DEV uint32_t last_le(const uint32_t* tab, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (tab[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
 template <class K>
-__global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
+__global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, uint64_t nelem,
+                                                                  const Node* __restrict__ nodes,
                                                                   const uint32_t* __restrict__ chunk2node,
                                                                   const uint4* __restrict__ cuts, uint32_t c0,
                                                                   uint32_t nchunks, uint32_t* err) {
     using LY = PipeLayout<K>;
+    constexpr uint32_t VT = pipe_vt<K>();
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* scratch = smem + PIPE_SLOTS * LY::SLOT;
     PipeDesc* desc = reinterpret_cast<PipeDesc*>(scratch + LY::SCRATCH);
     uint64_t* bars = reinterpret_cast<uint64_t*>(desc + PIPE_SLOTS);
     uint64_t* full = bars;                // [PIPE_SLOTS]
     uint64_t* empty = bars + PIPE_SLOTS;  // [PIPE_SLOTS]
+    __shared__ uint64_t s_e0[MAXSEG][MAX_WAY];  // producer: global element index of each window
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
         for (uint32_t sl = 0; sl < PIPE_SLOTS; ++sl) {
@@ -515,8 +582,9 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         for (uint32_t c = cbeg; c < cend;) {
             // batch descriptors of chunks c .. c+31 (lane l <-> chunk c+l)
             const uint32_t x = c + lane;
-            const bool xv = x < cend;
-            uint32_t nid = xv ? chunk2node[x] : 0;
+            const uint32_t nvalid = min(32u, cend - c);
+            const bool xv = lane < nvalid;
+            uint32_t nid = xv ? chunk2node[x] : INF32;
             Node nd;
             uint4 st = make_uint4(0, 0, 0, 0), en = make_uint4(0, 0, 0, 0);
             if (xv) {
@@ -532,103 +600,172 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     en.w = nd.arity > 3 ? nd.pos[4] - nd.pos[3] : 0;
                 }
             } else {
-                nid = INF32;
+                nd.arity = 2;
+                nd.parity = 0;
+#pragma unroll
+                for (int t = 0; t < 5; ++t) nd.pos[t] = 0;
             }
-            const uint32_t nvalid = min(32u, cend - c);
+            const uint32_t tot = (en.x - st.x) + (en.y - st.y) + (en.z - st.z) + (en.w - st.w);
+            // segment starts (node changes) and inclusive prefixes over the batch:
+            // PT records, PC records + 2 VT per segment (pass layout slack), PS segments
+            const uint32_t nid_prev = __shfl_up_sync(PS_FULL, nid, 1);
+            const uint32_t sgs = (lane == 0 || nid != nid_prev) ? 1u : 0u;
+            uint32_t PT = tot, PC = tot + sgs * 2 * VT, PS = sgs;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t a1 = __shfl_up_sync(PS_FULL, PT, d), a2 = __shfl_up_sync(PS_FULL, PC, d);
+                const uint32_t a3 = __shfl_up_sync(PS_FULL, PS, d);
+                if (lane >= (uint32_t)d) {
+                    PT += a1;
+                    PC += a2;
+                    PS += a3;
+                }
+            }
+            const uint32_t XT = PT - tot, XC = PC - (tot + sgs * 2 * VT), XS = PS - sgs;
             PT_MARK(0)
             uint32_t u = 0;
             while (u < nvalid) {
-                // unit = lanes u..V of the same node with total <= cut_cap
+                // unit = lanes u..V: chunks of one node with <= cut_cap records, or
+                // several segments with sum(records + 2 VT) <= CAP, <= MAXSEG of them
                 const uint32_t nid_u = __shfl_sync(PS_FULL, nid, u);
-                const uint32_t sx = __shfl_sync(PS_FULL, st.x, u), sy = __shfl_sync(PS_FULL, st.y, u);
-                const uint32_t sz = __shfl_sync(PS_FULL, st.z, u), sw = __shfl_sync(PS_FULL, st.w, u);
-                const uint32_t tot = (en.x - sx) + (en.y - sy) + (en.z - sz) + (en.w - sw);
-                const bool ok = lane >= u && lane < nvalid && nid == nid_u && tot <= cut_cap<K>();
-                uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
-                // contiguous run of ok lanes starting at u
+                const uint32_t XTu = __shfl_sync(PS_FULL, XT, u), XCu = __shfl_sync(PS_FULL, XC, u);
+                const uint32_t XSu = __shfl_sync(PS_FULL, XS, u), sgsu = __shfl_sync(PS_FULL, sgs, u);
+                const bool same = nid == nid_u;
+                const uint32_t sumT = PT - XTu;
+                const uint32_t sumC = PC - XCu + (sgsu ? 0u : 2 * VT);
+                const uint32_t nsg = PS - XSu + (sgsu ? 0u : 1u);
+                const bool ok = lane >= u && lane < nvalid &&
+                                (same ? sumT <= cut_cap<K>() : (sumC <= LY::CAP && nsg <= MAXSEG));
+                const uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
                 const uint32_t runlen = __ffs(~bal) ? __ffs(~bal) - 1 : 32 - u;
                 const uint32_t V = u + max(runlen, 1u) - 1;
-                const uint32_t ex = __shfl_sync(PS_FULL, en.x, V), ey = __shfl_sync(PS_FULL, en.y, V);
-                const uint32_t ez = __shfl_sync(PS_FULL, en.z, V), ew = __shfl_sync(PS_FULL, en.w, V);
-                // node fields of lane u
-                uint32_t npos[5];
+                // segments of the unit: starts at u and at node changes in (u, V]
+                const uint32_t mseg = __ballot_sync(PS_FULL, lane >= u && lane <= V && (lane == u || sgs));
+                const uint32_t nseg = __popc(mseg);
+                const bool has = lane < nseg;
+                const uint32_t as = has ? __fns(mseg, 0, lane + 1) : u;
+                const uint32_t bs = (lane + 1 < nseg) ? __fns(mseg, 0, lane + 2) - 1 : V;
+                uint32_t sv4[4], ev4[4], npos[5];
+                sv4[0] = __shfl_sync(PS_FULL, st.x, as);
+                sv4[1] = __shfl_sync(PS_FULL, st.y, as);
+                sv4[2] = __shfl_sync(PS_FULL, st.z, as);
+                sv4[3] = __shfl_sync(PS_FULL, st.w, as);
+                ev4[0] = __shfl_sync(PS_FULL, en.x, bs);
+                ev4[1] = __shfl_sync(PS_FULL, en.y, bs);
+                ev4[2] = __shfl_sync(PS_FULL, en.z, bs);
+                ev4[3] = __shfl_sync(PS_FULL, en.w, bs);
 #pragma unroll
-                for (int t = 0; t < 5; ++t) npos[t] = __shfl_sync(PS_FULL, nd.pos[t], u);
-                const uint32_t w = __shfl_sync(PS_FULL, (uint32_t)nd.arity, u);
-                const uint32_t par = __shfl_sync(PS_FULL, (uint32_t)nd.parity, u);
-                // ---- stage the unit into slot (unit & 1) ----
+                for (int t = 0; t < 5; ++t) npos[t] = __shfl_sync(PS_FULL, nd.pos[t], as);
+                const uint32_t w = __shfl_sync(PS_FULL, (uint32_t)nd.arity, as);
+                const uint32_t par = __shfl_sync(PS_FULL, (uint32_t)nd.parity, as);
+                // per segment (lane s < nseg): windows, region sizes, pass layouts
+                uint32_t len[4], kph[4], vph[4], kb[4], vb[4];
+                uint32_t T = 0, kreg = 0, vreg = 0;
+#pragma unroll
+                for (uint32_t t = 0; t < 4; ++t) {
+                    len[t] = (has && t < w) ? ev4[t] - sv4[t] : 0;
+                    const uint64_t e0 = (uint64_t)npos[t] + sv4[t];
+                    kph[t] = (uint32_t)((e0 * sizeof(K)) & 15);
+                    vph[t] = (uint32_t)((e0 * 4) & 15);
+                    kb[t] = len[t] ? align16c(kph[t] + len[t] * (uint32_t)sizeof(K)) : 0;
+                    vb[t] = len[t] ? align16c(vph[t] + len[t] * 4u) : 0;
+                    T += len[t];
+                    kreg += kb[t];
+                    vreg += vb[t];
+                }
+                const uint32_t LXs = len[0] + len[1], LYs = T - LXs;
+                const bool last = lane + 1 == nseg;
+                const uint32_t px = (LXs + VT - 1) / VT * VT, py = (LYs + VT - 1) / VT * VT;
+                const uint32_t size1 = !has ? 0u : !last ? px + py : (LYs ? px + LYs : LXs);
+                const uint32_t size2 = !has ? 0u : !last ? (T + VT - 1) / VT * VT : T;
+                uint32_t ek = kreg, ev = vreg, e1 = size1, e2 = size2;  // inclusive scans over segments
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t b1 = __shfl_up_sync(PS_FULL, ek, d), b2 = __shfl_up_sync(PS_FULL, ev, d);
+                    const uint32_t b3 = __shfl_up_sync(PS_FULL, e1, d), b4 = __shfl_up_sync(PS_FULL, e2, d);
+                    if (lane >= (uint32_t)d) {
+                        ek += b1;
+                        ev += b2;
+                        e1 += b3;
+                        e2 += b4;
+                    }
+                }
+                const uint32_t end1 = __shfl_sync(PS_FULL, e1, 31), end2 = __shfl_sync(PS_FULL, e2, 31);
+                // ---- stage the unit into slot (unit % PIPE_SLOTS) ----
                 const uint32_t slot = unit % PIPE_SLOTS;
                 if (unit >= PIPE_SLOTS) mbar_wait(&empty[slot], ((unit / PIPE_SLOTS) - 1) & 1);
                 PT_MARK(1)
                 uint8_t* sbase = smem + slot * LY::SLOT;
-                const uint32_t sv4[4] = {sx, sy, sz, sw};
-                const uint32_t ev4[4] = {ex, ey, ez, ew};
-                // lane a (< w) handles keys of window a, lane 4+a values of window a
-                const uint32_t wa = lane & 3;
-                const bool is_val = lane >= 4;
-                uint32_t len = 0, phase = 0, bytes_region = 0, tx = 0;
-                uint64_t e0 = 0;
-                const uint32_t ebytes = is_val ? 4u : (uint32_t)sizeof(K);
-                if (lane < 8 && wa < w) {
-                    len = ev4[wa] - sv4[wa];
-                    e0 = (uint64_t)npos[wa] + sv4[wa];
-                    const uint64_t b0 = e0 * ebytes;
-                    phase = (uint32_t)(b0 & 15);
-                    bytes_region = len ? align16c(phase + len * ebytes) : 0;
-                }
-                // exclusive prefix of region sizes within the key lanes (0..3) and value lanes (4..7)
-                uint32_t pre = 0;
+                PipeDesc& d = desc[slot];
+                if (has) {
+                    PipeSeg& g = d.seg[lane];
+                    uint32_t ko = ek - kreg, vo = LY::KEY_BYTES + (ev - vreg);
+                    uint64_t out = npos[0];
 #pragma unroll
-                for (uint32_t t = 0; t < 4; ++t) {
-                    const uint32_t r = __shfl_sync(PS_FULL, bytes_region, (lane & 4) + t);
-                    if (t < wa) pre += r;
+                    for (uint32_t t = 0; t < 4; ++t) {
+                        g.koff[t] = ko + kph[t];
+                        g.voff[t] = vo + vph[t];
+                        g.len[t] = len[t];
+                        s_e0[lane][t] = (uint64_t)npos[t] + sv4[t];
+                        ko += kb[t];
+                        vo += vb[t];
+                        out += (t < w) ? sv4[t] : 0u;
+                    }
+                    g.out = out;
+                    g.w = w;
+                    g.par = par;
+                    g.T = T;
+                    g.lx = LXs;
+                    const uint32_t b1s = e1 - size1;
+                    d.s1[2 * lane] = b1s;
+                    d.s1[2 * lane + 1] = b1s + px;
+                    d.s2[lane] = e2 - size2;
                 }
-                const uint32_t region = (is_val ? LY::KEY_BYTES : 0u) + pre;
-                if (lane < 8 && wa < w && len) {
-                    const uint8_t* src = is_val ? reinterpret_cast<const uint8_t*>(bufs.vb(par ^ 1))
-                                                : reinterpret_cast<const uint8_t*>(bufs.kb(par ^ 1));
-                    const uint64_t b0 = e0 * ebytes, b1 = (e0 + len) * ebytes;
-                    const uint64_t a0 = b0 & ~15ull, a1 = b1 & ~15ull;
-                    if (a1 > a0) {
-                        tma_load_1d(sbase + region, src + a0, (uint32_t)(a1 - a0), &full[slot]);
-                        tx = (uint32_t)(a1 - a0);
-                    }
-                    // tail bytes [max(a1, b0), b1) with ordinary loads
-                    for (uint64_t bb = (a1 > b0 ? a1 : b0); bb < b1; bb += ebytes) {
-                        if (is_val)
-                            *reinterpret_cast<int32_t*>(sbase + region + (bb - a0)) =
-                                *reinterpret_cast<const int32_t*>(src + bb);
-                        else
-                            *reinterpret_cast<K*>(sbase + region + (bb - a0)) = *reinterpret_cast<const K*>(src + bb);
-                    }
-                }
-                uint32_t txs = tx;
-                for (int d = 16; d; d >>= 1) txs += __shfl_xor_sync(PS_FULL, txs, d);
-                uint32_t total = 0;  // window lengths live in key lanes 0..3
-#pragma unroll
-                for (uint32_t t = 0; t < 4; ++t) total += __shfl_sync(PS_FULL, len, t);
-                if (lane < 8) {
-                    PipeDesc& d = desc[slot];
-                    if (lane < 4) {
-                        d.koff[wa] = region + phase;
-                        d.len[wa] = len;
-                    } else {
-                        d.voff[wa] = region + phase;
-                    }
+                if (lane == 0) {
+                    d.nseg = nseg;
+                    d.done = 0;
+                    d.end1 = end1;
+                    d.end2 = end2;
+                    if (end1 > LY::CAP + VT - 1 || end2 > LY::CAP + VT - 1) atomicOr(err, ERR_CUT);
                 }
                 __syncwarp();
-                if (lane == 0) {
-                    PipeDesc& d = desc[slot];
-                    uint64_t out = npos[0];
-                    for (uint32_t t = 0; t < w; ++t) out += sv4[t];
-                    d.out = out;
-                    d.T = total;
-                    d.w = w;
-                    d.par = par;
-                    d.done = 0;
-                    if (total > cut_cap<K>()) atomicOr(err, ERR_CUT);
-                    mbar_arrive_tx(&full[slot], txs);
+                // window copies: op = (segment, window, keys|values), spread over the lanes
+                uint32_t tx = 0;
+                for (uint32_t op = lane; op < nseg * 8; op += 32) {
+                    const uint32_t sg = op >> 3, t = op & 3;
+                    const bool is_val = (op & 4) != 0;
+                    const PipeSeg& g = d.seg[sg];
+                    const uint32_t ln = g.len[t];
+                    if (ln == 0) continue;
+                    const uint32_t eb = is_val ? 4u : (uint32_t)sizeof(K);
+                    const uint32_t doff = is_val ? g.voff[t] : g.koff[t];  // includes the phase
+                    const uint64_t e0 = s_e0[sg][t];
+                    const uint8_t* src = is_val ? reinterpret_cast<const uint8_t*>(bufs.vb(g.par ^ 1))
+                                                : reinterpret_cast<const uint8_t*>(bufs.kb(g.par ^ 1));
+                    const uint64_t b0 = e0 * eb, b1 = (e0 + ln) * eb;
+                    const uint64_t a0 = b0 & ~15ull, a1 = b1 & ~15ull;
+                    uint8_t* dst = sbase + doff - (uint32_t)(b0 & 15);  // 16-byte aligned region start
+                    const uint64_t r1 = (b1 + 15) & ~15ull;
+                    if (r1 <= nelem * eb) {
+                        // whole region [a0, r1) in one copy: the bytes past the window stay
+                        // inside the source array and land in this window's own slack
+                        tma_load_1d(dst, src + a0, (uint32_t)(r1 - a0), &full[slot]);
+                        tx += (uint32_t)(r1 - a0);
+                        continue;
+                    }
+                    if (a1 > a0) {
+                        tma_load_1d(dst, src + a0, (uint32_t)(a1 - a0), &full[slot]);
+                        tx += (uint32_t)(a1 - a0);
+                    }
+                    // tail bytes [max(a1, b0), b1) at the array end with ordinary loads
+                    for (uint64_t bb = (a1 > b0 ? a1 : b0); bb < b1; bb += eb) {
+                        if (is_val)
+                            *reinterpret_cast<int32_t*>(dst + (bb - a0)) = *reinterpret_cast<const int32_t*>(src + bb);
+                        else
+                            *reinterpret_cast<K*>(dst + (bb - a0)) = *reinterpret_cast<const K*>(src + bb);
+                    }
                 }
+                for (int dd = 16; dd; dd >>= 1) tx += __shfl_xor_sync(PS_FULL, tx, dd);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_tx(&full[slot], tx);
                 PT_MARK(2)
                 PT_COUNT(3)
                 unit++;
@@ -648,8 +785,11 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
 
     // ------------------------------ consumers ---------------------------------
     const uint32_t ctid = tid - 32;
-    const uint32_t clane = ctid & 31;
+    const uint32_t clane = ctid & 31, wid = ctid >> 5;
     Rec<K>* const xr = reinterpret_cast<Rec<K>*>(scratch);
+    constexpr uint32_t ER = sizeof(K) == 4 ? 4 : 2;  // records per 16-byte store group
+    const uint32_t ob = VT * ctid;                   // this thread's first output of a pass layout
+    const uint32_t r0w = VT * 32 * wid, r1w = VT * 32 * (wid + 1);  // this warp's outputs
     PT_START(ctid == 0)
     for (uint32_t i = 0;; ++i) {
         const uint32_t slot = i % PIPE_SLOTS;
@@ -658,94 +798,73 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         PT_USTART
         const PipeDesc& d = desc[slot];
         if (d.done) break;
-        const uint32_t T = d.T, w = d.w, par = d.par;
-        const uint64_t out = d.out;
         uint8_t* sbase = smem + slot * LY::SLOT;
-        Win<K> win[4];
-#pragma unroll
-        for (uint32_t a = 0; a < 4; ++a) {
-            win[a].k = reinterpret_cast<const K*>(sbase + d.koff[a]);
-            win[a].v = reinterpret_cast<const int32_t*>(sbase + d.voff[a]);
-            win[a].len = a < w ? d.len[a] : 0;
-        }
-        auto wincur = [&](uint32_t a, uint32_t b, uint32_t base, uint32_t o0, uint32_t o1) {
+        Rec<K>* const orec = reinterpret_cast<Rec<K>*>(sbase);
+        auto wincur = [&](const PipeSeg& g, uint32_t a, uint32_t base, uint32_t o, uint32_t oe) {
             WinCur<K> c;
-            c.ak = win[a].k;
-            c.bk = win[b].k;
-            c.av = win[a].v;
-            c.bv = win[b].v;
-            c.la = win[a].len;
-            c.lb = win[b].len;
-            c.o = o0;
-            c.oe = o1;
+            c.ak = reinterpret_cast<const K*>(sbase + g.koff[a]);
+            c.bk = reinterpret_cast<const K*>(sbase + g.koff[a + 1]);
+            c.av = reinterpret_cast<const int32_t*>(sbase + g.voff[a]);
+            c.bv = reinterpret_cast<const int32_t*>(sbase + g.voff[a + 1]);
+            c.la = g.len[a];
+            c.lb = g.len[a + 1];
+            c.o = o;
+            c.oe = oe;
             c.base = base;
             return c;
         };
-        Rec<K>* orec;
-        constexpr uint32_t NC = PIPE_CONSUMERS;
-        // final records are placed with the global 16-byte phase of the
-        // destination so the store phase moves aligned 16-byte vectors
-        constexpr uint32_t ER = sizeof(K) == 4 ? 4 : 2;  // records per store group
-        const uint32_t al = (uint32_t)(out % ER);
-        constexpr uint32_t VT = pipe_vt<K>();
-        const uint32_t o0 = min(T, VT * ctid), o1 = min(T, VT * ctid + VT);
-        if (w >= 3) {
-            // pass 1: X = merge(A, B) -> xr[0, LX);  Y = merge(C, D) (3-way: C) -> xr[LXp, LXp + LY)
-            // with LXp = LX rounded up to VT: thread t takes outputs [VT*t, VT*t + VT)
-            // of that layout, so every warp runs one merge (no X/Y divergence)
-            const uint32_t LX = win[0].len + win[1].len, LYn = T - LX;
-            const uint32_t LXp = (LX + VT - 1) / VT * VT;
-            const uint32_t ob = VT * ctid;
-            const bool isY = ob >= LXp;
-            WinCur<K> c;
-            c.ak = isY ? win[2].k : win[0].k;
-            c.bk = isY ? win[3].k : win[1].k;
-            c.av = isY ? win[2].v : win[0].v;
-            c.bv = isY ? win[3].v : win[1].v;
-            c.la = isY ? win[2].len : win[0].len;
-            c.lb = isY ? win[3].len : win[1].len;
-            c.o = isY ? ob - LXp : ob;
-            c.oe = isY ? min(ob + VT - LXp, LYn) : min(ob + VT, LX);
-            c.base = isY ? LXp : 0;
-            single_merge(c, xr);
-            PT_WARP(16)
-            consumer_sync();
-            PT_MARK(5)
-            // pass 2: merge X and Y into the slot (its input windows are consumed)
-            orec = reinterpret_cast<Rec<K>*>(sbase);
-            RecCur<K> p0;
-            p0.r = xr;
-            p0.offa = 0;
-            p0.offb = LXp;
-            p0.la = LX;
-            p0.lb = LYn;
-            p0.base = al;
-            p0.o = o0;
-            p0.oe = o1;
-            single_merge(p0, orec);
-        } else {
-            // 2-way: merge(A, B) straight into scratch
-            orec = xr;
-            WinCur<K> c0 = wincur(0, 1, al, o0, o1);
-            single_merge(c0, orec);
-        }
-        PT_WARP(24)
-        // store: every warp moves its own outputs [VT*32*w, VT*32*(w+1)) as soon as
-        // they are written (no CTA barrier): full ER-groups of the phase-shifted
-        // layout as 16-byte vectors, the partial groups at both ends record by record
-        __syncwarp();
-        PT_MARK(6)
-        K* __restrict__ dstK = bufs.kb(par);
-        int32_t* __restrict__ dstV = bufs.vb(par);
-        {
-            const uint32_t wid = ctid >> 5;
-            const uint32_t rs = al + min(T, VT * 32 * wid), re = al + min(T, VT * 32 * (wid + 1));
+        if (d.nseg == 1) {
+            // ---- one segment: pass 2 output phase-shifted for 16-byte stores ----
+            const PipeSeg& g = d.seg[0];
+            const uint32_t T = g.T, par = g.par;
+            const uint64_t out = g.out;
+            const uint32_t al = (uint32_t)(out % ER);
+            const uint32_t o0 = min(T, ob), o1 = min(T, ob + VT);
+            Rec<K>* res;
+            if (g.w >= 3) {
+                // pass 1: X = merge(A, B) -> xr[0, LX);  Y = merge(C, D) (3-way: C) -> xr[LXp, LXp + LY)
+                // (LXp = LX rounded up to VT: every thread works inside X or inside Y)
+                const uint32_t LX = g.lx, LYn = T - LX, LXp = d.s1[1];
+                const bool isY = ob >= LXp;
+                WinCur<K> c = isY ? wincur(g, 2, LXp, ob - LXp, min(ob + VT - LXp, LYn))
+                                  : wincur(g, 0, 0, ob, min(ob + VT, LX));
+                single_merge(c, xr);
+                PT_WARP(16)
+                consumer_sync();
+                PT_MARK(5)
+                // pass 2: merge X and Y into the slot (its input windows are consumed)
+                RecCur<K> p0;
+                p0.r = xr;
+                p0.offa = 0;
+                p0.offb = LXp;
+                p0.la = LX;
+                p0.lb = LYn;
+                p0.base = al;
+                p0.o = o0;
+                p0.oe = o1;
+                single_merge(p0, orec);
+                res = orec;
+            } else {
+                // 2-way: merge(A, B) straight into scratch
+                WinCur<K> c = wincur(g, 0, al, o0, o1);
+                single_merge(c, xr);
+                res = xr;
+            }
+            PT_WARP(24)
+            // store: every warp moves its own outputs as soon as they are written:
+            // full ER-groups of the phase-shifted layout as 16-byte vectors, the
+            // partial groups at both ends record by record
+            __syncwarp();
+            PT_MARK(6)
+            K* __restrict__ dstK = bufs.kb(par);
+            int32_t* __restrict__ dstV = bufs.vb(par);
+            const uint32_t rs = al + min(T, r0w), re = al + min(T, r1w);
             const uint64_t gbase = out - al;  // global element of record index 0
             if (rs < re) {
                 const uint32_t g0 = (rs + ER - 1) / ER, g1 = re / ER;
                 for (uint32_t j = g0 + clane; j < g1; j += 32) {
                     const uint32_t r0 = j * ER;
-                    const uint4* src = reinterpret_cast<const uint4*>(orec + r0);
+                    const uint4* src = reinterpret_cast<const uint4*>(res + r0);
                     if (sizeof(K) == 4) {
                         const uint4 q0 = src[0], q1 = src[1];  // (k0,v0,k1,v1) (k2,v2,k3,v3)
                         *reinterpret_cast<uint4*>(dstK + gbase + r0) = make_uint4(q0.x, q0.z, q1.x, q1.z);
@@ -765,9 +884,62 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                     rr = t0 < re ? t0 : INF32;
                 }
                 if (rr != INF32) {
-                    const Rec<K> rec = orec[rr];
+                    const Rec<K> rec = res[rr];
                     dstK[gbase + rr] = rec.k;
                     dstV[gbase + rr] = rec.v;
+                }
+            }
+        } else {
+            // ---- several segments: both passes through the VT-aligned part layouts ----
+            const uint32_t nseg = d.nseg;
+            if (ob < d.end1) {
+                const uint32_t pp = last_le(d.s1, 2 * nseg, ob);
+                const PipeSeg& g = d.seg[pp >> 1];
+                const bool isY = pp & 1;
+                const uint32_t Lp = isY ? g.T - g.lx : g.lx;
+                const uint32_t o = ob - d.s1[pp];
+                if (o < Lp) {
+                    WinCur<K> c = wincur(g, isY ? 2 : 0, d.s1[pp], o, min(o + VT, Lp));
+                    single_merge(c, xr);
+                }
+            }
+            PT_WARP(16)
+            consumer_sync();
+            PT_MARK(5)
+            if (ob < d.end2) {
+                const uint32_t sg = last_le(d.s2, nseg, ob);
+                const PipeSeg& g = d.seg[sg];
+                const uint32_t o = ob - d.s2[sg];
+                if (o < g.T) {
+                    RecCur<K> p0;
+                    p0.r = xr;
+                    p0.offa = d.s1[2 * sg];
+                    p0.offb = d.s1[2 * sg + 1];
+                    p0.la = g.lx;
+                    p0.lb = g.T - g.lx;
+                    p0.base = d.s2[sg];
+                    p0.o = o;
+                    p0.oe = min(o + VT, g.T);
+                    single_merge(p0, orec);
+                }
+            }
+            PT_WARP(24)
+            __syncwarp();
+            PT_MARK(6)
+            // store this warp's outputs segment by segment (coalesced 4-byte stores)
+            const uint32_t re = min(r1w, d.end2);
+            if (r0w < re) {
+                for (uint32_t sg = last_le(d.s2, nseg, r0w); sg < nseg && d.s2[sg] < re; ++sg) {
+                    const PipeSeg& g = d.seg[sg];
+                    const uint32_t lo = max(r0w, d.s2[sg]), hi = min(re, d.s2[sg] + g.T);
+                    K* __restrict__ dstK = bufs.kb(g.par);
+                    int32_t* __restrict__ dstV = bufs.vb(g.par);
+                    const uint64_t gb = g.out - d.s2[sg];
+                    for (uint32_t r = lo + clane; r < hi; r += 32) {
+                        const Rec<K> rec = orec[r];
+                        dstK[gb + r] = rec.k;
+                        dstV[gb + r] = rec.v;
+                    }
                 }
             }
         }

@@ -366,7 +366,7 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         nd.parity = (uint8_t)(depth & 1);
         const uint32_t w = nd.arity;
         const uint32_t size = nd.pos[w] - nd.pos[0];
-        uint32_t nch = size <= SMALL_NODE ? 0 : 1;
+        uint32_t nch = size <= SMALL_KERNEL_MAX ? 0 : 1;
         if (size > cap) {
             const uint32_t spacing = cap / w;
             for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / spacing;
@@ -381,7 +381,7 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
         if (depth < 0) atomicOr(&sum->err, ERR_CHAIN);
         if (nd.flags & 1) {
             sum->spine_cost[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size;
-            sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_NODE;
+            sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_KERNEL_MAX;
         }
     }
     // per-level cost / small counts: one atomic per distinct power per warp
@@ -393,14 +393,18 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
             if (!(nd.flags & 1)) {
                 key = nd.power;
                 sz = nd.pos[nd.arity] - nd.pos[0];
-                sm = sz <= SMALL_NODE;
+                sm = sz <= SMALL_KERNEL_MAX;
             }
         }
         const uint32_t grp = __match_any_sync(PS_FULL, key);
         const uint32_t gsz = __reduce_add_sync(grp, sz), gsm = __reduce_add_sync(grp, sm);
+        const uint32_t gmx = __reduce_max_sync(grp, sm ? sz : 0u);
         if (key != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(grp) - 1)) {
             atomicAdd(&sum->level_cost[key], (unsigned long long)gsz);
-            if (gsm) atomicAdd(&sum->level_small[key], gsm);
+            if (gsm) {
+                atomicAdd(&sum->level_small[key], gsm);
+                atomicMax(&sum->level_small_max[key], gmx);
+            }
         }
     }
     for (int d = 16; d; d >>= 1) {
