@@ -128,7 +128,7 @@ struct Layout {
     uint64_t lvlP[16];
     // offsets
     uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
-        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, chunk2node, cuts,
+        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts,
         scantmp_u32, scantmp_i32, total;
 };
 
@@ -205,6 +205,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.nodes = take((L.rmax + MAX_SPINE) * sizeof(Node));
     L.nch = take((L.rmax + MAX_SPINE + 2) * 4);
     L.chunk_base = take((L.rmax + MAX_SPINE + 2) * 4);
+    L.stage_chunk = take((NPOW + 3 + MAX_SPINE) * 4);
     L.chunk2node = take(L.chunks_max * 4);
     L.scantmp_u32 = take(L.scan_tmp * 4);
     L.scantmp_i32 = take(L.scan_tmp * 4);
@@ -215,7 +216,11 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
 // Host copy of the summary plus the per-stage chunk ranges.
 struct TreeInfo {
     Summary s;
-    std::vector<uint32_t> node_chunk;  // chunk_base per node (+ total at end)
+    // chunk_base at level offsets [0..NPOW], at spine nodes [NPOW+1+i], total [NPOW+2+MAX_SPINE]
+    uint32_t stage_chunk[NPOW + 3 + MAX_SPINE];
+    uint32_t level_chunk(uint32_t p) const { return stage_chunk[p]; }
+    uint32_t spine_chunk(uint32_t i) const { return stage_chunk[NPOW + 1 + i]; }
+    uint32_t total_chunks() const { return stage_chunk[NPOW + 2 + MAX_SPINE]; }
 };
 
 template <class T>
@@ -236,7 +241,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     const uint32_t log2k = k == 4 ? 2 : 1;
     // T1 powers (array over 0..padded)
     const uint32_t padded = (uint32_t)L.lev_size[0];
-    tree_powers_kernel<<<grid_for(padded, 256), 256, 0, s>>>(b, r, n, log2k, P, padded, err);
+    launch_k(tree_powers_kernel, grid_for(padded, 256), 256, 0, s, b, r, n, log2k, P, padded, err);
     PS_LAUNCH_CHECK();
     // T2 min tree
     MinTree mt;
@@ -249,7 +254,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
             const uint64_t groups = size / 32;
             const uint64_t outp = align_up(groups, 32);
             uint8_t* out = at<uint8_t>(ws, L.minlev[nlev]);
-            tree_minlevel_kernel<<<grid_for(outp, 256), 256, 0, s>>>(mt.lev[nlev - 1], (uint32_t)groups, out,
+            launch_k(tree_minlevel_kernel, grid_for(outp, 256), 256, 0, s, mt.lev[nlev - 1], (uint32_t)groups, out,
                                                                      (uint32_t)outp);
             PS_LAUNCH_CHECK();
             mt.lev[nlev++] = out;
@@ -259,7 +264,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     mt.nlev = nlev;
     uint32_t* Rle = at<uint32_t>(ws, L.Rle);
     uint32_t* Lle = at<uint32_t>(ws, L.Lle);
-    tree_nearest_kernel<<<grid_for(r, 256), 256, 0, s>>>(mt, P, r, Rle, Lle);
+    launch_k(tree_nearest_kernel, grid_for(r, 256), 256, 0, s, mt, P, r, Rle, Lle);
     PS_LAUNCH_CHECK();
     // T3 classify
     int32_t* Dd = at<int32_t>(ws, L.Dd);
@@ -272,17 +277,17 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     uint32_t* htot = at<uint32_t>(ws, L.hist_tot);
     uint32_t* spine = at<uint32_t>(ws, L.spine);
     Node* nodes = at<Node>(ws, L.nodes);
-    tree_classify_kernel<0><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
+    launch_k(tree_classify_kernel<0>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist, hoff, (int64_t)NPOW * nblocks, false, true,
                                                    at<uint32_t>(ws, L.scantmp_u32), htot, s)));
-    tree_level_offsets_kernel<<<1, 128, 0, s>>>(hoff, htot, nblocks, sum);
+    launch_k(tree_level_offsets_kernel, 1, 128, 0, s, hoff, htot, nblocks, sum);
     PS_LAUNCH_CHECK();
-    tree_classify_kernel<1><<<nblocks, CLS_THREADS, 0, s>>>(P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
+    launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
-    tree_spine_kernel<<<1, 1, 0, s>>>(b, r, k, strict, spine, nodes, Dd, sum);
+    launch_k(tree_spine_kernel, 1, 1, 0, s, b, r, k, strict, spine, nodes, Dd, sum);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Dd, Dd, (int64_t)r + 1, false, false,
@@ -294,32 +299,34 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_CUDA(cudaStreamSynchronize(s));
     const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
-    tree_stack_max_kernel<<<grid_for(r, 256), 256, 0, s>>>(Sd, r, sum, (uint32_t)stack_cap);
+    launch_k(tree_stack_max_kernel, grid_for(r, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap);
     PS_LAUNCH_CHECK();
     if (leafpar) {
-        tree_leaf_parity_kernel<<<grid_for(r, 256), 256, 0, s>>>(Dd, r, leafpar);
+        launch_k(tree_leaf_parity_kernel, grid_for(r, 256), 256, 0, s, Dd, r, leafpar);
         PS_LAUNCH_CHECK();
     }
     if (nnodes) {
-        tree_nodes_finalize_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, Dd, slack_mode, cap, sum);
+        launch_k(tree_nodes_finalize_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, nnodes, Dd, slack_mode, cap, sum);
         PS_LAUNCH_CHECK();
         uint32_t* nch = at<uint32_t>(ws, L.nch);
         uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
-        tree_nchunks_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, nnodes, nch);
+        launch_k(tree_nchunks_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, nnodes, nch);
         PS_LAUNCH_CHECK();
         PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nnodes, false, true,
                                                        at<uint32_t>(ws, L.scantmp_u32), cb + nnodes, s)));
-        tree_copy_chunk_base_kernel<<<grid_for(nnodes, 256), 256, 0, s>>>(nodes, cb, nnodes);
+        launch_k(tree_copy_chunk_base_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, cb, nnodes);
         PS_LAUNCH_CHECK();
-        info.node_chunk.resize(nnodes + 1);
-        PS_CUDA(cudaMemcpyAsync(info.node_chunk.data(), cb, (nnodes + 1) * 4, cudaMemcpyDeviceToHost, s));
+        uint32_t* sc = at<uint32_t>(ws, L.stage_chunk);
+        launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, sum, nnodes, sc);
+        PS_LAUNCH_CHECK();
+        PS_CUDA(cudaMemcpyAsync(info.stage_chunk, sc, sizeof(info.stage_chunk), cudaMemcpyDeviceToHost, s));
     }
     PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
-    if (nnodes && info.node_chunk[nnodes] > 0) {
-        const uint32_t total = info.node_chunk[nnodes];
+    if (nnodes && info.total_chunks() > 0) {
+        const uint32_t total = info.total_chunks();
         if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
-        tree_chunk_map_kernel<<<grid_for(total, 256), 256, 0, s>>>(nodes, nnodes, total,
+        launch_k(tree_chunk_map_kernel, grid_for(total, 256), 256, 0, s, nodes, nnodes, total,
                                                                    at<uint32_t>(ws, L.chunk2node));
         PS_LAUNCH_CHECK();
     }
@@ -370,19 +377,19 @@ struct MergeRunner {
         const uint32_t nbig = (nhi - nlo) - nsmall;
         if (nsmall) {
             const uint32_t G = small_group(small_max);
-            merge_small_kernel<K><<<grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem, s>>>(
+            launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem, s, 
                 bufs, nodes, nlo, nhi, G);
             PS_LAUNCH_CHECK();
         }
         if (c1 > c0) {
             if (c1 - c0 > nbig) {
                 const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
-                merge_partition_kernel<K><<<grid_for(c1 - c0, 8), 256, 0, s>>>(bufs, nodes, c2n, c0, c1, cuts);
+                launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1, cuts);
                 PS_LAUNCH_CHECK();
                 if (prof) prof->end(pp);
             }
             const uint32_t units = c1 - c0;
-            merge_pipe_kernel<K><<<std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s>>>(
+            launch_k(merge_pipe_kernel<K>, std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s, 
                 bufs, nelem, nodes, c2n, cuts, c0, units, err);
             PS_LAUNCH_CHECK();
         }
@@ -475,7 +482,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
 
     // ---- N1 pass 1: run detection ------------------------------------------
     const int ph_rd = prof.begin(0, -1, 0, 0, n * (int64_t)sizeof(K));
-    rd_types_kernel<K><<<ngroups, 256, 0, s>>>(keys, (uint64_t)n, ty, cg);
+    launch_k(rd_types_kernel<K>, ngroups, 256, 0, s, keys, (uint64_t)n, ty, cg);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpMin<uint32_t>>(cg, Fg, ngroups, true, false, at<uint32_t>(ws, L.scantmp_u32),
                                                    nullptr, s)));
@@ -490,7 +497,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             PS_CUDA(cudaFuncSetAttribute(rd_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
             PS_CUDA(cudaFuncSetAttribute(rd_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
         }
-        rd_tables_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
+        launch_k(rd_tables_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
                                                    err);
         PS_LAUNCH_CHECK();
         uint64_t span = GROUP;
@@ -498,7 +505,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         for (uint64_t l = 0; l < L.tab_levels; ++l) {
             spans[l] = span;
             if (l + 1 < L.tab_levels) {
-                rd_compose_kernel<<<(unsigned)L.lvlP[l + 1], 32, fan_smem, s>>>(
+                launch_k(rd_compose_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
                     at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
                     at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
                 PS_LAUNCH_CHECK();
@@ -506,20 +513,20 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             }
         }
         const uint64_t top = L.tab_levels - 1;
-        rd_top_kernel<<<1, 32, fan_smem, s>>>(at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
+        launch_k(rd_top_kernel, 1, 32, fan_smem, s, at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
                                        (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
         PS_LAUNCH_CHECK();
         for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
-            rd_down_kernel<<<(unsigned)L.lvlP[l + 1], 32, fan_smem, s>>>(
+            launch_k(rd_down_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
                 at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
                 at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
             PS_LAUNCH_CHECK();
         }
-        rd_emit_kernel<<<ngroups, 256, smem, s>>>(ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
+        launch_k(rd_emit_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
                                                at<uint64_t>(ws, L.lvl_ent[0]), b, nat, err);
         PS_LAUNCH_CHECK();
     } else {
-        rd_serial_kernel<<<1, 32, 0, s>>>(ty, (uint64_t)n, m, b, nat, sum);
+        launch_k(rd_serial_kernel, 1, 32, 0, s, ty, (uint64_t)n, m, b, nat, sum);
         PS_LAUNCH_CHECK();
     }
     prof.end(ph_rd);
@@ -559,12 +566,12 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         if (argsort) {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-            form_leaves_kernel<K, true><<<grid, FORM_THREADS, smem, s>>>(bufs, (uint64_t)n, b, nat, leafpar, r, ty,
+            launch_k(form_leaves_kernel<K, true>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r, ty,
                                                                          (uint32_t)m);
         } else {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-            form_leaves_kernel<K, false><<<grid, FORM_THREADS, smem, s>>>(bufs, (uint64_t)n, b, nat, leafpar, r, ty,
+            launch_k(form_leaves_kernel<K, false>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r, ty,
                                                                           (uint32_t)m);
         }
         PS_LAUNCH_CHECK();
@@ -578,9 +585,9 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                          err, s);
         if (rc) return rc;
         int stage = 0;
-        auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint64_t cost, uint32_t nsmall, uint32_t small_max) -> int {
+        auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint64_t cost, uint32_t nsmall,
+                             uint32_t small_max) -> int {
             if (nhi <= nlo) return PS_OK;
-            const uint32_t c0 = info.node_chunk[nlo], c1 = info.node_chunk[nhi];
             const int ph = prof.begin(4, stage, nhi - nlo, c1 - c0, 2 * (int64_t)cost * rec_bytes);
             int rc2 = mr.stage(nlo, nhi, c0, c1, nsmall, small_max, &prof, stage);
             prof.end(ph);
@@ -588,12 +595,13 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             return rc2;
         };
         for (int p = (int)NPOW - 1; p >= 1; --p) {
-            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.s.level_cost[p], info.s.level_small[p],
-                           info.s.level_small_max[p]);
+            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.level_chunk(p), info.level_chunk(p + 1),
+                           info.s.level_cost[p], info.s.level_small[p], info.s.level_small_max[p]);
             if (rc) return rc;
         }
         for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
-            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.s.spine_cost[i], info.s.spine_small[i], SMALL_NODE);
+            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.spine_chunk(i), info.spine_chunk(i + 1),
+                           info.s.spine_cost[i], info.s.spine_small[i], SMALL_NODE);
             if (rc) return rc;
         }
     }
@@ -704,7 +712,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
     const dim3 sgrid(cdiv((uint64_t)G * SEL_CANDIDATES, 8), 2);
     for (int pass = 0; pass < 4; ++pass) {
         for (int it = 0; it < rounds; ++it) {
-            shard_select_kernel<K><<<sgrid, 256, 0, s>>>(S, targets, bounds);
+            launch_k(shard_select_kernel<K>, sgrid, 256, 0, s, S, targets, bounds);
             PS_LAUNCH_CHECK();
         }
         PS_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
@@ -726,7 +734,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
     // ---- gather the windows (peer loads over NVLink) into Lk/Lv ------------------
     K* lk = at<K>(ws, L.lk);
     int32_t* lv = at<int32_t>(ws, L.lv);
-    shard_gather_kernel<K><<<(unsigned)std::min<uint64_t>(cdiv(slab, 256), 148 * 16), 256, 0, s>>>(
+    launch_k(shard_gather_kernel<K>, (unsigned)std::min<uint64_t>(cdiv(slab, 256), 148 * 16), 256, 0, s, 
         S, bounds, bounds + 2 * MAX_SHARDS, lk, lv, slab);
     PS_LAUNCH_CHECK();
 

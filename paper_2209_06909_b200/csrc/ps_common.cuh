@@ -4,6 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
+#include <utility>
+
 #define PS_DEV __device__ __forceinline__
 #define PS_FULL 0xFFFFFFFFu
 
@@ -92,6 +96,29 @@ struct Summary {
     uint32_t level_small_max[NPOW];           // largest small node per power bucket
     uint32_t spine_small[MAX_SPINE];
 };
+
+// Programmatic dependent launch (PDL).  Every kernel is launched with
+// programmatic stream serialization, so its launch overlaps the tail of the
+// previous kernel in the stream; pdl_wait() (first statement of every kernel)
+// blocks until that predecessor has completed and its writes are visible.
+PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    static const bool pdl = getenv("PS_NO_PDL") == nullptr;  // PS_NO_PDL=1: plain stream order (A/B runs)
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 PS_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 PS_DEV uint32_t warp_id() { return threadIdx.x >> 5; }

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
                                                                    const uint32_t* __restrict__ nat,
                                                                    const uint8_t* __restrict__ leafpar, uint32_t r,
                                                                    const uint32_t* __restrict__ ty, uint32_t m) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
     uint32_t* snat = sb + (FORM_TILE + 2);

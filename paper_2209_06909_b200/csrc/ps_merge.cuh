@@ -163,6 +163,7 @@ template <class K>
 __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
                                                               const uint32_t* __restrict__ chunk2node, uint32_t c0,
                                                               uint32_t c1, uint4* __restrict__ cuts) {
+    pdl_wait();
     const uint32_t c = c0 + blockIdx.x * 8 + warp_id();
     if (c >= c1) return;
     const uint32_t lane = lane_id();
@@ -265,6 +266,7 @@ size_t merge_small_smem_bytes() {
 template <class K>
 __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
                                                                        uint32_t nlo, uint32_t nhi, uint32_t G) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t smem[];
     // per node of the group: packed start, global start, run starts (relative), size, parity
     __shared__ uint32_t s_pre[SMALL_WARPS][33];
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                                                                   const uint32_t* __restrict__ chunk2node,
                                                                   const uint4* __restrict__ cuts, uint32_t c0,
                                                                   uint32_t nchunks, uint32_t* err) {
+    pdl_wait();
     using LY = PipeLayout<K>;
     constexpr uint32_t VT = pipe_vt<K>();
     extern __shared__ __align__(128) uint8_t smem[];

@@ -38,6 +38,7 @@ PS_DEV uint32_t range_mask(uint64_t q0, uint64_t lo, uint64_t hi) {
 template <class K>
 __global__ void __launch_bounds__(256) rd_types_kernel(const K* __restrict__ a, uint64_t n,
                                                        uint32_t* __restrict__ ty, uint32_t* __restrict__ cg) {
+    pdl_wait();
     __shared__ uint32_t sw[GROUP_WORDS];
     __shared__ uint32_t smin[8];
     const uint32_t g = blockIdx.x;
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restri
                                                         const uint32_t* __restrict__ Fg, uint32_t ngroups,
                                                         uint64_t* __restrict__ tile_tab, uint32_t* __restrict__ Ft,
                                                         uint64_t* __restrict__ group_tab, uint32_t* err) {
+    pdl_wait();
     __shared__ uint32_t s_chg[GROUP_WORDS + 1];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
     __shared__ uint64_t s_Ft[TILES_PER_GROUP];
@@ -287,6 +289,7 @@ PS_DEV uint32_t stage_tables(const uint64_t* __restrict__ in, uint32_t j0, uint3
 __global__ void __launch_bounds__(32) rd_compose_kernel(const uint64_t* __restrict__ in, uint32_t P, uint64_t span,
                                                         const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
                                                         uint64_t* __restrict__ out, uint32_t* err) {
+    pdl_wait();
     extern __shared__ uint64_t s_tab[];
     __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t o = blockIdx.x;
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(32) rd_top_kernel(const uint64_t* __restrict__
                                                     const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
                                                     uint64_t* __restrict__ entries, uint32_t* __restrict__ b,
                                                     Summary* sum, uint32_t* err) {
+    pdl_wait();
     extern __shared__ uint64_t s_tab[];
     __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t M1 = m + 1;
@@ -335,6 +339,7 @@ __global__ void __launch_bounds__(32) rd_down_kernel(const uint64_t* __restrict_
                                                      const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
                                                      const uint64_t* __restrict__ up_entries,
                                                      uint64_t* __restrict__ entries, uint32_t* err) {
+    pdl_wait();
     extern __shared__ uint64_t s_tab[];
     __shared__ uint64_t s_F[TSCAN_FAN];
     const uint32_t o = blockIdx.x;
@@ -363,6 +368,7 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
                                                       const uint64_t* __restrict__ group_entries,
                                                       uint32_t* __restrict__ b, uint32_t* __restrict__ nat,
                                                       uint32_t* err) {
+    pdl_wait();
     __shared__ uint32_t s_chg[GROUP_WORDS + 1];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
     __shared__ uint64_t s_entry[TILES_PER_GROUP];
@@ -407,6 +413,7 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
 // apart, so at most n/m steps); one warp scans change bits 1024 at a time.
 __global__ void rd_serial_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint64_t m,
                                  uint32_t* __restrict__ b, uint32_t* __restrict__ nat, Summary* sum) {
+    pdl_wait();
     const uint32_t lane = lane_id();
     const uint64_t nwords = (n + 31) / 32;
     uint64_t p = 0, c = 0;

@@ -72,6 +72,7 @@ PS_DEV T block_exclusive(T v, T& total, T* sw /* >= 32 */) {
 template <class T, class Op>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, T* __restrict__ partial,
                                                                    int64_t n, int reverse) {
+    pdl_wait();
     __shared__ T sw[32];
     Op op;
     const int64_t base = (int64_t)blockIdx.x * SCAN_BLK;
@@ -89,6 +90,7 @@ template <class T, class Op>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const T* in, T* out, int64_t n,
                                                                   const T* __restrict__ carry, int reverse,
                                                                   int exclusive, T* total_out) {
+    pdl_wait();
     __shared__ T items[SCAN_BLK];
     __shared__ T sw[32];
     Op op;
@@ -141,17 +143,17 @@ cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclu
     if (n <= 0) return cudaSuccess;
     int64_t nb = (n + SCAN_BLK - 1) / SCAN_BLK;
     if (nb == 1) {
-        scan_apply_kernel<T, Op><<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr, reverse, exclusive, total_out);
+        launch_k(scan_apply_kernel<T, Op>, 1, SCAN_THREADS, 0, s, in, out, n, nullptr, reverse, exclusive, total_out);
         launch_counter()++;
         return cudaGetLastError();
     }
     T* partial = tmp;
     T* rest = tmp + nb + 32;
-    scan_reduce_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, partial, n, reverse);
+    launch_k(scan_reduce_kernel<T, Op>, (unsigned)nb, SCAN_THREADS, 0, s, in, partial, n, reverse);
     launch_counter() += 2;
     cudaError_t e = device_scan<T, Op>(partial, partial, nb, false, true, rest, nullptr, s);
     if (e != cudaSuccess) return e;
-    scan_apply_kernel<T, Op><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, partial, reverse, exclusive,
+    launch_k(scan_apply_kernel<T, Op>, (unsigned)nb, SCAN_THREADS, 0, s, in, out, n, partial, reverse, exclusive,
                                                                     total_out);
     return cudaGetLastError();
 }

@@ -51,6 +51,7 @@ PS_DEV uint64_t shard_count_before(const K* __restrict__ a, uint64_t lo, uint64_
 template <class K>
 __global__ void __launch_bounds__(256) shard_select_kernel(ShardSet<K> S, const uint64_t* __restrict__ targets,
                                                            unsigned long long* bounds) {
+    pdl_wait();
     const uint32_t tgt = blockIdx.y;
     const uint32_t wid = blockIdx.x * 8 + warp_id();
     const uint32_t lane = lane_id();
@@ -93,6 +94,7 @@ template <class K>
 __global__ void shard_gather_kernel(ShardSet<K> S, const unsigned long long* __restrict__ bounds_begin,
                                     const unsigned long long* __restrict__ bounds_end, K* __restrict__ dk,
                                     int32_t* __restrict__ dv, uint64_t total) {
+    pdl_wait();
     __shared__ uint64_t s_cb[MAX_SHARDS], s_off[MAX_SHARDS + 1];
     if (threadIdx.x == 0) {
         uint64_t acc = 0;

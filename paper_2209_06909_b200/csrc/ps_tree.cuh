@@ -21,6 +21,7 @@ namespace ps {
 // T1: powers.  P[j] for j in [0, padded): P[0] = P[r] = 0, j > r -> 0xFF.
 __global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
                                    uint8_t* __restrict__ P, uint32_t padded, uint32_t* err) {
+    pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= padded) return;
     uint32_t v;
@@ -48,6 +49,7 @@ __global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, u
 // T2: one level of the 32-ary min tree (bytes).
 __global__ void tree_minlevel_kernel(const uint8_t* __restrict__ in, uint32_t in_groups, uint8_t* __restrict__ out,
                                      uint32_t out_padded) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= out_padded) return;
     uint32_t v = 0xFF;
@@ -132,6 +134,7 @@ PS_DEV uint32_t find_left_le(const MinTree& t, uint32_t j, uint32_t v) {
 // T3a: Rle[j] = first j' > j with P[j'] <= P[j]; Lle[j] = last j' < j with P[j'] <= P[j].
 __global__ void tree_nearest_kernel(MinTree t, const uint8_t* __restrict__ P, uint32_t r, uint32_t* __restrict__ Rle,
                                     uint32_t* __restrict__ Lle) {
+    pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
     if (j >= r) return;
     const uint32_t v = P[j];
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
     const uint32_t* __restrict__ b, uint32_t r, uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
     const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff, int32_t* __restrict__ Sdiff,
     uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum) {
+    pdl_wait();
     __shared__ uint32_t whist[32][NPOW];
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     for (uint32_t i = tid; i < 32 * NPOW; i += blockDim.x) (&whist[0][0])[i] = 0;
@@ -273,6 +277,7 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
 __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                                   uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
                                   int32_t* __restrict__ Ddiff, Summary* sum) {
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint32_t H = sum->nspine;
     if (H > MAX_SPINE) {
@@ -358,6 +363,7 @@ __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, ui
 //             1 -> 2-way 0, 3/4-way 1 ("4way-nosentinel"), 2 -> 0.
 __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nnodes, const int32_t* __restrict__ S,
                                            int slack_mode, uint32_t cap, Summary* sum) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
     if (i < nnodes) {
@@ -437,7 +443,26 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
     }
 }
 
+// chunk_base at the node indices the host schedules stages by: level offsets
+// (out[0..NPOW]), spine nodes (out[NPOW+1+i], i <= nspine_nodes) and the total
+// (out[NPOW+2+MAX_SPINE]); cb has nnodes+1 entries.
+__global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum,
+                                         uint32_t nnodes, uint32_t* __restrict__ out) {
+    pdl_wait();
+    const uint32_t t = threadIdx.x;
+    if (t <= NPOW) {
+        const uint32_t i = sum->level_off[t];
+        out[t] = cb[i < nnodes ? i : nnodes];
+    }
+    for (uint32_t i = t; i <= MAX_SPINE; i += blockDim.x) {
+        const uint32_t j = sum->nmain + i;
+        out[NPOW + 1 + i] = cb[j < nnodes ? j : nnodes];
+    }
+    if (t == 0) out[NPOW + 2 + MAX_SPINE] = cb[nnodes];
+}
+
 __global__ void tree_leaf_parity_kernel(const int32_t* __restrict__ S, uint32_t r, uint8_t* __restrict__ leafpar) {
+    pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= r) return;
     const int32_t a = j == 0 ? 0 : S[j];
@@ -446,6 +471,7 @@ __global__ void tree_leaf_parity_kernel(const int32_t* __restrict__ S, uint32_t 
 }
 
 __global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r, Summary* sum, uint32_t cap) {
+    pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
     int32_t v = (j < r) ? H[j] : 0;
     for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
@@ -458,6 +484,7 @@ __global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r,
 // level offsets of the power buckets from the scanned block histograms
 __global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
                                           uint32_t nblocks, Summary* sum) {
+    pdl_wait();
     const uint32_t p = threadIdx.x;
     if (p < NPOW) sum->level_off[p] = blockOff[(uint64_t)p * nblocks];
     if (p == 0) {
@@ -468,11 +495,13 @@ __global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff,
 
 __global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ base,
                                             uint32_t nnodes) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nnodes) nodes[i].chunk_base = base[i];
 }
 
 __global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t* __restrict__ out) {
+    pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nnodes) out[i] = nodes[i].nchunks;
 }
@@ -480,6 +509,7 @@ __global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nno
 // chunk -> node map by binary search over the nodes' chunk_base.
 __global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t total_chunks,
                                       uint32_t* __restrict__ chunk2node) {
+    pdl_wait();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= total_chunks) return;
     uint32_t lo = 0, hi = nnodes;  // find last node with chunk_base <= c
