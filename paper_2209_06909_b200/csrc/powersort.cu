@@ -120,6 +120,54 @@ struct WsHeader {
     uint64_t off_sum, off_b, off_nat, off_nodes;
 };
 
+// Small device->host reads go through a host-mapped pinned buffer written by a
+// kernel: a cudaMemcpyAsync would queue behind bulk transfers of other streams
+// on the copy engines (the pipelined end-to-end path), a kernel store does not.
+struct HostMap {
+    uint8_t* h = nullptr;
+    uint8_t* d = nullptr;
+    size_t size = 0;
+};
+thread_local HostMap g_map;
+
+__global__ void publish_kernel(const uint32_t* __restrict__ a, uint32_t na, const uint32_t* __restrict__ b,
+                               uint32_t nb, uint32_t* __restrict__ dst) {
+    pdl_wait();
+    for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) dst[i] = a[i];
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[na + i] = b[i];
+}
+
+__global__ void write_header_kernel(WsHeader h, WsHeader* dst) {
+    pdl_wait();
+    if (threadIdx.x == 0) *dst = h;
+}
+
+int host_map_ensure(size_t bytes) {
+    if (g_map.size >= bytes) return PS_OK;
+    if (g_map.h) cudaFreeHost(g_map.h);
+    g_map = HostMap();
+    void* h = nullptr;
+    PS_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    void* d = nullptr;
+    PS_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    g_map.h = (uint8_t*)h;
+    g_map.d = (uint8_t*)d;
+    g_map.size = bytes;
+    return PS_OK;
+}
+
+// Copies device ranges a (and b) to host a_out (b_out) and synchronizes the stream.
+int publish(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out, cudaStream_t s) {
+    int rc = host_map_ensure(abytes + bbytes);
+    if (rc) return rc;
+    PS_CUDA(launch_k(publish_kernel, 1, 256, 0, s, (const uint32_t*)a, (uint32_t)(abytes / 4), (const uint32_t*)b,
+                     (uint32_t)(bbytes / 4), (uint32_t*)g_map.d));
+    PS_CUDA(cudaStreamSynchronize(s));
+    memcpy(a_out, g_map.h, abytes);
+    if (bbytes) memcpy(b_out, g_map.h + abytes, bbytes);
+    return PS_OK;
+}
+
 struct Layout {
     uint64_t n, m, kb, rmax, ngroups, ntiles, chunks_max, scan_tmp;
     uint32_t nlev;
@@ -295,8 +343,10 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Sd, Sd, (int64_t)r + 1, false, false,
                                                  at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
     // Need node count for finalize: read the summary (sync #2a)
-    PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
-    PS_CUDA(cudaStreamSynchronize(s));
+    {
+        int rc = publish(sum, sizeof(Summary), &info.s, nullptr, 0, nullptr, s);
+        if (rc) return rc;
+    }
     const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
     launch_k(tree_stack_max_kernel, grid_for(r, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap);
@@ -316,13 +366,15 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
                                                        at<uint32_t>(ws, L.scantmp_u32), cb + nnodes, s)));
         launch_k(tree_copy_chunk_base_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, cb, nnodes);
         PS_LAUNCH_CHECK();
-        uint32_t* sc = at<uint32_t>(ws, L.stage_chunk);
-        launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, sum, nnodes, sc);
+        launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, sum, nnodes, at<uint32_t>(ws, L.stage_chunk));
         PS_LAUNCH_CHECK();
-        PS_CUDA(cudaMemcpyAsync(info.stage_chunk, sc, sizeof(info.stage_chunk), cudaMemcpyDeviceToHost, s));
     }
-    PS_CUDA(cudaMemcpyAsync(&info.s, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
-    PS_CUDA(cudaStreamSynchronize(s));
+    {
+        int rc = nnodes ? publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk),
+                                  sizeof(info.stage_chunk), info.stage_chunk, s)
+                        : publish(sum, sizeof(Summary), &info.s, nullptr, 0, nullptr, s);
+        if (rc) return rc;
+    }
     if (nnodes && info.total_chunks() > 0) {
         const uint32_t total = info.total_chunks();
         if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
@@ -413,8 +465,7 @@ int write_header(uint8_t* ws, const Layout& L, int64_t n, int64_t m, int k, int 
     h.off_b = L.b;
     h.off_nat = L.nat;
     h.off_nodes = L.nodes;
-    PS_CUDA(cudaMemcpyAsync(ws + L.header, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-    PS_CUDA(cudaStreamSynchronize(s));
+    PS_CUDA(launch_k(write_header_kernel, 1, 32, 0, s, h, reinterpret_cast<WsHeader*>(ws + L.header)));
     return PS_OK;
 }
 
@@ -531,8 +582,10 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     }
     prof.end(ph_rd);
     Summary h;
-    PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
-    PS_CUDA(cudaStreamSynchronize(s));
+    {
+        int rc = publish(sum, sizeof(Summary), &h, nullptr, 0, nullptr, s);
+        if (rc) return rc;
+    }
     if (h.err) return fail(PS_EINVARIANT, "run detection invariant violated (flags " + std::to_string(h.err) + ")");
     const uint32_t r = h.r;
     if (r < 1 || r + 2 > L.rmax) return fail(PS_EINVARIANT, "run count out of range: " + std::to_string(r));
@@ -605,12 +658,14 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             if (rc) return rc;
         }
     }
-    PS_CUDA(cudaMemcpyAsync(&h, sum, sizeof(Summary), cudaMemcpyDeviceToHost, s));
-    PS_CUDA(cudaStreamSynchronize(s));
+    {
+        int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
+        if (rc) return rc;
+        rc = publish(sum, sizeof(Summary), &h, nullptr, 0, nullptr, s);
+        if (rc) return rc;
+    }
     if (h.err) return fail(PS_EINVARIANT, "merge invariant violated (flags " + std::to_string(h.err) + ")");
     prof.finish();
-    int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
-    if (rc) return rc;
 
     // ---- N5: SortStats (statskit.py:75-98) ----------------------------------------
     memset(st, 0, sizeof(*st));
@@ -979,6 +1034,7 @@ int ps_tree_from_profile(const int64_t* lengths, int64_t r, int32_t k, int32_t s
     }
     int rc = write_header(ws, L, (int64_t)n, 1, k, 0, (uint32_t)r, info.s.nmain, info.s.nspine_nodes, s);
     if (rc) return rc;
+    PS_CUDA(cudaStreamSynchronize(s));
     if (merge_cost) *merge_cost = (int64_t)info.s.merge_cost;
     if (max_stack_height) *max_stack_height = info.s.max_stack;
     return PS_OK;
