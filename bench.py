@@ -90,13 +90,21 @@ def load_peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(config):
-    """dram bytes per merge launch from the committed ncu capture, or None."""
-    path = os.path.join(REPO, "profiles", "merge_traffic.json")
+def load_traffic(config, n):
+    """DRAM bytes per merge_pipe_kernel launch from the committed ncu capture of
+    one sort of this workload (profiles/*_pipe_traffic_<config>.json), or None."""
+    import glob
+
+    from paper_2209_06909_b200 import workloads
+
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "*_pipe_traffic_%s.json" % config)))
+    if not paths or n != workloads.FULL_N.get(config):
+        return None
     try:
-        with open(path) as f:
+        with open(paths[-1]) as f:
             t = json.load(f)
-        return t.get(config)
+        return {"dram_bytes_per_launch": t["dram_bytes_per_launch"], "launches": t["launches"],
+                "dram_bytes_per_step": t["dram_bytes_total"], "source": os.path.relpath(paths[-1], REPO)}
     except Exception:
         return None
 
@@ -545,7 +553,9 @@ def run_ours(args):
     per_step = {k: {"ms": v["ms"] / K, "GB": v["bytes"] / K / 1e9} for k, v in agg.items()}
     achieved = merge_bytes / (merge_ms / 1e3) / 1e9 if merge_ms else 0.0
     pass_gbs = merge_bytes / ((merge_ms + part_ms) / 1e3) / 1e9 if merge_ms else 0.0
-    traffic = load_traffic(args.config)
+    traffic = load_traffic(args.config, n)
+    if traffic:
+        traffic["dram_over_algorithmic"] = traffic["dram_bytes_per_step"] / (merge_bytes / K) if merge_bytes else None
     roofline = {
         "bound": "hbm",
         "kernel": "merge_pipe_kernel + merge_small_kernel (all merge launches of a step)",
@@ -554,7 +564,8 @@ def run_ours(args):
         "unit": "GB/s",
         "frac": achieved / peak if peak else None,
         "peak_source": peak_src,
-        "traffic": traffic,
+        "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+        "traffic_detail": traffic,
         "algorithmic_bytes_per_step": merge_bytes / K,
         "launches_per_step": merge_launches / K,
         "merge_pass_gbs_incl_partition": pass_gbs,

@@ -130,8 +130,8 @@ struct HostMap {
 };
 thread_local HostMap g_map;
 
-__global__ void publish_kernel(const uint32_t* __restrict__ a, uint32_t na, const uint32_t* __restrict__ b,
-                               uint32_t nb, uint32_t* __restrict__ dst) {
+__global__ void publish_kernel(const uint4* __restrict__ a, uint32_t na, const uint4* __restrict__ b, uint32_t nb,
+                               uint4* __restrict__ dst) {
     pdl_wait();
     for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) dst[i] = a[i];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[na + i] = b[i];
@@ -156,17 +156,24 @@ int host_map_ensure(size_t bytes) {
     return PS_OK;
 }
 
-// Copies device ranges a (and b) to host a_out (b_out) and synchronizes the stream.
+// Copies device ranges a (and b) to host a_out (b_out) and synchronizes the
+// stream.  Device sources are 16-byte aligned workspace regions; whole 16-byte
+// words are moved (16-byte PCIe writes), only `bytes` are returned.
 int publish(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out, cudaStream_t s) {
-    int rc = host_map_ensure(abytes + bbytes);
+    const size_t a16 = (abytes + 15) / 16, b16 = (bbytes + 15) / 16;
+    int rc = host_map_ensure((a16 + b16) * 16);
     if (rc) return rc;
-    PS_CUDA(launch_k(publish_kernel, 1, 256, 0, s, (const uint32_t*)a, (uint32_t)(abytes / 4), (const uint32_t*)b,
-                     (uint32_t)(bbytes / 4), (uint32_t*)g_map.d));
+    PS_CUDA(launch_k(publish_kernel, 1, 128, 0, s, (const uint4*)a, (uint32_t)a16, (const uint4*)b, (uint32_t)b16,
+                     (uint4*)g_map.d));
     PS_CUDA(cudaStreamSynchronize(s));
     memcpy(a_out, g_map.h, abytes);
-    if (bbytes) memcpy(b_out, g_map.h + abytes, bbytes);
+    if (bbytes) memcpy(b_out, g_map.h + a16 * 16, bbytes);
     return PS_OK;
 }
+
+// leading Summary fields the host needs at each synchronization point
+constexpr size_t SUM_HEAD = offsetof(Summary, level_off);    // r, err, node counts, max_stack
+constexpr size_t SUM_STATS = offsetof(Summary, level_cost);  // + level offsets and the counters
 
 struct Layout {
     uint64_t n, m, kb, rmax, ngroups, ntiles, chunks_max, scan_tmp;
@@ -208,7 +215,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
         if (P <= TSCAN_FAN) break;
         P = cdiv(P, TSCAN_FAN);
     }
-    uint64_t big = std::max<uint64_t>({L.rmax + 2, L.ngroups + 2, (uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2,
+    uint64_t big = std::max<uint64_t>({L.rmax + MAX_SPINE + 2, L.ngroups + 2, (uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2,
                                        L.rmax});
     L.scan_tmp = scan_tmp_elems(big);
 
@@ -342,12 +349,8 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
                                                  at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
     PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Sd, Sd, (int64_t)r + 1, false, false,
                                                  at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
-    // Need node count for finalize: read the summary (sync #2a)
-    {
-        int rc = publish(sum, sizeof(Summary), &info.s, nullptr, 0, nullptr, s);
-        if (rc) return rc;
-    }
-    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
+    // node-indexed kernels run over the bound nmax and read the node count on the device
+    const uint32_t nmax = r + MAX_SPINE;
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
     launch_k(tree_stack_max_kernel, grid_for(r, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap);
     PS_LAUNCH_CHECK();
@@ -355,26 +358,24 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
         launch_k(tree_leaf_parity_kernel, grid_for(r, 256), 256, 0, s, Dd, r, leafpar);
         PS_LAUNCH_CHECK();
     }
-    if (nnodes) {
-        launch_k(tree_nodes_finalize_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, nnodes, Dd, slack_mode, cap, sum);
-        PS_LAUNCH_CHECK();
-        uint32_t* nch = at<uint32_t>(ws, L.nch);
-        uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
-        launch_k(tree_nchunks_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, nnodes, nch);
-        PS_LAUNCH_CHECK();
-        PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nnodes, false, true,
-                                                       at<uint32_t>(ws, L.scantmp_u32), cb + nnodes, s)));
-        launch_k(tree_copy_chunk_base_kernel, grid_for(nnodes, 256), 256, 0, s, nodes, cb, nnodes);
-        PS_LAUNCH_CHECK();
-        launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, sum, nnodes, at<uint32_t>(ws, L.stage_chunk));
-        PS_LAUNCH_CHECK();
-    }
+    launch_k(tree_nodes_finalize_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, Dd, slack_mode, cap, sum);
+    PS_LAUNCH_CHECK();
+    uint32_t* nch = at<uint32_t>(ws, L.nch);
+    uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
+    launch_k(tree_nchunks_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, (const Summary*)sum, nch);
+    PS_LAUNCH_CHECK();
+    PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nmax, false, true, at<uint32_t>(ws, L.scantmp_u32),
+                                                   cb + nmax, s)));
+    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, nodes, cb, nmax, (const Summary*)sum);
+    PS_LAUNCH_CHECK();
+    launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, (const Summary*)sum, nmax, at<uint32_t>(ws, L.stage_chunk));
+    PS_LAUNCH_CHECK();
     {
-        int rc = nnodes ? publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk),
-                                  sizeof(info.stage_chunk), info.stage_chunk, s)
-                        : publish(sum, sizeof(Summary), &info.s, nullptr, 0, nullptr, s);
+        int rc = publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
+                         info.stage_chunk, s);
         if (rc) return rc;
     }
+    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
     if (nnodes && info.total_chunks() > 0) {
         const uint32_t total = info.total_chunks();
         if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
@@ -583,7 +584,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     prof.end(ph_rd);
     Summary h;
     {
-        int rc = publish(sum, sizeof(Summary), &h, nullptr, 0, nullptr, s);
+        int rc = publish(sum, SUM_HEAD, &h, nullptr, 0, nullptr, s);
         if (rc) return rc;
     }
     if (h.err) return fail(PS_EINVARIANT, "run detection invariant violated (flags " + std::to_string(h.err) + ")");
@@ -661,7 +662,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     {
         int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
         if (rc) return rc;
-        rc = publish(sum, sizeof(Summary), &h, nullptr, 0, nullptr, s);
+        rc = publish(sum, SUM_STATS, &h, nullptr, 0, nullptr, s);
         if (rc) return rc;
     }
     if (h.err) return fail(PS_EINVARIANT, "merge invariant violated (flags " + std::to_string(h.err) + ")");

@@ -361,9 +361,16 @@ __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, ui
 // T5: per-node depth/parity, chunk counts and merge statistics; leaf parity.
 // slack_mode: 0 -> slack = arity ("4way"/"2way" sentinel kernels),
 //             1 -> 2-way 0, 3/4-way 1 ("4way-nosentinel"), 2 -> 0.
-__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nnodes, const int32_t* __restrict__ S,
+// node count is read on the device (nmain + nspine_nodes, <= nmax): no host sync
+PS_DEV uint32_t node_count(const Summary* sum, uint32_t nmax) {
+    const uint32_t c = sum->nmain + sum->nspine_nodes;
+    return c < nmax ? c : nmax;
+}
+
+__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
                                            int slack_mode, uint32_t cap, Summary* sum) {
     pdl_wait();
+    const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
     if (i < nnodes) {
@@ -447,8 +454,9 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nn
 // (out[0..NPOW]), spine nodes (out[NPOW+1+i], i <= nspine_nodes) and the total
 // (out[NPOW+2+MAX_SPINE]); cb has nnodes+1 entries.
 __global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum,
-                                         uint32_t nnodes, uint32_t* __restrict__ out) {
+                                         uint32_t nmax, uint32_t* __restrict__ out) {
     pdl_wait();
+    const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t t = threadIdx.x;
     if (t <= NPOW) {
         const uint32_t i = sum->level_off[t];
@@ -494,16 +502,18 @@ __global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff,
 }
 
 __global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ base,
-                                            uint32_t nnodes) {
+                                            uint32_t nmax, const Summary* __restrict__ sum) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nnodes) nodes[i].chunk_base = base[i];
+    if (i < node_count(sum, nmax)) nodes[i].chunk_base = base[i];
 }
 
-__global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t* __restrict__ out) {
+// nchunks per node, zero for the padding up to nmax (the scan runs over nmax)
+__global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nmax, const Summary* __restrict__ sum,
+                                    uint32_t* __restrict__ out) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nnodes) out[i] = nodes[i].nchunks;
+    if (i < nmax) out[i] = i < node_count(sum, nmax) ? nodes[i].nchunks : 0u;
 }
 
 // chunk -> node map by binary search over the nodes' chunk_base.
