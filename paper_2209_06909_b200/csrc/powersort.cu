@@ -103,6 +103,7 @@ int fail(int code, const std::string& msg) {
         PS_CUDA(cudaGetLastError()); \
     } while (0)
 
+constexpr uint32_t NBARS = NPOW + MAX_SPINE + 8;  // fused-partition stages per sort
 constexpr uint64_t WS_MAGIC = 0x5053423230304b31ull;  // "PSB200K1"
 
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -183,7 +184,7 @@ struct Layout {
     uint64_t lvlP[16];
     // offsets
     uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
-        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts,
+        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts, bars,
         scantmp_u32, scantmp_i32, total;
 };
 
@@ -245,6 +246,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
         L.nat = take(L.rmax * 4);
         L.leafpar = take(L.rmax);
         L.cuts = take(L.chunks_max * 16);
+        L.bars = take(NBARS * 4);
     }
     L.b = take((L.rmax + 2) * 4);
     for (uint32_t l = 0; l < L.nlev; ++l) L.minlev[l] = take(L.lev_size[l] + 32);
@@ -402,11 +404,20 @@ struct MergeRunner {
     uint32_t pipe_grid_max;
 
     uint64_t nelem;  // elements in each buffer
+    uint32_t* bars;  // grid-barrier counters, one per fused-partition pipe launch
+    uint32_t nbars, bar_next;
+    bool fuse;
 
     int init(Bufs<K> b, uint64_t n, const Node* nd, const uint32_t* chunk2node, uint4* ct, uint32_t* e,
-             cudaStream_t st) {
+             uint32_t* bar, uint32_t nbar, cudaStream_t st) {
         bufs = b;
         nelem = n;
+        bars = bar;
+        nbars = nbar;
+        bar_next = 0;
+        static const bool no_fuse = getenv("PS_NO_FUSE") != nullptr;  // A/B: stand-alone partition launches
+        fuse = !no_fuse && bar != nullptr;
+        if (fuse) PS_CUDA(cudaMemsetAsync(bar, 0, (size_t)nbar * 4, st));
         nodes = nd;
         c2n = chunk2node;
         cuts = ct;
@@ -435,15 +446,24 @@ struct MergeRunner {
             PS_LAUNCH_CHECK();
         }
         if (c1 > c0) {
-            if (c1 - c0 > nbig) {
-                const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
-                launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1, cuts);
-                PS_LAUNCH_CHECK();
-                if (prof) prof->end(pp);
+            uint32_t* bar = nullptr;
+            const uint32_t grid = std::min(c1 - c0, pipe_grid_max);
+            if (c1 - c0 > nbig) {  // some node has several chunks: cuts needed
+                // fused into the pipe launch while each of its warps has <= 4 cuts to
+                // find (the searches are latency-bound; more cuts need the wide grid)
+                if (fuse && bar_next < nbars && c1 - c0 <= 4u * grid * (PIPE_THREADS / 32)) {
+                    bar = bars + bar_next++;  // partition fused into the pipe launch
+                } else {
+                    const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
+                    launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1,
+                             cuts);
+                    PS_LAUNCH_CHECK();
+                    if (prof) prof->end(pp);
+                }
             }
             const uint32_t units = c1 - c0;
-            launch_k(merge_pipe_kernel<K>, std::min(units, pipe_grid_max), PIPE_THREADS, psmem, s, 
-                bufs, nelem, nodes, c2n, cuts, c0, units, err);
+            launch_k(merge_pipe_kernel<K>, grid, PIPE_THREADS, psmem, s, bufs, nelem, nodes,
+                     c2n, cuts, c0, units, err, bar);
             PS_LAUNCH_CHECK();
         }
         return PS_OK;
@@ -636,7 +656,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     if (nnodes) {
         MergeRunner<K> mr;
         int rc = mr.init(bufs, (uint64_t)n, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts),
-                         err, s);
+                         err, at<uint32_t>(ws, L.bars), NBARS, s);
         if (rc) return rc;
         int stage = 0;
         auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint64_t cost, uint32_t nsmall,
@@ -690,7 +710,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
 // ---------------------------------------------------------------------------
 // N6 cross-shard merge (ps_shard_merge)
 struct ShardLayout {
-    uint64_t bounds, targets, err, lk, lv, tk, tv, nodes, c2n, cuts, chunks_max, total;
+    uint64_t bounds, targets, err, lk, lv, tk, tv, nodes, c2n, cuts, bars, chunks_max, total;
 };
 
 ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
@@ -713,6 +733,7 @@ ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
     L.nodes = take(4 * sizeof(Node));
     L.c2n = take(L.chunks_max * 4);
     L.cuts = take(L.chunks_max * 16);
+    L.bars = take(NBARS * 4);
     L.total = off;
     return L;
 }
@@ -868,7 +889,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
             b.v[1] = at<int32_t>(ws, L.tv);
         }
         MergeRunner<K> mr;
-        int rc = mr.init(b, slab, d_nodes, d_c2n, d_cuts, d_err, s);
+        int rc = mr.init(b, slab, d_nodes, d_c2n, d_cuts, d_err, at<uint32_t>(ws, L.bars), NBARS, s);
         if (rc) return rc;
         rc = mr.stage(0, (uint32_t)nds.size(), 0, (uint32_t)c2n.size(), nsmall, SMALL_NODE, nullptr, (int)lvl);
         if (rc) return rc;

@@ -58,6 +58,7 @@ enum : uint32_t {
     ERR_STACK = 8u,      // run stack above run_stack_capacity (policy.py:117-120)
     ERR_CUT = 16u,       // merge chunk larger than CHUNK_CAP
     ERR_POWER = 32u,     // power outside 1..NPOW-1
+    ERR_BARRIER = 64u,   // grid barrier timed out (CTAs not co-resident)
 };
 
 // One merge of the tree.  pos[0..arity] are the run boundaries (positions):

@@ -157,15 +157,13 @@ PS_DEV void warp_count3(const K* r0, const K* r1, const K* r2, uint32_t l0, uint
     out[2] = __shfl_sync(PS_FULL, res, 20);
 }
 
-// Partition: one warp per chunk of the stage [c0, c1); the first chunk of each
-// node gets the zero cut.
+// Partition: the cut of chunk c's (run, j) pair (whole warp; every chunk index
+// of a node past its first maps to one (a, j) with j*S < L[a]); the cut lands at
+// its index in the merged cut order.  The first chunk of each node gets the
+// zero cut.
 template <class K>
-__global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
-                                                              const uint32_t* __restrict__ chunk2node, uint32_t c0,
-                                                              uint32_t c1, uint4* __restrict__ cuts) {
-    pdl_wait();
-    const uint32_t c = c0 + blockIdx.x * 8 + warp_id();
-    if (c >= c1) return;
+PS_DEV void partition_chunk(const Bufs<K>& bufs, const Node* __restrict__ nodes, const uint32_t* __restrict__ chunk2node,
+                            uint32_t c, uint4* __restrict__ cuts) {
     const uint32_t lane = lane_id();
     const Node nd = nodes[chunk2node[c]];
     uint32_t q = c - nd.chunk_base;
@@ -204,6 +202,40 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
         mm += got[o] ? (got[o] - 1) / S : 0;
     }
     if (lane == 0) cuts[nd.chunk_base + 1 + mm] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+}
+
+// Stand-alone partition launch: one warp per chunk of [c0, c1).
+template <class K>
+__global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
+                                                              const uint32_t* __restrict__ chunk2node, uint32_t c0,
+                                                              uint32_t c1, uint4* __restrict__ cuts) {
+    pdl_wait();
+    const uint32_t c = c0 + blockIdx.x * 8 + warp_id();
+    if (c >= c1) return;
+    partition_chunk<K>(bufs, nodes, chunk2node, c, cuts);
+}
+
+// Barrier over all CTAs of a grid whose CTAs are co-resident (the persistent
+// pipe grid: <= one CTA per SM).  ctr is zeroed before the launch.  A bounded
+// spin turns a missing CTA into ERR_BARRIER instead of a hang.
+PS_DEV void grid_barrier(uint32_t* ctr, uint32_t nblocks, uint32_t* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        for (uint32_t spins = 0;; ++spins) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= nblocks) break;
+            __nanosleep(100);
+            if (spins > (1u << 23)) {
+                atomicOr(err, ERR_BARRIER);
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -553,8 +585,9 @@ template <class K>
 __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, uint64_t nelem,
                                                                   const Node* __restrict__ nodes,
                                                                   const uint32_t* __restrict__ chunk2node,
-                                                                  const uint4* __restrict__ cuts, uint32_t c0,
-                                                                  uint32_t nchunks, uint32_t* err) {
+                                                                  uint4* __restrict__ cuts, uint32_t c0,
+                                                                  uint32_t nchunks, uint32_t* err,
+                                                                  uint32_t* __restrict__ bar_ctr) {
     pdl_wait();
     using LY = PipeLayout<K>;
     constexpr uint32_t VT = pipe_vt<K>();
@@ -573,7 +606,17 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         }
         mbar_fence_init();
     }
-    __syncthreads();
+    if (bar_ctr) {
+        // fused partition: all warps of the grid compute the stage's cuts, then a
+        // grid barrier (a cut lands at its merged index, possibly in another
+        // CTA's chunk range)
+        const uint32_t nw = gridDim.x * (PIPE_THREADS / 32);
+        for (uint32_t c = blockIdx.x * (PIPE_THREADS / 32) + (tid >> 5); c < nchunks; c += nw)
+            partition_chunk<K>(bufs, nodes, chunk2node, c0 + c, cuts);
+        grid_barrier(bar_ctr, gridDim.x, err);
+    } else {
+        __syncthreads();
+    }
 
     if (tid < 32) {
         // ------------------------------ producer ------------------------------
