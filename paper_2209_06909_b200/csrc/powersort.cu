@@ -344,7 +344,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
-    launch_k(tree_spine_kernel, 1, 1, 0, s, b, r, k, strict, spine, nodes, Dd, sum);
+    launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Dd, Dd, (int64_t)r + 1, false, false,

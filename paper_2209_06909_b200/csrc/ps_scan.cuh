@@ -125,6 +125,50 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const T* in, T
     if (total_out && threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) *total_out = op(c, total);
 }
 
+// Small n: one CTA walks the tiles in order with a running carry (one launch
+// instead of reduce + recursive scan + apply).
+constexpr int64_t SCAN_SEQ_MAX = 8 * SCAN_BLK;
+
+template <class T, class Op>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_seq_kernel(const T* in, T* out, int64_t n, int reverse,
+                                                                int exclusive, T* total_out) {
+    pdl_wait();
+    __shared__ T items[SCAN_BLK];
+    __shared__ T sw[32];
+    Op op;
+    T carry = Op::id();
+    for (int64_t base = 0; base < n; base += SCAN_BLK) {
+        for (int i = threadIdx.x; i < SCAN_BLK; i += SCAN_THREADS) {
+            int64_t g = base + i;
+            items[i] = g < n ? in[reverse ? n - 1 - g : g] : Op::id();
+        }
+        __syncthreads();
+        T loc[SCAN_ITEMS];
+        T acc = Op::id();
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            loc[j] = items[threadIdx.x * SCAN_ITEMS + j];
+            acc = op(acc, loc[j]);
+        }
+        T total;
+        T pre = op(carry, block_exclusive<T, Op>(acc, total, sw));
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            T inc = op(pre, loc[j]);
+            items[threadIdx.x * SCAN_ITEMS + j] = exclusive ? pre : inc;
+            pre = inc;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < SCAN_BLK; i += SCAN_THREADS) {
+            int64_t g = base + i;
+            if (g < n) out[reverse ? n - 1 - g : g] = items[i];
+        }
+        carry = op(carry, total);
+        __syncthreads();
+    }
+    if (total_out && threadIdx.x == 0) *total_out = carry;
+}
+
 // Elements of temporary storage device_scan needs for n items.
 inline int64_t scan_tmp_elems(int64_t n) {
     int64_t t = 0;
@@ -142,8 +186,8 @@ cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclu
                         cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     int64_t nb = (n + SCAN_BLK - 1) / SCAN_BLK;
-    if (nb == 1) {
-        launch_k(scan_apply_kernel<T, Op>, 1, SCAN_THREADS, 0, s, in, out, n, nullptr, reverse, exclusive, total_out);
+    if (n <= SCAN_SEQ_MAX) {
+        launch_k(scan_seq_kernel<T, Op>, 1, SCAN_THREADS, 0, s, in, out, n, (int)reverse, (int)exclusive, total_out);
         launch_counter()++;
         return cudaGetLastError();
     }

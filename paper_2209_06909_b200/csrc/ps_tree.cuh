@@ -273,51 +273,57 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
     }
 }
 
-// T4: the spine and _merge_down (policy.py:146-175), one thread.
+// T4: the spine and _merge_down (policy.py:146-175): staged by the CTA, replayed by one thread.
 __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                                   uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
                                   int32_t* __restrict__ Ddiff, Summary* sum) {
     pdl_wait();
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // the stack entries are staged and sorted by the CTA, their run starts are
+    // gathered in parallel; one thread then replays _merge_down from shared memory
+    __shared__ uint32_t s_list[MAX_SPINE];
+    __shared__ uint32_t s_beta[MAX_SPINE + 2];  // beta[1] = 0, beta[h] = s_{h-1}; [H+1] = first run_begin
+    __shared__ uint32_t s_bval[MAX_SPINE + 2];  // b[beta[h]]
+    __shared__ uint32_t s_br;
+    const uint32_t t = threadIdx.x;
     uint32_t H = sum->nspine;
     if (H > MAX_SPINE) {
-        atomicOr(&sum->err, ERR_SPINE);
+        if (t == 0) atomicOr(&sum->err, ERR_SPINE);
         H = MAX_SPINE;
     }
-    // sort (insertion sort, H <= MAX_SPINE)
-    for (uint32_t i = 1; i < H; ++i) {
-        uint32_t x = spine_list[i];
-        int jj = (int)i - 1;
-        while (jj >= 0 && spine_list[jj] > x) {
-            spine_list[jj + 1] = spine_list[jj];
-            jj--;
-        }
-        spine_list[jj + 1] = x;
+    if (t < H) {  // rank sort of distinct boundary indices
+        const uint32_t x = spine_list[t];
+        uint32_t rank = 0;
+        for (uint32_t i = 0; i < H; ++i) rank += spine_list[i] < x;
+        s_list[rank] = x;
     }
+    __syncthreads();
+    for (uint32_t h = t + 1; h <= H + 1; h += blockDim.x)
+        s_beta[h] = h == 1 ? 0u : (h <= H ? s_list[h - 2] : (H ? s_list[H - 1] : 0u));
+    __syncthreads();
+    for (uint32_t h = t + 1; h <= H + 1; h += blockDim.x) s_bval[h] = b[s_beta[h]];
+    if (t == 0) s_br = b[r];
+    __syncthreads();
+    if (t != 0) return;
     const uint32_t nmain = sum->level_off[NPOW];
     uint32_t nn = 0;
-    // stack begins (boundary indices): beta[1] = 0, beta[h] = s_{h-1}
-    uint32_t beta[MAX_SPINE + 2];
     uint32_t height = H;
-    beta[1] = 0;
-    for (uint32_t h = 2; h <= H; ++h) beta[h] = spine_list[h - 2];
-    uint32_t run_begin = H ? spine_list[H - 1] : 0;
-    auto emit = [&](const uint32_t* bb, uint32_t w) {
+    uint32_t run_begin = H + 1;  // index into s_beta / s_bval
+    auto emit = [&](const uint32_t* hh, uint32_t w) {
         Node nd;
         for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = 0;
-        for (uint32_t i = 0; i < w; ++i) nd.pos[i] = b[bb[i]];
-        nd.pos[w] = b[r];
+        for (uint32_t i = 0; i < w; ++i) nd.pos[i] = s_bval[hh[i]];
+        nd.pos[w] = s_br;
         nd.arity = (uint8_t)w;
         nd.parity = 0;
         nd.power = 0;
         nd.flags = 1;
-        nd.probe = bb[1];
+        nd.probe = s_beta[hh[1]];
         nd.chunk_base = 0;
         nd.nchunks = 0;
         nd.order = nn;
         nodes[nmain + nn] = nd;
         nn++;
-        atomicAdd(&Ddiff[bb[0] + 1], 1);
+        atomicAdd(&Ddiff[s_beta[hh[0]] + 1], 1);
         atomicAdd(&Ddiff[r], -1);
     };
     if (H > 0) {
@@ -325,33 +331,33 @@ __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, ui
             const uint32_t n_runs = height + 1;
             const uint32_t rem = n_runs % 3;
             if (rem == 0) {
-                const uint32_t b2 = beta[height--];
-                const uint32_t b1 = beta[height--];
-                const uint32_t bb[3] = {b1, b2, run_begin};
-                emit(bb, 3);
-                run_begin = b1;
+                const uint32_t h2 = height--;
+                const uint32_t h1 = height--;
+                const uint32_t hh[3] = {h1, h2, run_begin};
+                emit(hh, 3);
+                run_begin = h1;
             } else if (rem == 2) {
-                const uint32_t b1 = beta[height--];
-                const uint32_t bb[2] = {b1, run_begin};
-                emit(bb, 2);
-                run_begin = b1;
+                const uint32_t h1 = height--;
+                const uint32_t hh[2] = {h1, run_begin};
+                emit(hh, 2);
+                run_begin = h1;
             }
             while (height) {
-                const uint32_t b3 = beta[height--];
-                const uint32_t b2 = beta[height--];
-                const uint32_t b1 = beta[height--];
-                const uint32_t bb[4] = {b1, b2, b3, run_begin};
-                emit(bb, 4);
-                run_begin = b1;
+                const uint32_t h3 = height--;
+                const uint32_t h2 = height--;
+                const uint32_t h1 = height--;
+                const uint32_t hh[4] = {h1, h2, h3, run_begin};
+                emit(hh, 4);
+                run_begin = h1;
             }
         } else {
             while (height) {
                 const uint32_t cnt = (k - 1) < height ? (k - 1) : height;
-                uint32_t bb[4];
-                for (uint32_t i = 0; i < cnt; ++i) bb[cnt - 1 - i] = beta[height--];
-                bb[cnt] = run_begin;
-                emit(bb, cnt + 1);
-                run_begin = bb[0];
+                uint32_t hh[4];
+                for (uint32_t i = 0; i < cnt; ++i) hh[cnt - 1 - i] = height--;
+                hh[cnt] = run_begin;
+                emit(hh, cnt + 1);
+                run_begin = hh[0];
             }
         }
     }
