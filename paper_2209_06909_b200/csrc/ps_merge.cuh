@@ -447,6 +447,11 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
 // one node (a unit of one segment may be several chunks of one node; several
 // segments pack consecutive whole small-to-mid nodes or chunk ranges).
 constexpr uint32_t MAXSEG = 32;
+// PS_XR2=1: two first-pass scratch buffers used alternately, so a unit's end
+// needs no CTA barrier (needs fewer consumers to fit shared memory)
+#ifndef PS_XR2
+#define PS_XR2 0
+#endif
 
 template <class K>
 struct PipeLayout {
@@ -462,6 +467,7 @@ struct PipeLayout {
     static constexpr uint32_t SLOT = align16c(cmax(KEY_BYTES + VAL_BYTES, PADN * RECB));
     // scratch: first-pass records X || Y of every segment (or the 2-way output)
     static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
+    static constexpr uint32_t NXR = PS_XR2 ? 2 : 1;  // scratch buffers (2: alternate by unit)
 };
 
 struct PipeSeg {
@@ -479,7 +485,8 @@ struct PipeDesc {
 
 template <class K>
 size_t merge_pipe_smem_bytes() {
-    return PIPE_SLOTS * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::SCRATCH + PIPE_SLOTS * sizeof(PipeDesc) + 64;
+    return PIPE_SLOTS * (size_t)PipeLayout<K>::SLOT + PipeLayout<K>::NXR * (size_t)PipeLayout<K>::SCRATCH +
+           PIPE_SLOTS * sizeof(PipeDesc) + 64;
 }
 
 // Merge-path cursors.  WinCur merges two TMA-landed SoA windows, RecCur two padded record runs;
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     constexpr uint32_t VT = pipe_vt<K>();
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* scratch = smem + PIPE_SLOTS * LY::SLOT;
-    PipeDesc* desc = reinterpret_cast<PipeDesc*>(scratch + LY::SCRATCH);
+    PipeDesc* desc = reinterpret_cast<PipeDesc*>(scratch + LY::NXR * LY::SCRATCH);
     uint64_t* bars = reinterpret_cast<uint64_t*>(desc + PIPE_SLOTS);
     uint64_t* full = bars;                // [PIPE_SLOTS]
     uint64_t* empty = bars + PIPE_SLOTS;  // [PIPE_SLOTS]
@@ -832,7 +839,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     // ------------------------------ consumers ---------------------------------
     const uint32_t ctid = tid - 32;
     const uint32_t clane = ctid & 31, wid = ctid >> 5;
-    Rec<K>* const xr = reinterpret_cast<Rec<K>*>(scratch);
+    Rec<K>* const xr0 = reinterpret_cast<Rec<K>*>(scratch);
     constexpr uint32_t ER = sizeof(K) == 4 ? 4 : 2;  // records per 16-byte store group
     const uint32_t ob = VT * ctid;                   // this thread's first output of a pass layout
     const uint32_t r0w = VT * 32 * wid, r1w = VT * 32 * (wid + 1);  // this warp's outputs
@@ -844,6 +851,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         PT_USTART
         const PipeDesc& d = desc[slot];
         if (d.done) break;
+        Rec<K>* const xr = xr0 + (LY::NXR == 2 ? (i & 1) * (LY::SCRATCH / LY::RECB) : 0);
+        const bool single_pass = d.nseg == 1 && d.seg[0].w < 3;  // read before the slot is released
         uint8_t* sbase = smem + slot * LY::SLOT;
         Rec<K>* const orec = reinterpret_cast<Rec<K>*>(sbase);
         auto wincur = [&](const PipeSeg& g, uint32_t a, uint32_t base, uint32_t o, uint32_t oe) {
@@ -991,8 +1000,9 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         }
         __syncwarp();
         if (clane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
-        // scratch xr is rewritten by the next unit's first pass
-        consumer_sync();
+        // scratch xr is rewritten by the next unit's first pass (with two scratch
+        // buffers only single-pass units, which have no barrier of their own, need it)
+        if (LY::NXR == 1 || single_pass) consumer_sync();
         PT_MARK(7)
         PT_COUNT(8)
     }
