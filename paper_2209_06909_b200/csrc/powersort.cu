@@ -943,6 +943,8 @@ int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_conf
     memset(stats, 0, sizeof(*stats));
     if (n == 0) return PS_OK;  // policy.py:207-209
     if (!keys || !values || !workspace) return fail(PS_EINVAL, "NULL pointer argument");
+    if (((uintptr_t)keys | (uintptr_t)values | (uintptr_t)workspace) & 15)
+        return fail(PS_EINVAL, "keys, values and workspace must be 16-byte aligned (TMA and vector access)");
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = (uint8_t*)workspace;
     switch (dtype) {

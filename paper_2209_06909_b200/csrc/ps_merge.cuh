@@ -275,6 +275,18 @@ PS_DEV void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes, ui
         "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA bulk store smem -> global (bulk async-group), its commit and waits
+PS_DEV void tma_store_1d(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+                 "r"(smem_u32(smem_src)), "r"(bytes)
+                 : "memory");
+}
+PS_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+PS_DEV void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+PS_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the async proxy (TMA)
+PS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // named barrier 1 over the consumer warps only
 #ifndef PS_SLOTS
 #define PS_SLOTS 2
@@ -452,6 +464,11 @@ constexpr uint32_t MAXSEG = 32;
 #ifndef PS_XR2
 #define PS_XR2 0
 #endif
+// PS_BULK_STORE=1: single-segment 3/4-way units leave through TMA bulk stores
+// issued by the producer warp (the consumers only write SoA outputs to the slot)
+#ifndef PS_BULK_STORE
+#define PS_BULK_STORE 1
+#endif
 
 template <class K>
 struct PipeLayout {
@@ -468,6 +485,10 @@ struct PipeLayout {
     // scratch: first-pass records X || Y of every segment (or the 2-way output)
     static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
     static constexpr uint32_t NXR = PS_XR2 ? 2 : 1;  // scratch buffers (2: alternate by unit)
+    // SoA output of a bulk-stored unit inside its slot: keys at 0, values at OV
+    static constexpr uint32_t EPK = 16 / (uint32_t)sizeof(K);  // keys per 16 bytes
+    static constexpr uint32_t OV = align16c((PADN + 4) * (uint32_t)sizeof(K));
+    static_assert(OV + (PADN + 4) * 4 <= SLOT, "SoA outputs must fit the slot");
 };
 
 struct PipeSeg {
@@ -570,6 +591,36 @@ PS_DEV void single_merge(C& c, Rec<K>* out) {
     for (uint32_t t = 0; t < pipe_vt<K>(); ++t) c.step(outp, t);
 }
 
+// Pass 2 into SoA outputs (keys[o], vals[o]) for the bulk-store path.
+template <class K>
+PS_DEV void single_merge_soa(RecCur<K>& c, K* outk, int32_t* outv) {
+    if (c.o >= c.oe) return;
+    uint32_t lo = c.o > c.lb ? c.o - c.lb : 0, hi = c.o < c.la ? c.o : c.la;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        const bool le = !(c.keyB(c.o - 1 - m) < c.keyA(m));
+        lo = le ? m + 1 : lo;
+        hi = le ? hi : m;
+    }
+    c.i = lo;
+    c.j = c.o - lo;
+    c.heads();
+    K* ok = outk + c.o;
+    int32_t* ov = outv + c.o;
+#pragma unroll
+    for (uint32_t t = 0; t < pipe_vt<K>(); ++t) {
+        const bool takeA = c.i < c.la && (c.j >= c.lb || !(c.b.k < c.a.k));
+        const Rec<K> r = takeA ? c.a : c.b;
+        ok[t] = r.k;
+        ov[t] = r.v;
+        c.i += takeA;
+        c.j += !takeA;
+        const Rec<K> nx = c.r[takeA ? c.ia(c.i) : c.ib(c.j)];
+        c.a = takeA ? nx : c.a;
+        c.b = takeA ? c.b : nx;
+    }
+}
+
 // A TMA-landed input window: SoA keys / values, unpadded.
 template <class K>
 struct Win {
@@ -631,6 +682,36 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         const uint32_t cbeg = c0 + (uint32_t)(((uint64_t)nchunks * blockIdx.x) / gridDim.x);
         const uint32_t cend = c0 + (uint32_t)(((uint64_t)nchunks * (blockIdx.x + 1)) / gridDim.x);
         uint32_t unit = 0;
+        uint32_t pend = 0;  // slots whose (bulk-store) unit still has to leave
+        // Stores the bulk unit that occupied slot sl (its descriptor is still there):
+        // the 16-byte-aligned middle of the keys and of the values with one TMA
+        // bulk store each, the <= 3 edge elements at each end with lane stores.
+        auto bulk_store = [&](uint32_t sl) {
+            const PipeSeg& g = desc[sl].seg[0];
+            const uint8_t* sb = smem + sl * LY::SLOT;
+            const K* sk = reinterpret_cast<const K*>(sb);
+            const int32_t* sv = reinterpret_cast<const int32_t*>(sb + LY::OV);
+            K* dk = bufs.kb(g.par);
+            int32_t* dv = bufs.vb(g.par);
+            const uint64_t out = g.out;
+            const uint32_t T = g.T;
+            const uint32_t pk = (uint32_t)(out % LY::EPK), pv = (uint32_t)(out % 4);
+            const uint32_t k0 = min(T, (LY::EPK - pk) % LY::EPK), v0 = min(T, (4 - pv) % 4);
+            const uint32_t kt = (uint32_t)((out + T) % LY::EPK), vt = (uint32_t)((out + T) % 4);
+            const uint32_t k1 = max(k0, T >= kt ? T - kt : 0u), v1 = max(v0, T >= vt ? T - vt : 0u);
+            if (lane == 0) {
+                if (k1 > k0) tma_store_1d(dk + out + k0, sk + pk + k0, (k1 - k0) * (uint32_t)sizeof(K));
+                if (v1 > v0) tma_store_1d(dv + out + v0, sv + pv + v0, (v1 - v0) * 4u);
+                bulk_commit();
+            }
+            const uint32_t q = lane & 3;
+            const uint32_t e = (lane & 4) ? k1 + q : q;  // keys: head lanes 0-3, tail 4-7
+            if (lane < 8 && e < ((lane & 4) ? T : k0)) dk[out + e] = sk[pk + e];
+            const uint32_t f = (lane & 4) ? v1 + q : q;  // values: head lanes 8-11, tail 12-15
+            if (lane >= 8 && lane < 16 && f < ((lane & 4) ? T : v0)) dv[out + f] = sv[pv + f];
+            if (lane == 0) bulk_wait_read_all();  // the slot may be overwritten afterwards
+            __syncwarp();
+        };
         PT_START(lane == 0)
         for (uint32_t c = cbeg; c < cend;) {
             // batch descriptors of chunks c .. c+31 (lane l <-> chunk c+l)
@@ -745,6 +826,10 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 // ---- stage the unit into slot (unit % PIPE_SLOTS) ----
                 const uint32_t slot = unit % PIPE_SLOTS;
                 if (unit >= PIPE_SLOTS) mbar_wait(&empty[slot], ((unit / PIPE_SLOTS) - 1) & 1);
+                if (pend & (1u << slot)) {
+                    bulk_store(slot);
+                    pend &= ~(1u << slot);
+                }
                 PT_MARK(1)
                 uint8_t* sbase = smem + slot * LY::SLOT;
                 PipeDesc& d = desc[slot];
@@ -818,6 +903,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 }
                 for (int dd = 16; dd; dd >>= 1) tx += __shfl_xor_sync(PS_FULL, tx, dd);
                 __syncwarp();
+                if (PS_BULK_STORE && nseg == 1 && __shfl_sync(PS_FULL, w, 0) >= 3) pend |= 1u << slot;
                 if (lane == 0) mbar_arrive_tx(&full[slot], tx);
                 PT_MARK(2)
                 PT_COUNT(3)
@@ -826,13 +912,23 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             }
             c += nvalid;
         }
-        // termination marker
+        // termination marker, then the units still in flight leave
         const uint32_t slot = unit % PIPE_SLOTS;
         if (unit >= PIPE_SLOTS) mbar_wait(&empty[slot], ((unit / PIPE_SLOTS) - 1) & 1);
+        if (pend & (1u << slot)) bulk_store(slot);
+        pend &= ~(1u << slot);
+        __syncwarp();
         if (lane == 0) {
             desc[slot].done = 1;
             mbar_arrive(&full[slot]);
         }
+        for (uint32_t v = unit >= PIPE_SLOTS - 1 ? unit - (PIPE_SLOTS - 1) : 0; v < unit; ++v) {
+            const uint32_t sl = v % PIPE_SLOTS;
+            if (!(pend & (1u << sl))) continue;
+            mbar_wait(&empty[sl], (v / PIPE_SLOTS) & 1);
+            bulk_store(sl);
+        }
+        if (lane == 0) bulk_wait_all();
         return;
     }
 
@@ -897,6 +993,17 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 p0.base = al;
                 p0.o = o0;
                 p0.oe = o1;
+                if (PS_BULK_STORE) {
+                    // SoA outputs phase-aligned with their destinations; the producer
+                    // stores them with TMA once every warp has arrived on empty[slot]
+                    single_merge_soa(p0, reinterpret_cast<K*>(sbase) + (uint32_t)(out % LY::EPK),
+                                     reinterpret_cast<int32_t*>(sbase + LY::OV) + (uint32_t)(out % 4));
+                    fence_proxy_async_smem();
+                    PT_WARP(24)
+                    __syncwarp();
+                    PT_MARK(6)
+                    goto unit_done;
+                }
                 single_merge(p0, orec);
                 res = orec;
             } else {
@@ -999,6 +1106,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             }
         }
         __syncwarp();
+    unit_done:
         if (clane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
         // scratch xr is rewritten by the next unit's first pass (with two scratch
         // buffers only single-pass units, which have no barrier of their own, need it)

@@ -177,6 +177,13 @@ def _sort_tensor(keys, values, config, values_mode, collect_runs=True):
     lib = _lib.load()
     dt = _dtype_id(keys)
     cfg = _cfg_struct(config, values_mode)
+    if keys.data_ptr() % 16 or values.data_ptr() % 16:
+        # the C ABI needs 16-byte aligned arrays (TMA); sort aligned copies of views
+        k2, v2 = keys.clone(), values.clone()
+        stats = _sort_tensor(k2, v2, config, values_mode, collect_runs)
+        keys.copy_(k2)
+        values.copy_(v2)
+        return stats
     with torch.cuda.device(keys.device):
         nbytes = lib.ps_workspace_size(n, dt, cfg)
         if nbytes == 0:

@@ -142,6 +142,28 @@ def test_values_payload_permuted(dev):
     assert np.array_equal(keys.cpu().numpy(), keys_np[perm])
 
 
+def test_unaligned_tensor_views(dev):
+    # views at 4-byte offsets: the C ABI rejects them (TMA needs 16-byte
+    # alignment), the Python entry point sorts aligned copies
+    from paper_2209_06909_b200 import _lib
+
+    base_np = workloads.cfg2(n=100_003, seed=2)
+    full = torch.from_numpy(base_np).to(dev)
+    view = full[1:]
+    assert view.data_ptr() % 16 != 0
+    out, perm, stats = stable_argsort(view, SortConfig())
+    ref = oracle.sort(base_np[1:])
+    assert np.array_equal(perm.cpu().numpy(), ref.values)
+    vals = torch.zeros(view.numel(), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    cfg = _lib.PsConfig(4, 3, 24, 0, _lib.VALUES_ARGSORT)
+    st = _lib.PsStats()
+    ws = torch.empty(lib.ps_workspace_size(view.numel(), 0, cfg), dtype=torch.uint8, device=dev)
+    rc = lib.ps_sort(0, view.data_ptr(), vals.data_ptr(), view.numel(), cfg, ws.data_ptr(), ws.numel(), st,
+                     torch.cuda.current_stream(dev).cuda_stream)
+    assert rc == 1  # PS_EINVAL
+
+
 def test_list_api_records(dev):
     from operator import itemgetter
 
