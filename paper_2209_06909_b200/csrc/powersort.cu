@@ -449,9 +449,9 @@ struct MergeRunner {
             uint32_t* bar = nullptr;
             const uint32_t grid = std::min(c1 - c0, pipe_grid_max);
             if (c1 - c0 > nbig) {  // some node has several chunks: cuts needed
-                // fused into the pipe launch while each of its warps has <= 4 cuts to
+                // fused into the pipe launch while each of its warps has <= 1 cut to
                 // find (the searches are latency-bound; more cuts need the wide grid)
-                if (fuse && bar_next < nbars && c1 - c0 <= 4u * grid * (PIPE_THREADS / 32)) {
+                if (fuse && bar_next < nbars && c1 - c0 <= grid * (PIPE_THREADS / 32)) {
                     bar = bars + bar_next++;  // partition fused into the pipe launch
                 } else {
                     const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
@@ -1134,6 +1134,11 @@ extern "C" int ps_debug_pipe_timing(unsigned long long* out, int reset) {
         unsigned long long z[40] = {0};
         cudaMemcpyToSymbol(ps::g_pipe_tim, z, sizeof(z));
     }
+    return PS_OK;
+}
+extern "C" int ps_debug_cta_timing(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, ps::g_cta_tim, sizeof(ps::g_cta_tim));
     return PS_OK;
 }
 #endif

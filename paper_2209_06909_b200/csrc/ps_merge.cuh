@@ -419,6 +419,16 @@ inline uint32_t small_group(uint32_t maxsz) {
 // Optional clock64 phase counters of the pipe kernel (build with -DPS_PIPE_TIMING)
 #ifdef PS_PIPE_TIMING
 __device__ unsigned long long g_pipe_tim[40];
+// per-CTA globaltimer stamps of the last pipe launch: start, after the fused
+// partition, first unit ready (consumer 0), consumers done, producer done
+__device__ unsigned long long g_cta_tim[1024][5];
+PS_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PT_CTA(idx) \
+    if (blockIdx.x < 1024) g_cta_tim[blockIdx.x][idx] = gtimer();
 #define PT_START(on) long long _pt0 = clock64(); const bool _pton = (on);
 #define PT_MARK(idx)                                                         \
     if (_pton) {                                                             \
@@ -435,6 +445,7 @@ __device__ unsigned long long g_pipe_tim[40];
 #else
 #define PT_USTART
 #define PT_WARP(idx)
+#define PT_CTA(idx)
 #define PT_START(on)
 #define PT_MARK(idx)
 #define PT_COUNT(idx)
@@ -658,6 +669,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     __shared__ uint64_t s_e0[MAXSEG][MAX_WAY];  // producer: global element index of each window
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
+        PT_CTA(0)
         for (uint32_t sl = 0; sl < PIPE_SLOTS; ++sl) {
             mbar_init(&full[sl], 1);
             mbar_init(&empty[sl], PIPE_CONSUMERS / 32);
@@ -674,6 +686,9 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         grid_barrier(bar_ctr, gridDim.x, err);
     } else {
         __syncthreads();
+    }
+    if (tid == 0) {
+        PT_CTA(1)
     }
 
     if (tid < 32) {
@@ -929,6 +944,9 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
             bulk_store(sl);
         }
         if (lane == 0) bulk_wait_all();
+        if (lane == 0) {
+            PT_CTA(4)
+        }
         return;
     }
 
@@ -943,10 +961,18 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
     for (uint32_t i = 0;; ++i) {
         const uint32_t slot = i % PIPE_SLOTS;
         mbar_wait(&full[slot], (i / PIPE_SLOTS) & 1);
+        if (i == 0 && ctid == 0) {
+            PT_CTA(2)
+        }
         PT_MARK(4)
         PT_USTART
         const PipeDesc& d = desc[slot];
-        if (d.done) break;
+        if (d.done) {
+            if (ctid == 0) {
+                PT_CTA(3)
+            }
+            break;
+        }
         Rec<K>* const xr = xr0 + (LY::NXR == 2 ? (i & 1) * (LY::SCRATCH / LY::RECB) : 0);
         const bool single_pass = d.nseg == 1 && d.seg[0].w < 3;  // read before the slot is released
         uint8_t* sbase = smem + slot * LY::SLOT;

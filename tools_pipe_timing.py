@@ -28,3 +28,14 @@ for i, nm in enumerate(names):
     print('%-14s total %14d   per unit %10.1f cycles' % (nm, v, per))
 print('per-warp pass1 work (cycles/unit, to the barrier):', ' '.join('%6.0f' % (int(buf[16 + w]) / cu) for w in range(8)))
 print('per-warp pass2 work (cycles/unit, since unit start):', ' '.join('%6.0f' % (int(buf[24 + w]) / cu) for w in range(8)))
+# per-CTA stamps of the last pipe launch of the sort (the root merge)
+cta = np.zeros((1024, 5), dtype=np.uint64)
+lib.ps_debug_cta_timing.argtypes = [ctypes.c_void_p]
+lib.ps_debug_cta_timing(cta.ctypes.data)
+g = int(np.count_nonzero(cta[:, 0]))
+c = cta[:g].astype(np.int64)
+t0 = c[:, 0].min()
+print('last launch: %d CTAs; us from the first CTA start:' % g)
+for j, nm in enumerate(['start', 'after partition', 'first unit ready', 'consumers done', 'producer done']):
+    v = (c[:, j] - t0) / 1e3
+    print('  %-18s min %7.2f  median %7.2f  max %7.2f' % (nm, v.min(), np.median(v), v.max()))
