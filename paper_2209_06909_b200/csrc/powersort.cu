@@ -184,7 +184,7 @@ struct Layout {
     uint64_t lvlP[16];
     // offsets
     uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
-        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts, bars,
+        minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts, bars, tile_first,
         scantmp_u32, scantmp_i32, total;
 };
 
@@ -236,6 +236,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
         L.cg = take((L.ngroups + 1) * 4);
         L.Fg = take((L.ngroups + 1) * 4);
         L.Ft = take((L.ntiles + 1) * 4);
+        L.tile_first = take((L.ntiles + 1) * 4);
         if (m <= MAX_M_TILED) {
             L.tile_tab = take(L.ntiles * M1 * 8);
             for (uint64_t l = 0; l < L.tab_levels; ++l) {
@@ -595,7 +596,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             PS_LAUNCH_CHECK();
         }
         launch_k(rd_emit_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
-                                               at<uint64_t>(ws, L.lvl_ent[0]), b, nat, err);
+                 at<uint64_t>(ws, L.lvl_ent[0]), b, nat, at<uint32_t>(ws, L.tile_first), err);
         PS_LAUNCH_CHECK();
     } else {
         launch_k(rd_serial_kernel, 1, 32, 0, s, ty, (uint64_t)n, m, b, nat, sum);
@@ -636,17 +637,20 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     {
         const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M));
         const unsigned grid = grid_for((uint64_t)n, FORM_TILE);
+        static_assert(FORM_TILE == TILE, "leaf formation tiles are run detection's chain tiles");
+        // per-tile first leaf, written by rd_emit_kernel (tiled detector only)
+        const uint32_t* tile_first = m <= MAX_M_TILED ? at<uint32_t>(ws, L.tile_first) : nullptr;
         const int ph = prof.begin(2, -1, r, 0, n * ((int64_t)sizeof(K) + rec_bytes));
         if (argsort) {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             launch_k(form_leaves_kernel<K, true>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r, ty,
-                                                                         (uint32_t)m);
+                     (uint32_t)m, tile_first);
         } else {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-            launch_k(form_leaves_kernel<K, false>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r, ty,
-                                                                          (uint32_t)m);
+            launch_k(form_leaves_kernel<K, false>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r,
+                     ty, (uint32_t)m, tile_first);
         }
         PS_LAUNCH_CHECK();
         prof.end(ph);

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
                                                                    const uint32_t* __restrict__ b,
                                                                    const uint32_t* __restrict__ nat,
                                                                    const uint8_t* __restrict__ leafpar, uint32_t r,
-                                                                   const uint32_t* __restrict__ ty, uint32_t m) {
+                                                                   const uint32_t* __restrict__ ty, uint32_t m,
+                                                                   const uint32_t* __restrict__ tile_first) {
     pdl_wait();
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
@@ -93,7 +94,19 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     const uint64_t t0 = (uint64_t)blockIdx.x * FORM_TILE;
     const uint64_t t1 = min(t0 + FORM_TILE, n);
     const uint32_t tid = threadIdx.x;
-    if (tid < 32) {
+    if (tile_first) {
+        // leaves covering t0 and t1-1 from the per-tile table of run detection
+        if (tid == 0) {
+            const uint32_t lo = tile_first[blockIdx.x];
+            uint32_t lo2 = r - 1;
+            if (t1 < n) {
+                const uint32_t nx = tile_first[blockIdx.x + 1];  // covers t1
+                lo2 = b[nx] == t1 ? nx - 1 : nx;
+            }
+            s_first = lo;
+            s_cnt = lo2 - lo + 1;
+        }
+    } else if (tid < 32) {
         // last leaf with b <= t0 and last leaf with b <= t1-1: 32-ary warp searches
         const uint32_t lo = warp_last_le(b, r, (uint32_t)t0);
         const uint32_t lo2 = warp_last_le(b, r, (uint32_t)(t1 - 1));
@@ -118,6 +131,81 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     // belongs to the owner of its lower position), so the reordering is safe.
     constexpr uint32_t FORM_BATCH = 4;
     enum : uint8_t { F_NONE = 0, F_COPY = 1, F_ARGV = 2, F_SWAP = 3 };
+    if (cnt <= 16) {
+        // few (long) leaves: leaf by leaf, all threads striding over its positions
+        for (uint32_t li = 0; li < cnt; ++li) {
+            const uint64_t bj = sb[li], ej = sb[li + 1];
+            const uint32_t len = (uint32_t)(ej - bj);
+            if (snat[li] < len) continue;  // extended window, below
+            const uint32_t par = spar[li];
+            bool desc = false;
+            if (len >= 2) {
+                const uint64_t q = bj + 1;
+                desc = !((ty[q >> 5] >> (q & 31)) & 1u);
+            }
+            K* dk = bufs.kb(par);
+            int32_t* dv = bufs.vb(par);
+            const uint64_t lo = bj > t0 ? bj : t0, hi = ej < t1 ? ej : t1;
+            if (!desc) {
+                if (!par && !ARGSORT) continue;  // in place already
+                for (uint64_t p0 = lo + tid; p0 < hi; p0 += FORM_THREADS * FORM_BATCH) {
+                    K kk[FORM_BATCH];
+                    int32_t vv[FORM_BATCH];
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
+                        if (p < hi) {
+                            if (par) kk[u] = K0[p];
+                            vv[u] = ARGSORT ? (int32_t)p : V0[p];
+                        }
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
+                        if (p < hi) {
+                            if (par) dk[p] = kk[u];
+                            dv[p] = vv[u];
+                        }
+                    }
+                }
+            } else {
+                // mirrored pairs (p, s - p) belong to the owner of p <= s - p
+                const uint64_t sm = bj + ej - 1;
+                const uint64_t hi2 = hi < sm / 2 + 1 ? hi : sm / 2 + 1;
+                for (uint64_t p0 = lo + tid; p0 < hi2; p0 += FORM_THREADS * FORM_BATCH) {
+                    K ka[FORM_BATCH], kb[FORM_BATCH];
+                    int32_t va[FORM_BATCH], vb[FORM_BATCH];
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
+                        if (p < hi2) {
+                            const uint64_t mr = sm - p;
+                            ka[u] = K0[p];
+                            kb[u] = K0[mr];
+                            va[u] = ARGSORT ? (int32_t)p : V0[p];
+                            vb[u] = ARGSORT ? (int32_t)mr : V0[mr];
+                        }
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
+                        if (p < hi2) {
+                            const uint64_t mr = sm - p;
+                            if (p < mr) {
+                                dk[p] = kb[u];
+                                dv[p] = vb[u];
+                                dk[mr] = ka[u];
+                                dv[mr] = va[u];
+                            } else if (par || ARGSORT) {  // the center of an odd-length run
+                                dk[p] = ka[u];
+                                dv[p] = va[u];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else
     for (uint64_t pos0 = t0 + tid; pos0 < t1; pos0 += FORM_THREADS * FORM_BATCH) {
         uint8_t act[FORM_BATCH];
         uint8_t parb[FORM_BATCH];
@@ -184,6 +272,9 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     }
 
     // ---- extended windows starting in this tile: stable rank ---------------
+    bool anywin = false;
+    for (uint32_t i = tid; i < cnt; i += FORM_THREADS) anywin |= (snat[i] < sb[i + 1] - sb[i]) && (sb[i] >= t0);
+    if (!__syncthreads_or(anywin)) return;
     // compact the window leaf ids (block scan of flags, several rounds)
     uint32_t nwin = 0;
     for (uint32_t base = 0; base < cnt; base += FORM_THREADS) {

@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ Ft,
                                                       const uint64_t* __restrict__ group_entries,
                                                       uint32_t* __restrict__ b, uint32_t* __restrict__ nat,
-                                                      uint32_t* err) {
+                                                      uint32_t* __restrict__ tile_first, uint32_t* err) {
     pdl_wait();
     __shared__ uint32_t s_chg[GROUP_WORDS + 1];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
     const uint64_t lim = min(t + TILE, n);
     const uint64_t v = s_entry[w];
     uint64_t x = unpack_x(v), c = unpack_c(v);
+    // the run covering the tile's first position (leaf formation's tile = TILE)
+    if (t < n) tile_first[tile0 + w] = (uint32_t)(x == t ? c : c - 1);
     while (x < lim) {
         uint64_t e;
         const uint64_t nx = cv.next(x, &e);
