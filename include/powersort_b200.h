@@ -93,9 +93,16 @@ size_t ps_workspace_size(int64_t n, int32_t dtype, const ps_config* cfg);
  * policy.py:94-175 and the merge kernels of merges.py:75-500).
  * `workspace` is device memory of >= ps_workspace_size() bytes; it also holds
  * the run profile and merge tree afterwards (see ps_result_*).
- * Synchronises `stream` before returning (stats are host values). */
+ * keys, values and workspace must be 16-byte aligned.
+ * Returns once the merge tree is built (stats are host values); the merges
+ * stay queued on `stream` like any kernel work.  ps_check() synchronizes and
+ * reports merge-phase device invariants. */
 int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_config* cfg, void* workspace,
             size_t workspace_bytes, ps_stats* stats, void* stream);
+
+/* Synchronizes `stream` and returns PS_EINVARIANT if the last ps_sort on
+ * `workspace` raised a device invariant flag during its merges. */
+int ps_check(void* workspace, void* stream);
 
 /* Number of runs r and merge nodes of the last ps_sort / ps_tree_from_profile
  * that used `workspace`. */

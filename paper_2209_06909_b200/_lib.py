@@ -24,6 +24,7 @@ VALUES_PERMUTE, VALUES_ARGSORT = 0, 1
 EXPORTS = (
     "ps_workspace_size",
     "ps_sort",
+    "ps_check",
     "ps_result_counts",
     "ps_result_runs",
     "ps_result_trace",
@@ -102,6 +103,7 @@ def load():
     lib.ps_workspace_size.argtypes = [i64, i32, ctypes.POINTER(PsConfig)]
     lib.ps_workspace_size.restype = sz
     lib.ps_sort.argtypes = [i32, vp, vp, i64, ctypes.POINTER(PsConfig), vp, sz, ctypes.POINTER(PsStats), vp]
+    lib.ps_check.argtypes = [vp, vp]
     lib.ps_sort.restype = ctypes.c_int
     lib.ps_result_counts.argtypes = [vp, i64p, i64p]
     lib.ps_result_counts.restype = ctypes.c_int

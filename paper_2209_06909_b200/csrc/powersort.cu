@@ -656,7 +656,14 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         prof.end(ph);
     }
 
+    {
+        int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
+        if (rc) return rc;
+    }
+
     // ---- N3/N4: merges, stage by stage ------------------------------------------
+    // enqueued without a final synchronization: the counters are known from the
+    // tree; merge-phase invariant flags are read by ps_check()
     if (nnodes) {
         MergeRunner<K> mr;
         int rc = mr.init(bufs, (uint64_t)n, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts),
@@ -683,16 +690,10 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             if (rc) return rc;
         }
     }
-    {
-        int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
-        if (rc) return rc;
-        rc = publish(sum, SUM_STATS, &h, nullptr, 0, nullptr, s);
-        if (rc) return rc;
-    }
-    if (h.err) return fail(PS_EINVARIANT, "merge invariant violated (flags " + std::to_string(h.err) + ")");
-    prof.finish();
+    prof.finish();  // synchronizes only while profiling
 
-    // ---- N5: SortStats (statskit.py:75-98) ----------------------------------------
+    // ---- N5: SortStats (statskit.py:75-98), from the tree summary ----------------
+    h = info.s;
     memset(st, 0, sizeof(*st));
     const int64_t M = (int64_t)h.merge_cost;
     st->merge_cost = M;
@@ -708,6 +709,21 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     st->moves = -1;
     st->comparisons_valid = 0;
     st->moves_valid = 0;
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Synchronizes `stream` and reports the device invariant flags of the last
+// ps_sort on `workspace` (merge-phase chunk bounds, grid barriers).
+int check_impl(void* workspace, cudaStream_t s) {
+    WsHeader hd;
+    PS_CUDA(cudaStreamSynchronize(s));
+    PS_CUDA(cudaMemcpy(&hd, workspace, sizeof(hd), cudaMemcpyDeviceToHost));
+    if (hd.magic != WS_MAGIC) return fail(PS_EINVAL, "workspace holds no sort");
+    uint32_t err = 0;
+    PS_CUDA(cudaMemcpy(&err, (const uint8_t*)workspace + hd.off_sum + offsetof(Summary, err), 4,
+                       cudaMemcpyDeviceToHost));
+    if (err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(err) + ")");
     return PS_OK;
 }
 
@@ -937,6 +953,11 @@ size_t ps_workspace_size(int64_t n, int32_t dtype, const ps_config* cfg) {
     return (size_t)make_layout((uint64_t)n, kb, (uint64_t)cfg->min_run_len, true).total;
 }
 
+int ps_check(void* workspace, void* stream) {
+    if (!workspace) return fail(PS_EINVAL, "NULL pointer argument");
+    return check_impl(workspace, (cudaStream_t)stream);
+}
+
 int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_config* cfg, void* workspace,
             size_t workspace_bytes, ps_stats* stats, void* stream) {
     int rc = validate_cfg(cfg);
@@ -967,6 +988,8 @@ int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_conf
 
 static int read_header(const void* workspace, WsHeader& h) {
     if (!workspace) return fail(PS_EINVAL, "workspace is NULL");
+    // ps_sort returns with work queued on its stream, which may be any stream
+    PS_CUDA(cudaDeviceSynchronize());
     PS_CUDA(cudaMemcpy(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost));
     if (h.magic != WS_MAGIC) return fail(PS_EINVAL, "workspace holds no sort result");
     return PS_OK;

@@ -584,16 +584,41 @@ struct RecCur {
 // past its range: they land in the slack between X and Y (Y starts VT-aligned)
 // or past the unit's last output, inside the record capacity (PADN >= CAP + VT
 // - 1), and are never read.  Its extra reads stay inside shared memory too.
-template <class C, class K>
-PS_DEV void single_merge(C& c, Rec<K>* out) {
-    if (c.o >= c.oe) return;
+// Merge-path diagonal: # of A among the first c.o outputs (ties to A).  With
+// PS_SEARCH4 the first rounds probe three points at once (4-ary), halving the
+// dependent shared-memory round trips for twice the probes.
+#ifndef PS_SEARCH4
+#define PS_SEARCH4 0
+#endif
+template <class C>
+PS_DEV uint32_t diag_search(const C& c) {
     uint32_t lo = c.o > c.lb ? c.o - c.lb : 0, hi = c.o < c.la ? c.o : c.la;
+    if (PS_SEARCH4) {
+        while (hi - lo > 3) {
+            const uint32_t span = hi - lo;
+            const uint32_t q1 = lo + (span >> 2), q2 = lo + (span >> 1), q3 = lo + ((3 * span) >> 2);
+            const bool p1 = !(c.keyB(c.o - 1 - q1) < c.keyA(q1));
+            const bool p2 = !(c.keyB(c.o - 1 - q2) < c.keyA(q2));
+            const bool p3 = !(c.keyB(c.o - 1 - q3) < c.keyA(q3));
+            const uint32_t nlo = p3 ? q3 + 1 : p2 ? q2 + 1 : p1 ? q1 + 1 : lo;
+            const uint32_t nhi = p3 ? hi : p2 ? q3 : p1 ? q2 : q1;
+            lo = nlo;
+            hi = nhi;
+        }
+    }
     while (lo < hi) {
         const uint32_t m = (lo + hi) >> 1;
         const bool le = !(c.keyB(c.o - 1 - m) < c.keyA(m));
         lo = le ? m + 1 : lo;
         hi = le ? hi : m;
     }
+    return lo;
+}
+
+template <class C, class K>
+PS_DEV void single_merge(C& c, Rec<K>* out) {
+    if (c.o >= c.oe) return;
+    const uint32_t lo = diag_search(c);
     c.i = lo;
     c.j = c.o - lo;
     c.heads();
@@ -606,13 +631,7 @@ PS_DEV void single_merge(C& c, Rec<K>* out) {
 template <class K>
 PS_DEV void single_merge_soa(RecCur<K>& c, K* outk, int32_t* outv) {
     if (c.o >= c.oe) return;
-    uint32_t lo = c.o > c.lb ? c.o - c.lb : 0, hi = c.o < c.la ? c.o : c.la;
-    while (lo < hi) {
-        const uint32_t m = (lo + hi) >> 1;
-        const bool le = !(c.keyB(c.o - 1 - m) < c.keyA(m));
-        lo = le ? m + 1 : lo;
-        hi = le ? hi : m;
-    }
+    const uint32_t lo = diag_search(c);
     c.i = lo;
     c.j = c.o - lo;
     c.heads();

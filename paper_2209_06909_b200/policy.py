@@ -100,17 +100,41 @@ class _Workspace:
 
     def __init__(self):
         self.buf = {}
+        self.stream = {}
 
     def get(self, device, nbytes):
+        """The device's workspace for use on its current stream.  A sort returns
+        with its merges still queued, so a switch of streams first orders the
+        new stream after the last one, and a grown buffer replaces the old one
+        only once the old one's work is done."""
         torch = _torch()
         cur = self.buf.get(device)
+        stream = torch.cuda.current_stream(device)
+        last = self.stream.get(device)
+        if last is not None and last != stream:
+            stream.wait_stream(last)
         if cur is None or cur.numel() < nbytes:
+            if last is not None:
+                last.synchronize()
             cur = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
             self.buf[device] = cur
+        self.stream[device] = stream
         return cur
 
 
 _WS = _Workspace()
+
+
+def check(device=None):
+    """Waits for the last sort on ``device`` (its merges run asynchronously)
+    and raises if a device invariant was violated during them (ps_check)."""
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws = _WS.buf.get(dev)
+    if ws is None:
+        return
+    lib = _lib.load()
+    _lib.check(lib.ps_check(ws.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
 
 
 def _cfg_struct(config, values_mode):

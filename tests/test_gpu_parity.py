@@ -31,8 +31,11 @@ def dev():
 
 
 def gpu_sort(keys_np, dev, **cfg):
+    from paper_2209_06909_b200.policy import check
+
     keys = torch.from_numpy(np.ascontiguousarray(keys_np)).to(dev)
     out, perm, stats = stable_argsort(keys, SortConfig(**cfg))
+    check(dev)  # merge-phase device invariants
     torch.cuda.synchronize()
     return out.cpu().numpy(), perm.cpu().numpy(), stats
 
