@@ -288,6 +288,28 @@ T* at(uint8_t* ws, uint64_t off) {
 
 inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)std::max<uint64_t>(1, cdiv(n, t)); }
 
+// End of the tree phase: one publish of the summary and the stage chunk
+// offsets (the host schedules the merges from them), then the chunk map.
+int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s) {
+    Summary* sum = at<Summary>(ws, L.sum);
+    {
+        int rc = publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
+                         info.stage_chunk, s);
+        if (rc) return rc;
+    }
+    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
+    if (nnodes && info.total_chunks() > 0) {
+        const uint32_t total = info.total_chunks();
+        if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
+        launch_k(tree_chunk_map_kernel, grid_for(total, 256), 256, 0, s, (const Node*)at<Node>(ws, L.nodes), nnodes,
+                 total, at<uint32_t>(ws, L.chunk2node));
+        PS_LAUNCH_CHECK();
+    }
+    if (info.s.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
+    if (info.s.err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(info.s.err) + ")");
+    return PS_OK;
+}
+
 // Builds the merge tree of the run boundaries b[0..r] (device, already in
 // place) for an array of n elements.  Leaves leaf parities when leafpar != 0.
 int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int strict, int slack_mode,
@@ -297,8 +319,57 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     const uint32_t* b = at<uint32_t>(ws, L.b);
     uint8_t* P = at<uint8_t>(ws, L.P);
     const uint32_t log2k = k == 4 ? 2 : 1;
-    // T1 powers (array over 0..padded)
     const uint32_t padded = (uint32_t)L.lev_size[0];
+    static const bool no_small_tree = getenv("PS_NO_SMALL_TREE") != nullptr;  // A/B: multi-kernel path
+    if (r <= TREE_SMALL_R && !no_small_tree) {
+        // the whole build in one CTA (tree_small_kernel), then one publish
+        TreeSmallArgs a;
+        memset(&a, 0, sizeof(a));
+        a.b = b;
+        a.r = r;
+        a.n = n;
+        a.log2k = log2k;
+        a.k = (uint32_t)k;
+        a.strict = strict;
+        a.slack_mode = slack_mode;
+        a.cap = cap;
+        a.stack_cap = (uint32_t)ps_run_stack_capacity(k, (int64_t)n);
+        a.P = P;
+        a.padded = padded;
+        a.mt.lev[0] = P;
+        uint32_t nlev = 1;
+        uint64_t size = align_up((uint64_t)r + 1, 32);
+        while (size > 32 && nlev < L.nlev) {
+            const uint64_t groups = size / 32;
+            const uint64_t outp = align_up(groups, 32);
+            a.mt.lev[nlev] = at<uint8_t>(ws, L.minlev[nlev]);
+            a.lev_groups[nlev] = (uint32_t)groups;
+            a.lev_padded[nlev] = (uint32_t)outp;
+            nlev++;
+            size = outp;
+        }
+        a.mt.nlev = nlev;
+        a.Rle = at<uint32_t>(ws, L.Rle);
+        a.Lle = at<uint32_t>(ws, L.Lle);
+        a.Dd = at<int32_t>(ws, L.Dd);
+        a.Sd = at<int32_t>(ws, L.Sd);
+        a.nblocks = (uint32_t)std::max<uint64_t>(1, cdiv(r > 1 ? r - 1 : 1, CLS_THREADS));
+        a.hist = at<uint32_t>(ws, L.hist);
+        a.hoff = at<uint32_t>(ws, L.hist_off);
+        a.htot = at<uint32_t>(ws, L.hist_tot);
+        a.spine = at<uint32_t>(ws, L.spine);
+        a.nodes = at<Node>(ws, L.nodes);
+        a.leafpar = leafpar;
+        a.nmax = r + MAX_SPINE;
+        a.nch = at<uint32_t>(ws, L.nch);
+        a.cb = at<uint32_t>(ws, L.chunk_base);
+        a.stage_chunk = at<uint32_t>(ws, L.stage_chunk);
+        a.sum = sum;
+        PS_CUDA(launch_k(tree_small_kernel, 1, CLS_THREADS, 0, s, a));
+        launch_counter()++;
+        return finish_tree(ws, L, info, s);
+    }
+    // T1 powers (array over 0..padded)
     launch_k(tree_powers_kernel, grid_for(padded, 256), 256, 0, s, b, r, n, log2k, P, padded, err);
     PS_LAUNCH_CHECK();
     // T2 min tree
@@ -373,22 +444,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_LAUNCH_CHECK();
     launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, (const Summary*)sum, nmax, at<uint32_t>(ws, L.stage_chunk));
     PS_LAUNCH_CHECK();
-    {
-        int rc = publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
-                         info.stage_chunk, s);
-        if (rc) return rc;
-    }
-    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
-    if (nnodes && info.total_chunks() > 0) {
-        const uint32_t total = info.total_chunks();
-        if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
-        launch_k(tree_chunk_map_kernel, grid_for(total, 256), 256, 0, s, nodes, nnodes, total,
-                                                                   at<uint32_t>(ws, L.chunk2node));
-        PS_LAUNCH_CHECK();
-    }
-    if (info.s.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
-    if (info.s.err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(info.s.err) + ")");
-    return PS_OK;
+    return finish_tree(ws, L, info, s);
 }
 
 // Runs one batch of disjoint merge nodes [nlo, nhi) whose chunks are

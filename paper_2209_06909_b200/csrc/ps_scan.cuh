@@ -169,6 +169,47 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_seq_kernel(const T* in, T* 
     if (total_out && threadIdx.x == 0) *total_out = carry;
 }
 
+// Whole-CTA scan (any blockDim <= 1024) for fused single-CTA kernels: tiles of
+// blockDim * ITEMS items with a running carry.  items: blockDim * ITEMS
+// elements of shared memory, sw: 32.  Ends with a CTA barrier.
+template <class T, class Op, int ITEMS>
+PS_DEV void cta_scan(const T* in, T* out, int64_t n, bool reverse, bool exclusive, T* total_out, T* items, T* sw) {
+    Op op;
+    T carry = Op::id();
+    const int TB = (int)blockDim.x * ITEMS;
+    for (int64_t base = 0; base < n; base += TB) {
+        for (int i = threadIdx.x; i < TB; i += blockDim.x) {
+            const int64_t g = base + i;
+            items[i] = g < n ? in[reverse ? n - 1 - g : g] : Op::id();
+        }
+        __syncthreads();
+        T loc[ITEMS];
+        T acc = Op::id();
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            loc[j] = items[threadIdx.x * ITEMS + j];
+            acc = op(acc, loc[j]);
+        }
+        T total;
+        T pre = op(carry, block_exclusive<T, Op>(acc, total, sw));
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const T inc = op(pre, loc[j]);
+            items[threadIdx.x * ITEMS + j] = exclusive ? pre : inc;
+            pre = inc;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < TB; i += blockDim.x) {
+            const int64_t g = base + i;
+            if (g < n) out[reverse ? n - 1 - g : g] = items[i];
+        }
+        carry = op(carry, total);
+        __syncthreads();
+    }
+    if (total_out && threadIdx.x == 0) *total_out = carry;
+    __syncthreads();
+}
+
 // Elements of temporary storage device_scan needs for n items.
 inline int64_t scan_tmp_elems(int64_t n) {
     int64_t t = 0;

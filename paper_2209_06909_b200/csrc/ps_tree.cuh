@@ -14,16 +14,14 @@
 #pragma once
 
 #include "ps_common.cuh"
+#include "ps_scan.cuh"
 
 namespace ps {
 
 // ---------------------------------------------------------------------------
 // T1: powers.  P[j] for j in [0, padded): P[0] = P[r] = 0, j > r -> 0xFF.
-__global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
-                                   uint8_t* __restrict__ P, uint32_t padded, uint32_t* err) {
-    pdl_wait();
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= padded) return;
+PS_DEV void tree_power_one(uint32_t j, const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
+                           uint8_t* __restrict__ P, uint32_t* err) {
     uint32_t v;
     if (j == 0 || j == r) {
         v = 0;
@@ -45,13 +43,16 @@ __global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, u
     }
     P[j] = (uint8_t)v;
 }
+__global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
+                                   uint8_t* __restrict__ P, uint32_t padded, uint32_t* err) {
+    pdl_wait();
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < padded) tree_power_one(j, b, r, n, log2k, P, err);
+}
 
 // T2: one level of the 32-ary min tree (bytes).
-__global__ void tree_minlevel_kernel(const uint8_t* __restrict__ in, uint32_t in_groups, uint8_t* __restrict__ out,
-                                     uint32_t out_padded) {
-    pdl_wait();
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= out_padded) return;
+PS_DEV void tree_minlevel_one(uint32_t i, const uint8_t* __restrict__ in, uint32_t in_groups,
+                              uint8_t* __restrict__ out) {
     uint32_t v = 0xFF;
     if (i < in_groups) {
         const uint4* p = reinterpret_cast<const uint4*>(in + (uint64_t)i * 32);
@@ -63,6 +64,12 @@ __global__ void tree_minlevel_kernel(const uint8_t* __restrict__ in, uint32_t in
         v = m & 0xFF;
     }
     out[i] = (uint8_t)v;
+}
+__global__ void tree_minlevel_kernel(const uint8_t* __restrict__ in, uint32_t in_groups, uint8_t* __restrict__ out,
+                                     uint32_t out_padded) {
+    pdl_wait();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < out_padded) tree_minlevel_one(i, in, in_groups, out);
 }
 
 struct MinTree {
@@ -203,18 +210,20 @@ constexpr uint32_t CLS_THREADS = 1024;
 // T3b (PASS 0): per-block / per-warp histogram of head powers, spine list,
 // depth and stack-height difference arrays.  (PASS 1): stable scatter of the
 // main-loop nodes into per-power buckets (ascending power, position order).
+// One block of CLS_THREADS boundaries (vb: the block's index); all threads of
+// a CLS_THREADS-thread CTA call it.
 template <int PASS>
-__global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
-    const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle, const uint32_t* __restrict__ Lle,
-    const uint32_t* __restrict__ b, uint32_t r, uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
-    const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff, int32_t* __restrict__ Sdiff,
-    uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum) {
-    pdl_wait();
+PS_DEV void tree_classify_block(uint32_t vb, const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle,
+                                const uint32_t* __restrict__ Lle, const uint32_t* __restrict__ b, uint32_t r,
+                                uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
+                                const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff,
+                                int32_t* __restrict__ Sdiff, uint32_t* __restrict__ spine_list,
+                                Node* __restrict__ nodes, Summary* sum) {
     __shared__ uint32_t whist[32][NPOW];
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     for (uint32_t i = tid; i < 32 * NPOW; i += blockDim.x) (&whist[0][0])[i] = 0;
     __syncthreads();
-    const uint32_t j = blockIdx.x * CLS_THREADS + tid + 1;
+    const uint32_t j = vb * CLS_THREADS + tid + 1;
     const bool valid = j < r;
     BoundaryClass c;
     c.head = false;
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
             whist[w][tid] = acc;
             acc += x;
         }
-        if (PASS == 0) blockHist[(uint64_t)tid * nblocks + blockIdx.x] = acc;
+        if (PASS == 0) blockHist[(uint64_t)tid * nblocks + vb] = acc;
     }
     __syncthreads();
     if (PASS == 0) {
@@ -257,7 +266,7 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
             }
         }
     } else if (c.head) {
-        const uint32_t slot = blockOff[(uint64_t)p * nblocks + blockIdx.x] + whist[warp][p] + rank;
+        const uint32_t slot = blockOff[(uint64_t)p * nblocks + vb] + whist[warp][p] + rank;
         Node nd;
         const uint32_t arity = c.nmem + 1;
         for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = i <= arity ? b[c.bidx[i]] : 0u;
@@ -271,13 +280,24 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
         nd.order = c.bidx[1 + c.nmem];  // R's boundary index
         nodes[slot] = nd;
     }
+    __syncthreads();  // whist is reused by the next call
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
+    const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle, const uint32_t* __restrict__ Lle,
+    const uint32_t* __restrict__ b, uint32_t r, uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
+    const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff, int32_t* __restrict__ Sdiff,
+    uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum) {
+    pdl_wait();
+    tree_classify_block<PASS>(blockIdx.x, P, Rle, Lle, b, r, k, nblocks, blockHist, blockOff, Ddiff, Sdiff, spine_list,
+                              nodes, sum);
 }
 
 // T4: the spine and _merge_down (policy.py:146-175): staged by the CTA, replayed by one thread.
-__global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
-                                  uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
-                                  int32_t* __restrict__ Ddiff, Summary* sum) {
-    pdl_wait();
+PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
+                           uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, int32_t* __restrict__ Ddiff,
+                           Summary* sum) {
     // the stack entries are staged and sorted by the CTA, their run starts are
     // gathered in parallel; one thread then replays _merge_down from shared memory
     __shared__ uint32_t s_list[MAX_SPINE];
@@ -363,6 +383,12 @@ __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, ui
     }
     sum->nspine_nodes = nn;
 }
+__global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
+                                  uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
+                                  int32_t* __restrict__ Ddiff, Summary* sum) {
+    pdl_wait();
+    tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum);
+}
 
 // T5: per-node depth/parity, chunk counts and merge statistics; leaf parity.
 // slack_mode: 0 -> slack = arity ("4way"/"2way" sentinel kernels),
@@ -373,11 +399,10 @@ PS_DEV uint32_t node_count(const Summary* sum, uint32_t nmax) {
     return c < nmax ? c : nmax;
 }
 
-__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                           int slack_mode, uint32_t cap, Summary* sum) {
-    pdl_wait();
+PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
+                                int slack_mode, uint32_t cap, Summary* sum) {
     const uint32_t nnodes = node_count(sum, nmax);
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = i0 + threadIdx.x;
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
     if (i < nnodes) {
         Node nd = nodes[i];
@@ -454,14 +479,19 @@ __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nm
             atomicAdd(dst, t);
         }
     }
+    __syncthreads();  // s_red is reused by the next call
+}
+__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
+                                           int slack_mode, uint32_t cap, Summary* sum) {
+    pdl_wait();
+    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum);
 }
 
 // chunk_base at the node indices the host schedules stages by: level offsets
 // (out[0..NPOW]), spine nodes (out[NPOW+1+i], i <= nspine_nodes) and the total
 // (out[NPOW+2+MAX_SPINE]); cb has nnodes+1 entries.
-__global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum,
-                                         uint32_t nmax, uint32_t* __restrict__ out) {
-    pdl_wait();
+PS_DEV void tree_stage_chunks_cta(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum, uint32_t nmax,
+                                   uint32_t* __restrict__ out) {
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t t = threadIdx.x;
     if (t <= NPOW) {
@@ -473,6 +503,11 @@ __global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const 
         out[NPOW + 1 + i] = cb[j < nnodes ? j : nnodes];
     }
     if (t == 0) out[NPOW + 2 + MAX_SPINE] = cb[nnodes];
+}
+__global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum,
+                                         uint32_t nmax, uint32_t* __restrict__ out) {
+    pdl_wait();
+    tree_stage_chunks_cta(cb, sum, nmax, out);
 }
 
 __global__ void tree_leaf_parity_kernel(const int32_t* __restrict__ S, uint32_t r, uint8_t* __restrict__ leafpar) {
@@ -496,15 +531,19 @@ __global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r,
 }
 
 // level offsets of the power buckets from the scanned block histograms
-__global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
-                                          uint32_t nblocks, Summary* sum) {
-    pdl_wait();
+PS_DEV void tree_level_offsets_cta(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
+                                   uint32_t nblocks, Summary* sum) {
     const uint32_t p = threadIdx.x;
     if (p < NPOW) sum->level_off[p] = blockOff[(uint64_t)p * nblocks];
     if (p == 0) {
         sum->level_off[NPOW] = *total;
         sum->nmain = *total;
     }
+}
+__global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
+                                          uint32_t nblocks, Summary* sum) {
+    pdl_wait();
+    tree_level_offsets_cta(blockOff, total, nblocks, sum);
 }
 
 __global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ base,
@@ -537,6 +576,113 @@ __global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, uint32_t n
             hi = mid;
     }
     chunk2node[c] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// The whole tree build (T1-T5) for r <= TREE_SMALL_R boundaries in ONE CTA of
+// CLS_THREADS threads: the phases of the multi-kernel path back to back with
+// CTA barriers instead of ~20 dependent launches.
+constexpr uint32_t TREE_SMALL_R = 1024;  // measured: wins at r = 491, loses at r = 4059
+
+struct TreeSmallArgs {
+    const uint32_t* b;
+    uint32_t r;
+    uint64_t n;
+    uint32_t log2k, k;
+    int strict, slack_mode;
+    uint32_t cap, stack_cap;
+    uint8_t* P;
+    uint32_t padded;
+    MinTree mt;
+    uint32_t lev_groups[8], lev_padded[8];  // level l >= 1: input groups, padded size
+    uint32_t* Rle;
+    uint32_t* Lle;
+    int32_t* Dd;
+    int32_t* Sd;
+    uint32_t nblocks;
+    uint32_t* hist;
+    uint32_t* hoff;
+    uint32_t* htot;
+    uint32_t* spine;
+    Node* nodes;
+    uint8_t* leafpar;  // nullable
+    uint32_t nmax;
+    uint32_t* nch;
+    uint32_t* cb;
+    uint32_t* stage_chunk;
+    Summary* sum;
+};
+
+__global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a) {
+    pdl_wait();
+    __shared__ uint32_t s_items[CLS_THREADS * 4];
+    __shared__ uint32_t s_sw[32];
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint32_t* err = &a.sum->err;
+    for (uint32_t i = tid; i < a.r + 2; i += nt) {
+        a.Dd[i] = 0;
+        a.Sd[i] = 0;
+    }
+    for (uint32_t j = tid; j < a.padded; j += nt) tree_power_one(j, a.b, a.r, a.n, a.log2k, a.P, err);
+    __syncthreads();
+    for (uint32_t l = 1; l < a.mt.nlev; ++l) {
+        uint8_t* out = const_cast<uint8_t*>(a.mt.lev[l]);
+        for (uint32_t i = tid; i < a.lev_padded[l]; i += nt) tree_minlevel_one(i, a.mt.lev[l - 1], a.lev_groups[l], out);
+        __syncthreads();
+    }
+    for (uint32_t j = tid + 1; j < a.r; j += nt) {
+        const uint32_t v = a.P[j];
+        a.Rle[j] = find_right_le(a.mt, j, v);
+        a.Lle[j] = find_left_le(a.mt, j, v);
+    }
+    __syncthreads();
+    for (uint32_t vb = 0; vb < a.nblocks; ++vb)
+        tree_classify_block<0>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, a.hist, nullptr, a.Dd, a.Sd, a.spine,
+                               a.nodes, a.sum);
+    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.hist, a.hoff, (int64_t)NPOW * a.nblocks, false, true, a.htot, s_items,
+                                           s_sw);
+    tree_level_offsets_cta(a.hoff, a.htot, a.nblocks, a.sum);
+    __syncthreads();
+    for (uint32_t vb = 0; vb < a.nblocks; ++vb)
+        tree_classify_block<1>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, nullptr, a.hoff, a.Dd, a.Sd, a.spine,
+                               a.nodes, a.sum);
+    tree_spine_cta(a.b, a.r, a.k, a.strict, a.spine, a.nodes, a.Dd, a.sum);
+    __syncthreads();
+    cta_scan<int32_t, OpSum<int32_t>, 4>(a.Dd, a.Dd, (int64_t)a.r + 1, false, false, nullptr,
+                                         reinterpret_cast<int32_t*>(s_items), reinterpret_cast<int32_t*>(s_sw));
+    cta_scan<int32_t, OpSum<int32_t>, 4>(a.Sd, a.Sd, (int64_t)a.r + 1, false, false, nullptr,
+                                         reinterpret_cast<int32_t*>(s_items), reinterpret_cast<int32_t*>(s_sw));
+    for (uint32_t j0 = 0; j0 < a.r; j0 += nt) {  // max stack height
+        const uint32_t j = j0 + tid + 1;
+        int32_t v = j < a.r ? a.Sd[j] : 0;
+        for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
+        if (lane_id() == 0 && v > 0) {
+            atomicMax(&a.sum->max_stack, (uint32_t)v);
+            if ((uint32_t)v > a.stack_cap) atomicOr(err, ERR_STACK);
+        }
+    }
+    if (a.leafpar) {
+        for (uint32_t j = tid; j < a.r; j += nt) {
+            const int32_t x = j == 0 ? 0 : a.Dd[j];
+            const int32_t y = j + 1 >= a.r ? 0 : a.Dd[j + 1];
+            a.leafpar[j] = (uint8_t)((x > y ? x : y) & 1);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
+        tree_finalize_block(i0, a.nodes, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum);
+    {
+        const uint32_t nn = node_count(a.sum, a.nmax);
+        for (uint32_t i = tid; i < a.nmax; i += nt) a.nch[i] = i < nn ? a.nodes[i].nchunks : 0u;
+    }
+    __syncthreads();
+    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.nch, a.cb, a.nmax, false, true, a.cb + a.nmax, s_items, s_sw);
+    {
+        const uint32_t nn = node_count(a.sum, a.nmax);
+        for (uint32_t i = tid; i < nn; i += nt) a.nodes[i].chunk_base = a.cb[i];
+    }
+    __syncthreads();
+    tree_stage_chunks_cta(a.cb, a.sum, a.nmax, a.stage_chunk);
 }
 
 }  // namespace ps
