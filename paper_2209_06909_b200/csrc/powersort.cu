@@ -369,37 +369,44 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
         launch_counter()++;
         return finish_tree(ws, L, info, s);
     }
-    // T1 powers (array over 0..padded)
-    launch_k(tree_powers_kernel, grid_for(padded, 256), 256, 0, s, b, r, n, log2k, P, padded, err);
-    PS_LAUNCH_CHECK();
-    // T2 min tree
+    // T1 powers (array over 0..padded) with min-tree level 1, T2 the other levels
+    int32_t* Dd = at<int32_t>(ws, L.Dd);
+    int32_t* Sd = at<int32_t>(ws, L.Sd);
     MinTree mt;
     memset(&mt, 0, sizeof(mt));
     mt.lev[0] = P;
     uint32_t nlev = 1;
+    uint32_t lev_groups[8] = {0}, lev_padded[8] = {0};
     {
         uint64_t size = align_up((uint64_t)r + 1, 32);
         while (size > 32 && nlev < L.nlev) {
             const uint64_t groups = size / 32;
             const uint64_t outp = align_up(groups, 32);
-            uint8_t* out = at<uint8_t>(ws, L.minlev[nlev]);
-            launch_k(tree_minlevel_kernel, grid_for(outp, 256), 256, 0, s, mt.lev[nlev - 1], (uint32_t)groups, out,
-                                                                     (uint32_t)outp);
-            PS_LAUNCH_CHECK();
-            mt.lev[nlev++] = out;
+            lev_groups[nlev] = (uint32_t)groups;
+            lev_padded[nlev] = (uint32_t)outp;
+            mt.lev[nlev] = at<uint8_t>(ws, L.minlev[nlev]);
+            nlev++;
             size = outp;
         }
     }
     mt.nlev = nlev;
+    {
+        uint8_t* lev1 = nlev > 1 ? const_cast<uint8_t*>(mt.lev[1]) : nullptr;
+        const uint64_t nthr = std::max<uint64_t>({padded, (uint64_t)lev_padded[1] * 32, (uint64_t)r + 2});
+        launch_k(tree_powers_kernel, grid_for(nthr, 256), 256, 0, s, b, r, n, log2k, P, padded, err, Dd, Sd, lev1,
+                 lev_padded[1]);
+        PS_LAUNCH_CHECK();
+    }
+    for (uint32_t l = 2; l < nlev; ++l) {
+        launch_k(tree_minlevel_kernel, grid_for(lev_padded[l], 256), 256, 0, s, mt.lev[l - 1], lev_groups[l],
+                 const_cast<uint8_t*>(mt.lev[l]), lev_padded[l]);
+        PS_LAUNCH_CHECK();
+    }
     uint32_t* Rle = at<uint32_t>(ws, L.Rle);
     uint32_t* Lle = at<uint32_t>(ws, L.Lle);
     launch_k(tree_nearest_kernel, grid_for(r, 256), 256, 0, s, mt, P, r, Rle, Lle);
     PS_LAUNCH_CHECK();
     // T3 classify
-    int32_t* Dd = at<int32_t>(ws, L.Dd);
-    int32_t* Sd = at<int32_t>(ws, L.Sd);
-    PS_CUDA(cudaMemsetAsync(Dd, 0, ((uint64_t)r + 2) * 4, s));
-    PS_CUDA(cudaMemsetAsync(Sd, 0, ((uint64_t)r + 2) * 4, s));
     const uint32_t nblocks = (uint32_t)std::max<uint64_t>(1, cdiv(r > 1 ? r - 1 : 1, CLS_THREADS));
     uint32_t* hist = at<uint32_t>(ws, L.hist);
     uint32_t* hoff = at<uint32_t>(ws, L.hist_off);
@@ -419,30 +426,21 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
-    PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Dd, Dd, (int64_t)r + 1, false, false,
-                                                 at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
-    PS_CUDA((device_scan<int32_t, OpSum<int32_t>>(Sd, Sd, (int64_t)r + 1, false, false,
-                                                 at<int32_t>(ws, L.scantmp_i32), nullptr, s)));
+    PS_CUDA((device_scan2<int32_t, OpSum<int32_t>>(Dd, Dd, Sd, Sd, (int64_t)r + 1, false, false,
+                                                  at<int32_t>(ws, L.scantmp_i32), s)));
     // node-indexed kernels run over the bound nmax and read the node count on the device
     const uint32_t nmax = r + MAX_SPINE;
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
-    launch_k(tree_stack_max_kernel, grid_for(r, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap);
-    PS_LAUNCH_CHECK();
-    if (leafpar) {
-        launch_k(tree_leaf_parity_kernel, grid_for(r, 256), 256, 0, s, Dd, r, leafpar);
-        PS_LAUNCH_CHECK();
-    }
-    launch_k(tree_nodes_finalize_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, Dd, slack_mode, cap, sum);
+    launch_k(tree_stack_max_kernel, grid_for(r + 1, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap, Dd, leafpar);
     PS_LAUNCH_CHECK();
     uint32_t* nch = at<uint32_t>(ws, L.nch);
     uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
-    launch_k(tree_nchunks_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, (const Summary*)sum, nch);
+    launch_k(tree_nodes_finalize_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, nch);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nmax, false, true, at<uint32_t>(ws, L.scantmp_u32),
                                                    cb + nmax, s)));
-    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, nodes, cb, nmax, (const Summary*)sum);
-    PS_LAUNCH_CHECK();
-    launch_k(tree_stage_chunks_kernel, 1, 128, 0, s, cb, (const Summary*)sum, nmax, at<uint32_t>(ws, L.stage_chunk));
+    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, nodes, cb, nmax, (const Summary*)sum,
+             at<uint32_t>(ws, L.stage_chunk));
     PS_LAUNCH_CHECK();
     return finish_tree(ws, L, info, s);
 }

@@ -131,8 +131,13 @@ constexpr int64_t SCAN_SEQ_MAX = 8 * SCAN_BLK;
 
 template <class T, class Op>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_seq_kernel(const T* in, T* out, int64_t n, int reverse,
-                                                                int exclusive, T* total_out) {
+                                                                int exclusive, T* total_out, const T* in2, T* out2) {
     pdl_wait();
+    if (blockIdx.x == 1) {  // a second, independent array of the same length (one launch for both)
+        in = in2;
+        out = out2;
+        total_out = nullptr;
+    }
     __shared__ T items[SCAN_BLK];
     __shared__ T sw[32];
     Op op;
@@ -210,6 +215,12 @@ PS_DEV void cta_scan(const T* in, T* out, int64_t n, bool reverse, bool exclusiv
     __syncthreads();
 }
 
+// Two independent arrays of n items each, scanned the same way; one launch when
+// small.  tmp as for device_scan.
+template <class T, class Op>
+cudaError_t device_scan2(const T* in, T* out, const T* in2, T* out2, int64_t n, bool reverse, bool exclusive, T* tmp,
+                         cudaStream_t s);
+
 // Elements of temporary storage device_scan needs for n items.
 inline int64_t scan_tmp_elems(int64_t n) {
     int64_t t = 0;
@@ -228,7 +239,8 @@ cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclu
     if (n <= 0) return cudaSuccess;
     int64_t nb = (n + SCAN_BLK - 1) / SCAN_BLK;
     if (n <= SCAN_SEQ_MAX) {
-        launch_k(scan_seq_kernel<T, Op>, 1, SCAN_THREADS, 0, s, in, out, n, (int)reverse, (int)exclusive, total_out);
+        launch_k(scan_seq_kernel<T, Op>, 1, SCAN_THREADS, 0, s, in, out, n, (int)reverse, (int)exclusive, total_out,
+                 (const T*)nullptr, (T*)nullptr);
         launch_counter()++;
         return cudaGetLastError();
     }
@@ -241,6 +253,21 @@ cudaError_t device_scan(const T* in, T* out, int64_t n, bool reverse, bool exclu
     launch_k(scan_apply_kernel<T, Op>, (unsigned)nb, SCAN_THREADS, 0, s, in, out, n, partial, reverse, exclusive,
                                                                     total_out);
     return cudaGetLastError();
+}
+
+template <class T, class Op>
+cudaError_t device_scan2(const T* in, T* out, const T* in2, T* out2, int64_t n, bool reverse, bool exclusive, T* tmp,
+                         cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (n <= SCAN_SEQ_MAX) {
+        launch_k(scan_seq_kernel<T, Op>, 2, SCAN_THREADS, 0, s, in, out, n, (int)reverse, (int)exclusive, (T*)nullptr,
+                 in2, out2);
+        launch_counter()++;
+        return cudaGetLastError();
+    }
+    cudaError_t e = device_scan<T, Op>(in, out, n, reverse, exclusive, tmp, nullptr, s);
+    if (e != cudaSuccess) return e;
+    return device_scan<T, Op>(in2, out2, n, reverse, exclusive, tmp, nullptr, s);
 }
 
 }  // namespace ps

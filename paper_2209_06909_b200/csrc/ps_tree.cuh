@@ -43,11 +43,26 @@ PS_DEV void tree_power_one(uint32_t j, const uint32_t* __restrict__ b, uint32_t 
     }
     P[j] = (uint8_t)v;
 }
+// grid over nthreads >= max(padded, 32 * lev1_padded, r + 2): also zeroes the
+// depth / stack-height difference arrays and writes min-tree level 1 (warp minima)
 __global__ void tree_powers_kernel(const uint32_t* __restrict__ b, uint32_t r, uint64_t n, uint32_t log2k,
-                                   uint8_t* __restrict__ P, uint32_t padded, uint32_t* err) {
+                                   uint8_t* __restrict__ P, uint32_t padded, uint32_t* err, int32_t* __restrict__ Dd,
+                                   int32_t* __restrict__ Sd, uint8_t* __restrict__ lev1, uint32_t lev1_padded) {
     pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < padded) tree_power_one(j, b, r, n, log2k, P, err);
+    if (j < r + 2) {
+        Dd[j] = 0;
+        Sd[j] = 0;
+    }
+    uint32_t v = 0xFF;
+    if (j < padded) {
+        tree_power_one(j, b, r, n, log2k, P, err);
+        v = P[j];
+    }
+    if (lev1) {
+        for (int d = 16; d; d >>= 1) v = min(v, __shfl_xor_sync(PS_FULL, v, d));
+        if (lane_id() == 0 && j / 32 < lev1_padded) lev1[j / 32] = (uint8_t)v;
+    }
 }
 
 // T2: one level of the 32-ary min tree (bytes).
@@ -400,7 +415,7 @@ PS_DEV uint32_t node_count(const Summary* sum, uint32_t nmax) {
 }
 
 PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                int slack_mode, uint32_t cap, Summary* sum) {
+                                int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch_out) {
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t i = i0 + threadIdx.x;
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
@@ -417,6 +432,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         }
         nd.nchunks = nch;
         nodes[i] = nd;
+        if (nch_out) nch_out[i] = nch;
         cost = size;
         m2 = w == 2;
         m3 = w == 3;
@@ -428,6 +444,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
             sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_KERNEL_MAX;
         }
     }
+    if (nch_out && i >= nnodes && i < nmax) nch_out[i] = 0;  // scan padding
     // per-level cost / small counts: one atomic per distinct power per warp
     // (main nodes are level-sorted, so a warp mostly holds one power)
     {
@@ -482,9 +499,9 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
     __syncthreads();  // s_red is reused by the next call
 }
 __global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                           int slack_mode, uint32_t cap, Summary* sum) {
+                                           int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch) {
     pdl_wait();
-    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum);
+    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, nch);
 }
 
 // chunk_base at the node indices the host schedules stages by: level offsets
@@ -519,9 +536,18 @@ __global__ void tree_leaf_parity_kernel(const int32_t* __restrict__ S, uint32_t 
     leafpar[j] = (uint8_t)((a > c ? a : c) & 1);
 }
 
-__global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r, Summary* sum, uint32_t cap) {
+// max stack height (H = inclusive scan of the stack difference array) and, with
+// leafpar, the leaf parities from the depths S
+__global__ void tree_stack_max_kernel(const int32_t* __restrict__ H, uint32_t r, Summary* sum, uint32_t cap,
+                                      const int32_t* __restrict__ S, uint8_t* __restrict__ leafpar) {
     pdl_wait();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (leafpar && j - 1 < r) {
+        const uint32_t jl = j - 1;
+        const int32_t a = jl == 0 ? 0 : S[jl];
+        const int32_t c = jl + 1 >= r ? 0 : S[jl + 1];
+        leafpar[jl] = (uint8_t)((a > c ? a : c) & 1);
+    }
     int32_t v = (j < r) ? H[j] : 0;
     for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
     if (lane_id() == 0 && v > 0) {
@@ -546,11 +572,14 @@ __global__ void tree_level_offsets_kernel(const uint32_t* __restrict__ blockOff,
     tree_level_offsets_cta(blockOff, total, nblocks, sum);
 }
 
+// chunk_base into the nodes; block 0 also gathers the stage chunk offsets
 __global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ base,
-                                            uint32_t nmax, const Summary* __restrict__ sum) {
+                                            uint32_t nmax, const Summary* __restrict__ sum,
+                                            uint32_t* __restrict__ stage_chunk) {
     pdl_wait();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < node_count(sum, nmax)) nodes[i].chunk_base = base[i];
+    if (blockIdx.x == 0) tree_stage_chunks_cta(base, sum, nmax, stage_chunk);
 }
 
 // nchunks per node, zero for the padding up to nmax (the scan runs over nmax)
@@ -670,11 +699,7 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a
     }
     __syncthreads();
     for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
-        tree_finalize_block(i0, a.nodes, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum);
-    {
-        const uint32_t nn = node_count(a.sum, a.nmax);
-        for (uint32_t i = tid; i < a.nmax; i += nt) a.nch[i] = i < nn ? a.nodes[i].nchunks : 0u;
-    }
+        tree_finalize_block(i0, a.nodes, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum, a.nch);
     __syncthreads();
     cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.nch, a.cb, a.nmax, false, true, a.cb + a.nmax, s_items, s_sw);
     {
