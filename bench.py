@@ -111,7 +111,7 @@ def load_traffic(config, n):
 
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled through NVML every
-    2 ms on a background thread while the timed region runs (the timed
+    0.5 ms on a background thread while the timed region runs (the timed
     region is tens of milliseconds, too short for nvidia-smi's 100 ms loop)."""
 
     REASONS = (
@@ -157,7 +157,7 @@ class ClockSampler:
             except Exception as e:  # pragma: no cover
                 self.err = str(e)
                 return
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def stop(self):
         if self.thread is None:
@@ -165,7 +165,7 @@ class ClockSampler:
         self.stop_flag.set()
         self.thread.join(timeout=2)
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.smax,
-                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML, 2 ms polling"}
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML, 0.5 ms polling"}
 
 
 def cpu_oracle_baseline(keys_np, k, seconds):
