@@ -45,6 +45,7 @@ size_t form_smem_bytes(uint32_t m) {
     const size_t cap = FORM_TILE + (m < MAX_FORM_M ? m : MAX_FORM_M);
     s += cap * sizeof(K);
     s += cap * 4;
+    s += (cap * 2 + 15) / 16 * 16;  // window index of every staged element
     return s;
 }
 
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     const uint32_t cap = FORM_TILE + (m < MAX_FORM_M ? m : MAX_FORM_M);
     K* wk = reinterpret_cast<K*>(smem + off);
     int32_t* wv = reinterpret_cast<int32_t*>(wk + cap);
+    uint16_t* widx = reinterpret_cast<uint16_t*>(wv + cap);
     __shared__ uint32_t s_first, s_cnt, s_nwin, s_wtot;
     __shared__ uint32_t sw32[32];
 
@@ -131,7 +133,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     // belongs to the owner of its lower position), so the reordering is safe.
     constexpr uint32_t FORM_BATCH = 4;
     enum : uint8_t { F_NONE = 0, F_COPY = 1, F_ARGV = 2, F_SWAP = 3 };
-    if (cnt <= 16) {
+    bool anynat = false;  // tiles made only of extended windows skip this pass
+    for (uint32_t i = tid; i < cnt; i += FORM_THREADS) anynat |= !(snat[i] < sb[i + 1] - sb[i]);
+    if (!__syncthreads_or(anynat)) {
+    } else if (cnt <= 16) {
         // few (long) leaves: leaf by leaf, all threads striding over its positions
         for (uint32_t li = 0; li < cnt; ++li) {
             const uint64_t bj = sb[li], ej = sb[li + 1];
@@ -319,6 +324,7 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
             const uint64_t p = (uint64_t)sb[wlist[lo]] + (e - woff[lo]);
             kk[u] = K0[p];
             vv[u] = ARGSORT ? (int32_t)p : V0[p];
+            widx[e] = (uint16_t)lo;
         }
 #pragma unroll
         for (uint32_t u = 0; u < 4; ++u) {
@@ -331,17 +337,16 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     }
     __syncthreads();
     for (uint32_t e = tid; e < wtot; e += FORM_THREADS) {
-        uint32_t lo = 0, hi = nwin;
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (woff[mid] <= e) lo = mid; else hi = mid;
-        }
+        const uint32_t lo = widx[e];
         const uint32_t wb = woff[lo], we = woff[lo + 1];
         const K x = wk[e];
+        // stable rank in the window: earlier elements <= x, later elements < x
+        // (one loop over the whole window: the same trip count on every lane)
         uint32_t rank = 0;
+#pragma unroll 4
         for (uint32_t f = wb; f < we; ++f) {
             const K y = wk[f];
-            rank += (y < x) || (!(x < y) && f < e);
+            rank += (uint32_t)(y < x) | ((uint32_t)(f < e) & (uint32_t)!(x < y));
         }
         const uint32_t leaf = wlist[lo];
         const uint32_t par = spar[leaf];
