@@ -308,6 +308,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     }
     if (tid == 0) woff[nwin] = wtot;
     __syncthreads();
+    // window index of every staged element (a thread per window)
+    for (uint32_t i = tid; i < nwin; i += FORM_THREADS)
+        for (uint32_t e = woff[i]; e < woff[i + 1]; ++e) widx[e] = (uint16_t)i;
+    __syncthreads();
     // stage
     for (uint32_t e0 = tid; e0 < wtot; e0 += FORM_THREADS * 4) {
         K kk[4];
@@ -316,15 +320,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         for (uint32_t u = 0; u < 4; ++u) {
             const uint32_t e = e0 + u * FORM_THREADS;
             if (e >= wtot) continue;
-            uint32_t lo = 0, hi = nwin;
-            while (hi - lo > 1) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (woff[mid] <= e) lo = mid; else hi = mid;
-            }
+            const uint32_t lo = widx[e];
             const uint64_t p = (uint64_t)sb[wlist[lo]] + (e - woff[lo]);
             kk[u] = K0[p];
             vv[u] = ARGSORT ? (int32_t)p : V0[p];
-            widx[e] = (uint16_t)lo;
         }
 #pragma unroll
         for (uint32_t u = 0; u < 4; ++u) {
