@@ -66,19 +66,17 @@ PS_DEV __host__ constexpr uint32_t cut_cap() {
 constexpr uint32_t MIN_CUT_SPACING =
     (cut_cap<int32_t>() < cut_cap<int64_t>() ? cut_cap<int32_t>() : cut_cap<int64_t>()) / MAX_WAY;
 
-// # of a[0..len) that are <= x (LE) or < x (!LE)
+// # of a[0..len) that are <= x (LE) or < x (!LE): branch-free binary lifting
+// (the predicate holds on a prefix; add the largest powers of two that keep it)
 template <class K, bool LE>
 PS_DEV uint32_t count_pred(const K* __restrict__ a, uint32_t len, K x) {
     uint32_t lo = 0;
-    while (len > 0) {
-        const uint32_t half = len >> 1;
-        const K y = a[lo + half];
-        const bool p = LE ? !(x < y) : (y < x);
-        if (p) {
-            lo += half + 1;
-            len -= half + 1;
-        } else {
-            len = half;
+    for (uint32_t step = len ? (1u << (31 - __clz(len))) : 0u; step; step >>= 1) {
+        const uint32_t probe = lo + step;
+        if (probe <= len) {
+            const K y = a[probe - 1];
+            const bool p = LE ? !(x < y) : (y < x);
+            lo = p ? probe : lo;
         }
     }
     return lo;
@@ -298,13 +296,39 @@ PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(PIPE_CONSUMER
 // Small nodes (size <= SMALL_NODE): one warp per group of G consecutive nodes
 // of the batch (G * largest small node <= SMALL_NODE, chosen by the host per
 // level), packed into the warp's shared-memory window.  Loads are batched;
-// each record's output index is its index in its run plus its rank in every
-// other run of its node (<= for earlier runs, < for later: the stable order).
+// each node is then merged by the warp's lanes with merge-path passes like the
+// pipe's (4-way = merge(merge(A,B), merge(C,D)), ties to the left).
 constexpr uint32_t SMALL_WARPS = 8;
 
 template <class K>
 size_t merge_small_smem_bytes() {
-    return (size_t)SMALL_WARPS * SMALL_NODE * (2 * (sizeof(K) + 4) + 1);
+    return (size_t)SMALL_WARPS * SMALL_NODE * (3 * (sizeof(K) + 4) + 1);
+}
+
+// outputs [0, la + lb) of merge(A, B) (ties to A) into (okk, ovv), the lanes of
+// a warp taking equal consecutive slices (diagonal search, then a serial merge)
+template <class K>
+PS_DEV void warp_merge2(const K* ak, const int32_t* av, uint32_t la, const K* bk, const int32_t* bv, uint32_t lb,
+                        K* okk, int32_t* ovv) {
+    const uint32_t lane = lane_id(), tot = la + lb;
+    const uint32_t per = (tot + 31) / 32;
+    const uint32_t o0 = min(tot, lane * per), o1 = min(tot, o0 + per);
+    if (o0 >= o1) return;
+    uint32_t lo = o0 > lb ? o0 - lb : 0, hi = o0 < la ? o0 : la;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        const bool le = !(bk[o0 - 1 - m] < ak[m]);
+        lo = le ? m + 1 : lo;
+        hi = le ? hi : m;
+    }
+    uint32_t i = lo, j = o0 - lo;
+    for (uint32_t o = o0; o < o1; ++o) {
+        const bool takeA = i < la && (j >= lb || !(bk[j] < ak[i]));
+        okk[o] = takeA ? ak[i] : bk[j];
+        ovv[o] = takeA ? av[i] : bv[j];
+        i += takeA;
+        j += !takeA;
+    }
 }
 
 template <class K>
@@ -322,12 +346,14 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
     if (first64 >= nhi) return;
     const uint32_t first = (uint32_t)first64;
     const uint32_t cnt = min(G, nhi - first);
-    uint8_t* base = smem + (size_t)warp * SMALL_NODE * (2 * (sizeof(K) + 4) + 1);
+    uint8_t* base = smem + (size_t)warp * SMALL_NODE * (3 * (sizeof(K) + 4) + 1);
     K* sk = reinterpret_cast<K*>(base);
     K* ok = sk + SMALL_NODE;
-    int32_t* sv = reinterpret_cast<int32_t*>(ok + SMALL_NODE);
+    K* xk = ok + SMALL_NODE;
+    int32_t* sv = reinterpret_cast<int32_t*>(xk + SMALL_NODE);
     int32_t* ov = sv + SMALL_NODE;
-    uint8_t* snid = reinterpret_cast<uint8_t*>(ov + SMALL_NODE);
+    int32_t* xv = ov + SMALL_NODE;
+    uint8_t* snid = reinterpret_cast<uint8_t*>(xv + SMALL_NODE);
     uint32_t sz = 0;
     if (lane < cnt) {
         const Node nd = nodes[first + lane];
@@ -381,24 +407,23 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
         }
     }
     __syncwarp();
-#pragma unroll 4
-    for (uint32_t i = lane; i < total; i += 32) {
-        const uint32_t j = snid[i];
-        const uint32_t nb = pre[j], q = i - nb;
-        const uint32_t* off = s_off[warp][j];
-        const uint32_t o1 = off[1], o2 = off[2], o3 = off[3], oe = pre[j + 1] - nb;
-        const uint32_t a = (q >= o1) + (q >= o2) + (q >= o3);
-        const K x = sk[i];
-        uint32_t rank = q - (a == 0 ? 0u : a == 1 ? o1 : a == 2 ? o2 : o3);
-        const K* nk = sk + nb;
-        if (a != 0) rank += count_pred<K, true>(nk, o1, x);
-        if (a != 1) rank += a > 1 ? count_pred<K, true>(nk + o1, o2 - o1, x) : count_pred<K, false>(nk + o1, o2 - o1, x);
-        if (a != 2) rank += a > 2 ? count_pred<K, true>(nk + o2, o3 - o2, x) : count_pred<K, false>(nk + o2, o3 - o2, x);
-        if (a != 3) rank += count_pred<K, false>(nk + o3, oe - o3, x);
-        ok[nb + rank] = x;
-        ov[nb + rank] = sv[i];
+    for (uint32_t jn = 0; jn < cnt; ++jn) {
+        const uint32_t nb = pre[jn], S = pre[jn + 1] - nb;
+        if (S == 0) continue;  // a big node of the batch
+        const uint32_t* off = s_off[warp][jn];
+        const uint32_t o1 = off[1], o2 = off[2], o3 = off[3];
+        const K* k0 = sk + nb;
+        const int32_t* v0 = sv + nb;
+        if (o2 >= S) {  // 2-way
+            warp_merge2<K>(k0, v0, o1, k0 + o1, v0 + o1, S - o1, ok + nb, ov + nb);
+        } else {  // 3/4-way: X = A+B, Y = C+D (D empty for 3-way), then X+Y
+            warp_merge2<K>(k0, v0, o1, k0 + o1, v0 + o1, o2 - o1, xk + nb, xv + nb);
+            warp_merge2<K>(k0 + o2, v0 + o2, o3 - o2, k0 + o3, v0 + o3, S - o3, xk + nb + o2, xv + nb + o2);
+            __syncwarp();
+            warp_merge2<K>(xk + nb, xv + nb, o2, xk + nb + o2, xv + nb + o2, S - o2, ok + nb, ov + nb);
+        }
+        __syncwarp();
     }
-    __syncwarp();
 #pragma unroll 4
     for (uint32_t i = lane; i < total; i += 32) {
         const uint32_t j = snid[i];
