@@ -41,7 +41,7 @@ constexpr uint32_t SMALL_NODE = 512;  // nodes up to this size: one warp each (n
 // Tiny nodes stay on the warp kernel: a pipeline unit holds at most MAXSEG of
 // them and its producer then dominates.
 #ifndef PS_SMALL_MAX
-#define PS_SMALL_MAX 256
+#define PS_SMALL_MAX 512
 #endif
 constexpr uint32_t SMALL_KERNEL_MAX = PS_SMALL_MAX;
 static_assert(SMALL_KERNEL_MAX <= SMALL_NODE, "small-kernel threshold exceeds its capacity");
