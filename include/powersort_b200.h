@@ -61,11 +61,15 @@ typedef struct {
     int64_t min_run_len;       /* >= 1 (MIN_RUN_LEN = 24, policy.py:34-36) */
     int32_t strict_merge_down; /* policy.py:146-175 */
     int32_t values_mode;       /* ps_values_mode */
+    int32_t count_comparisons; /* 1: exact comparisons / moves (CountingOrder, statskit.py:49-72);
+                                  ps_sort then synchronizes after the merges */
+    int32_t reserved;
 } ps_config;
 
 /* SortStats, statskit.py:75-98 (scalar fields).  comparisons / moves are
  * data-dependent counters of the reference's sequential kernels; they are
- * reported only when *_valid is 1 (not yet on device). */
+ * computed when ps_config.count_comparisons is set and reported when *_valid
+ * is 1 (comparisons of the "4way-nosentinel" stages kernels are not). */
 typedef struct {
     int64_t comparisons;
     int64_t merge_cost;

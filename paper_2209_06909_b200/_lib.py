@@ -49,6 +49,8 @@ class PsConfig(ctypes.Structure):
         ("min_run_len", ctypes.c_int64),
         ("strict_merge_down", ctypes.c_int32),
         ("values_mode", ctypes.c_int32),
+        ("count_comparisons", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

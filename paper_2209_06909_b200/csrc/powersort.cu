@@ -459,6 +459,8 @@ struct MergeRunner {
     uint32_t pipe_grid_max;
 
     uint64_t nelem;  // elements in each buffer
+    int count_variant = -1;  // >= 0: CountingOrder counters of this merge variant per stage
+    Summary* sum = nullptr;
     uint32_t* bars;  // grid-barrier counters, one per fused-partition pipe launch
     uint32_t nbars, bar_next;
     bool fuse;
@@ -494,6 +496,11 @@ struct MergeRunner {
               int stage_id) {
         if (nhi <= nlo) return PS_OK;
         const uint32_t nbig = (nhi - nlo) - nsmall;
+        if (count_variant >= 0) {  // before the merges overwrite nothing the counters read
+            launch_k(merge_counters_kernel<K>, grid_for(nhi - nlo, 8), 256, 0, s, bufs, nodes, nlo, nhi, count_variant,
+                     sum);
+            PS_LAUNCH_CHECK();
+        }
         if (nsmall) {
             const uint32_t G = small_group(small_max);
             launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem, s, 
@@ -594,6 +601,10 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M)
         return fail(PS_EINVAL, "min_run_len > " + std::to_string(MAX_FORM_M) + " is not supported on device yet");
     const bool argsort = cfg.values_mode == PS_VALUES_ARGSORT;
+    // data-dependent counters: comparisons / moves on request; copy-smaller's
+    // buffer and scan counters always (both need a sync after the merges)
+    const bool counting = cfg.count_comparisons != 0;
+    const bool need_counts = counting || cfg.variant == PS_VARIANT_2WAY_COPY_SMALLER;
     Summary* sum = at<Summary>(ws, L.sum);
     PS_CUDA(cudaMemsetAsync(sum, 0, sizeof(Summary), s));
     uint32_t* err = &sum->err;
@@ -699,12 +710,12 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             launch_k(form_leaves_kernel<K, true>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r, ty,
-                     (uint32_t)m, tile_first);
+                     (uint32_t)m, tile_first, counting ? sum : nullptr);
         } else {
             PS_CUDA(cudaFuncSetAttribute(form_leaves_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
             launch_k(form_leaves_kernel<K, false>, grid, FORM_THREADS, smem, s, bufs, (uint64_t)n, b, nat, leafpar, r,
-                     ty, (uint32_t)m, tile_first);
+                     ty, (uint32_t)m, tile_first, counting ? sum : nullptr);
         }
         PS_LAUNCH_CHECK();
         prof.end(ph);
@@ -723,6 +734,8 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         int rc = mr.init(bufs, (uint64_t)n, at<Node>(ws, L.nodes), at<uint32_t>(ws, L.chunk2node), at<uint4>(ws, L.cuts),
                          err, at<uint32_t>(ws, L.bars), NBARS, s);
         if (rc) return rc;
+        mr.count_variant = need_counts ? cfg.variant : -1;
+        mr.sum = sum;
         int stage = 0;
         auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint64_t cost, uint32_t nsmall,
                              uint32_t small_max) -> int {
@@ -747,6 +760,11 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     prof.finish();  // synchronizes only while profiling
 
     // ---- N5: SortStats (statskit.py:75-98), from the tree summary ----------------
+    Summary c;  // the data-dependent counters, after the merges
+    if (need_counts) {
+        int rc = publish(sum, SUM_STATS, &c, nullptr, 0, nullptr, s);
+        if (rc) return rc;
+    }
     h = info.s;
     memset(st, 0, sizeof(*st));
     const int64_t M = (int64_t)h.merge_cost;
@@ -763,6 +781,30 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     st->moves = -1;
     st->comparisons_valid = 0;
     st->moves_valid = 0;
+    const bool sentinel_tournament = cfg.variant == PS_VARIANT_4WAY;
+    const int64_t m34 = (int64_t)(h.merges[3] + h.merges[4]);
+    if (cfg.variant == PS_VARIANT_2WAY_COPY_SMALLER) {
+        // merges.py:145-201: only the smaller run is buffered; copied + written moves
+        const int64_t cw = (int64_t)(c.cs_copied + c.cs_written);
+        st->buffer_cost = (int64_t)c.cs_copied;
+        st->scan_reads = n + cw;
+        st->scan_writes = n + cw;
+    }
+    if (counting) {
+        // comparisons: detection + extension + merges; the stages kernels'
+        // 3/4-way merges are not counted
+        st->comparisons_valid = !(cfg.variant == PS_VARIANT_4WAY_NOSENTINEL && m34 > 0);
+        st->comparisons = st->comparisons_valid ? (int64_t)c.comparisons : -1;
+        // moves: reversals + insertions, then per merge 2 * size (buffer out and
+        // back), + 1 for a stages merge, copied + written for copy-smaller
+        int64_t mv = (int64_t)c.moves;
+        if (cfg.variant == PS_VARIANT_2WAY_COPY_SMALLER)
+            mv += (int64_t)(c.cs_copied + c.cs_written);
+        else
+            mv += 2 * M + (sentinel_tournament ? 0 : m34);
+        st->moves = mv;
+        st->moves_valid = 1;
+    }
     return PS_OK;
 }
 

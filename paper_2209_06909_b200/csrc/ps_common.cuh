@@ -91,6 +91,13 @@ struct Summary {
     unsigned long long merges[5];      // by arity
     unsigned long long scan_slack;     // sum of per-merge slack (variant-specific)
     unsigned long long buffer_cost;
+    // CountingOrder counters (ps_config.count_comparisons): comparisons and the
+    // data-dependent moves of detection / extension; copy-smaller's copied and
+    // written element totals (merges.py:145-201)
+    unsigned long long comparisons;
+    unsigned long long moves;
+    unsigned long long cs_copied;
+    unsigned long long cs_written;
     unsigned long long level_cost[NPOW];     // merge cost per power bucket
     unsigned long long spine_cost[MAX_SPINE]; // merge cost per merge_down node
     uint32_t level_small[NPOW];               // nodes <= SMALL_NODE per power bucket

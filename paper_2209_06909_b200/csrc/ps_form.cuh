@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
                                                                    const uint32_t* __restrict__ nat,
                                                                    const uint8_t* __restrict__ leafpar, uint32_t r,
                                                                    const uint32_t* __restrict__ ty, uint32_t m,
-                                                                   const uint32_t* __restrict__ tile_first) {
+                                                                   const uint32_t* __restrict__ tile_first,
+                                                                   Summary* __restrict__ counters) {
     pdl_wait();
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
@@ -125,6 +126,35 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         spar[i] = leafpar[first + i];
     }
     __syncthreads();
+
+    // ---- CountingOrder counters (statskit.py:49-72), when requested ---------
+    // detection of every leaf starting in this tile (runs.py:23-47): the natural
+    // run's pair compares plus the failing one before the array end; a reversal
+    // moves its natural length.  Extension compares / moves are per element below.
+    unsigned long long c_cmp = 0, c_mov = 0;
+    auto flush_counters = [&]() {  // all threads; warp sums, one atomic pair per warp
+        if (!counters) return;
+        for (int dd = 16; dd; dd >>= 1) {
+            c_cmp += __shfl_xor_sync(PS_FULL, c_cmp, dd);
+            c_mov += __shfl_xor_sync(PS_FULL, c_mov, dd);
+        }
+        if (lane_id() == 0) {
+            if (c_cmp) atomicAdd(&counters->comparisons, c_cmp);
+            if (c_mov) atomicAdd(&counters->moves, c_mov);
+        }
+    };
+    if (counters) {
+        for (uint32_t i = tid; i < cnt; i += FORM_THREADS) {
+            const uint64_t bj = sb[i];
+            if (bj < t0) continue;  // counted by the tile it starts in
+            const uint32_t nj = snat[i];
+            if (nj >= 2) {
+                c_cmp += nj - 1 + (bj + nj < n ? 1 : 0);
+                const uint64_t q = bj + 1;
+                if (!((ty[q >> 5] >> (q & 31)) & 1u)) c_mov += nj;  // strictly descending: reversed
+            }
+        }
+    }
 
     // ---- natural leaves: copy / mirrored swap ------------------------------
     // Positions are handled FORM_BATCH at a time per thread: all loads of a
@@ -279,7 +309,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     // ---- extended windows starting in this tile: stable rank ---------------
     bool anywin = false;
     for (uint32_t i = tid; i < cnt; i += FORM_THREADS) anywin |= (snat[i] < sb[i + 1] - sb[i]) && (sb[i] >= t0);
-    if (!__syncthreads_or(anywin)) return;
+    if (!__syncthreads_or(anywin)) {
+        flush_counters();
+        return;
+    }
     // compact the window leaf ids (block scan of flags, several rounds)
     uint32_t nwin = 0;
     for (uint32_t base = 0; base < cnt; base += FORM_THREADS) {
@@ -294,7 +327,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         if (flag) wlist[nwin + ex] = i;
         nwin += tot;
     }
-    if (nwin == 0) return;
+    if (nwin == 0) {
+        flush_counters();
+        return;
+    }
     // element offsets of the windows
     uint32_t wtot = 0;
     for (uint32_t base = 0; base < nwin; base += FORM_THREADS) {
@@ -341,18 +377,28 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         const K x = wk[e];
         // stable rank in the window: earlier elements <= x, later elements < x
         // (one loop over the whole window: the same trip count on every lane)
-        uint32_t rank = 0;
+        uint32_t rank = 0, shifts = 0;
 #pragma unroll 4
         for (uint32_t f = wb; f < we; ++f) {
             const K y = wk[f];
             rank += (uint32_t)(y < x) | ((uint32_t)(f < e) & (uint32_t)!(x < y));
+            if (counters) shifts += (uint32_t)(f < e) & (uint32_t)(x < y);
         }
         const uint32_t leaf = wlist[lo];
+        if (counters && e - wb >= snat[leaf]) {
+            // insertion of element q past the sorted natural prefix (runs.py:50-68):
+            // it shifts the earlier elements > x, compares each of them plus the
+            // first <= x if there is one, and moves shifts + 1 when it shifts
+            const uint32_t q = e - wb;
+            c_cmp += shifts + (shifts < q ? 1u : 0u);
+            c_mov += shifts ? shifts + 1u : 0u;
+        }
         const uint32_t par = spar[leaf];
         const uint64_t dst = (uint64_t)sb[leaf] + rank;
         bufs.kb(par)[dst] = x;
         bufs.vb(par)[dst] = wv[e];
     }
+    flush_counters();
 }
 
 }  // namespace ps

@@ -202,6 +202,82 @@ PS_DEV void partition_chunk(const Bufs<K>& bufs, const Node* __restrict__ nodes,
     if (lane == 0) cuts[nd.chunk_base + 1 + mm] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
 }
 
+// CountingOrder comparisons of the reference's merge kernels (merges.py:75-334)
+// and the written count of merge_2way_copy_smaller (:145-201) for the nodes of
+// one stage, from the merged positions e_a of every run's last record (and, for
+// a backward copy-smaller merge, of its first records); one warp per node.
+// Sentinel compares are not counted (statskit.py:64-67):
+//   2-way (sentinel, no-sentinel, copy-smaller forward): min(e0, e1) + 1
+//   copy-smaller backward (n1 > n2): T - max(f0, f1)
+//   3/4-way tournament: the two first-level compares (one for 3-way), the root
+//     compares while both sides hold records, min(MX, MY) + 1, and the refills
+//     of a side while both its runs hold records: the side's outputs before its
+//     first run ends.
+// Variant ids follow ps_variant; 3/4-way nodes of the stages kernels (4) are
+// not counted.
+template <class K>
+__global__ void __launch_bounds__(256) merge_counters_kernel(Bufs<K> bufs, const Node* __restrict__ nodes, uint32_t nlo,
+                                                             uint32_t nhi, int variant, Summary* sum) {
+    pdl_wait();
+    const uint32_t idx = nlo + blockIdx.x * 8 + warp_id();
+    unsigned long long cmp = 0, wr = 0;
+    const Node nd = nodes[idx < nhi ? idx : nlo];
+    // the stages kernels' 3/4-way nodes (variant 4) are not counted
+    if (idx < nhi && (variant != 4 || nd.arity == 2)) {
+        const uint32_t w = nd.arity, T = nd.pos[w] - nd.pos[0];
+        const K* src = bufs.kb(nd.parity ^ 1);
+        uint32_t L[4], e[4], g[4][3];
+#pragma unroll
+        for (uint32_t a = 0; a < 4; ++a) L[a] = a < w ? nd.pos[a + 1] - nd.pos[a] : 0;
+#pragma unroll
+        for (uint32_t a = 0; a < 4; ++a) {
+            e[a] = 0;
+            g[a][0] = g[a][1] = g[a][2] = 0;
+            if (a >= w) continue;
+            // records of the other runs (in order) before run a's last record
+            const uint32_t b0 = a == 0 ? 1 : 0, b1 = a <= 1 ? 2 : 1, b2 = a == 3 ? 2 : 3;
+            const K y = src[(uint64_t)nd.pos[a + 1] - 1];
+            warp_count3<K>(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
+                           b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < a, b1 < a, b2 < a, w - 1, y, g[a]);
+            e[a] = L[a] - 1 + g[a][0] + (w > 2 ? g[a][1] : 0) + (w > 3 ? g[a][2] : 0);
+        }
+        if (w == 2) {
+            if (variant == 1 && L[0] > L[1]) {
+                // backward: first records' positions, f0 = run 1 before run 0's first
+                // record (strictly smaller), f1 = run 0 not after run 1's first (<=)
+                uint32_t f[3];
+                warp_count3<K>(src + nd.pos[1], src, src, L[1], 0, 0, false, false, false, 1, src[nd.pos[0]], f);
+                const uint32_t f0 = f[0];
+                uint32_t h[3];
+                warp_count3<K>(src + nd.pos[0], src, src, L[0], 0, 0, true, false, false, 1, src[nd.pos[1]], h);
+                const uint32_t f1 = h[0];
+                cmp = T - max(f0, f1);
+                wr = T - f1;
+            } else {
+                cmp = min(e[0], e[1]) + 1;
+                wr = e[0] + 1;
+            }
+        } else {
+            const uint32_t MX = max(e[0], e[1]), MY = w == 4 ? max(e[2], e[3]) : e[2];
+            // side X outputs before its first run ends: g[0][0] = run 1 before run 0's last
+            const uint32_t CX = e[0] < e[1] ? L[0] - 1 + g[0][0] : L[1] - 1 + g[1][0];
+            // side Y: g[2][2] = run 3 before run 2's last, g[3][2] = run 2 before run 3's last
+            const uint32_t CY = w == 4 ? (e[2] < e[3] ? L[2] - 1 + g[2][2] : L[3] - 1 + g[3][2]) : 0;
+            cmp = 1 + (w == 4 ? 1 : 0) + (min(MX, MY) + 1) + CX + CY;
+        }
+        if (variant != 1) wr = 0;
+    }
+    if (lane_id() != 0) cmp = wr = 0;
+    for (int dd = 16; dd; dd >>= 1) {
+        cmp += __shfl_xor_sync(PS_FULL, cmp, dd);
+        wr += __shfl_xor_sync(PS_FULL, wr, dd);
+    }
+    if (lane_id() == 0) {
+        if (cmp) atomicAdd(&sum->comparisons, cmp);
+        if (wr) atomicAdd(&sum->cs_written, wr);
+    }
+}
+
 // Stand-alone partition launch: one warp per chunk of [c0, c1).
 template <class K>
 __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,

@@ -418,7 +418,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
                                 int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch_out) {
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t i = i0 + threadIdx.x;
-    unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0;
+    unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0, copied = 0;
     if (i < nnodes) {
         Node nd = nodes[i];
         const int32_t depth = S[nd.probe] - 1;
@@ -434,6 +434,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         nodes[i] = nd;
         if (nch_out) nch_out[i] = nch;
         cost = size;
+        if (w == 2) copied = min(nd.pos[1] - nd.pos[0], nd.pos[2] - nd.pos[1]);  // copy-smaller's buffer
         m2 = w == 2;
         m3 = w == 3;
         m4 = w == 4;
@@ -474,9 +475,10 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         m3 += __shfl_xor_sync(PS_FULL, m3, d);
         m4 += __shfl_xor_sync(PS_FULL, m4, d);
         slack += __shfl_xor_sync(PS_FULL, slack, d);
+        copied += __shfl_xor_sync(PS_FULL, copied, d);
     }
     // block reduction, then one set of atomics per block
-    __shared__ unsigned long long s_red[5][32];
+    __shared__ unsigned long long s_red[6][32];
     const uint32_t wv = threadIdx.x >> 5;
     if (lane_id() == 0) {
         s_red[0][wv] = cost;
@@ -484,14 +486,16 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         s_red[2][wv] = m3;
         s_red[3][wv] = m4;
         s_red[4][wv] = slack;
+        s_red[5][wv] = copied;
     }
     __syncthreads();
-    if (threadIdx.x < 5) {
+    if (threadIdx.x < 6) {
         unsigned long long t = 0;
         for (uint32_t q = 0; q < (blockDim.x + 31) / 32; ++q) t += s_red[threadIdx.x][q];
         if (t) {
-            unsigned long long* dst = threadIdx.x == 0 ? &sum->merge_cost
+            unsigned long long* dst = threadIdx.x == 0   ? &sum->merge_cost
                                     : threadIdx.x == 4 ? &sum->scan_slack
+                                    : threadIdx.x == 5 ? &sum->cs_copied
                                                        : &sum->merges[threadIdx.x + 1];
             atomicAdd(dst, t);
         }

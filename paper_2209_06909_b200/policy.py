@@ -56,6 +56,10 @@ class SortConfig:
     key: Optional[Callable] = None
     strict_merge_down: bool = False
     on_merge: Optional[Callable] = None
+    #: B200 extension: compute the exact ``comparisons`` / ``moves`` counters of
+    #: the reference's CountingOrder (statskit.py:49-72); the sort then waits
+    #: for its merges.  Off: both are reported as None.
+    count_comparisons: bool = False
 
 
 def _validated(config):
@@ -140,7 +144,7 @@ def check(device=None):
 def _cfg_struct(config, values_mode):
     return _lib.PsConfig(
         config.k, _lib.VARIANT_IDS[config.variant], config.min_run_len, int(bool(config.strict_merge_down)),
-        values_mode,
+        values_mode, int(bool(getattr(config, "count_comparisons", False))), 0,
     )
 
 

@@ -22,6 +22,12 @@ from paper_2209_06909_b200 import (  # noqa: E402
 NP_DTYPE = {"int32": np.int32, "int64": np.int64, "float32": np.float32}
 POLICY_FIELDS = ("merge_cost", "max_stack_height", "runs_detected", "merges2", "merges3", "merges4")
 COUNTER_FIELDS = ("buffer_cost", "scan_reads", "scan_writes")
+VARIANTS = {"2way": 2, "2way-copy-smaller": 2, "2way-nosentinel": 2, "4way": 4, "4way-nosentinel": 4}
+
+
+def comparisons_counted(variant, stats):
+    # the stages kernels' 3/4-way merges (merges.py:337-545) are not counted on device
+    return not (variant == "4way-nosentinel" and stats.merges3 + stats.merges4 > 0)
 
 
 @pytest.fixture(scope="module")
@@ -51,11 +57,16 @@ def test_golden_sorts(golden_sorts, dev):
         assert perm.tolist() == case["perm"], cfg
         assert np.array_equal(out.view(np.uint8), keys[perm].view(np.uint8))
         want = case["stats"]
-        for f in POLICY_FIELDS:
+        for f in POLICY_FIELDS + COUNTER_FIELDS:
             assert getattr(stats, f) == want[f], (f, cfg)
-        if case["variant"] != "2way-copy-smaller":
-            for f in COUNTER_FIELDS:
-                assert getattr(stats, f) == want[f], (f, cfg)
+        assert stats.comparisons is None and stats.moves is None
+        _, perm2, cstats = gpu_sort(keys, dev, count_comparisons=True, **cfg)
+        assert perm2.tolist() == case["perm"], cfg
+        assert cstats.moves == want["moves"], (cfg, keys.size)
+        if comparisons_counted(case["variant"], cstats):
+            assert cstats.comparisons == want["comparisons"], (cfg, keys.size)
+        else:
+            assert cstats.comparisons is None
         assert stats.run_lengths == want["run_lengths"]
         assert stats.natural_run_lengths == want["natural_run_lengths"]
         assert [[list(b), l] for b, l in read_trace(device=dev)] == case["trace"], cfg
@@ -85,6 +96,26 @@ def test_recipes_vs_oracle(name, n, k, dev):
     assert stats.natural_run_lengths == ref.natural_run_lengths
     assert read_trace(device=dev) == ref.trace
     assert scanned_elements_estimate(stats, n) == 4 * ref.stats["merge_cost"] + 2 * n
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+@pytest.mark.parametrize("name,mrl", [("cfg1", 24), ("cfg2", 24), ("cfg3", 7), ("cfg4", 200), ("cfg5", 24)])
+def test_counters_vs_oracle(name, mrl, variant, dev):
+    # CountingOrder comparisons / moves and copy-smaller's buffer / scan counters
+    # through the pipe kernel's stage sizes (statskit.py:49-98)
+    n = 1 << 19
+    keys = workloads.generate(name, n=n, seed=23)
+    k = VARIANTS[variant]
+    ref = oracle.sort(keys, k=k, variant=variant, min_run_len=mrl)
+    out, perm, stats = gpu_sort(keys, dev, k=k, variant=variant, min_run_len=mrl, count_comparisons=True)
+    assert np.array_equal(perm, ref.values)
+    for f in POLICY_FIELDS + COUNTER_FIELDS + ("moves",):
+        assert getattr(stats, f) == ref.stats[f], f
+    if comparisons_counted(variant, stats):
+        assert stats.comparisons == ref.stats["comparisons"]
+    _, _, plain = gpu_sort(keys, dev, k=k, variant=variant, min_run_len=mrl)
+    for f in COUNTER_FIELDS:  # copy-smaller's counters without count_comparisons
+        assert getattr(plain, f) == ref.stats[f], f
 
 
 def test_cfg1_full_matches_reference_golden(golden_cfg_full, dev):
