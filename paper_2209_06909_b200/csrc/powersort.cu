@@ -127,15 +127,22 @@ struct WsHeader {
 struct HostMap {
     uint8_t* h = nullptr;
     uint8_t* d = nullptr;
-    size_t size = 0;
+    size_t size = 0;    // data bytes; a 16-byte flag word follows
+    uint32_t seq = 0;   // last publish sequence number
 };
 thread_local HostMap g_map;
 
+// Copies whole 16-byte words to mapped host memory, then raises the flag word
+// to seq: every thread fences its writes at system scope before the CTA
+// barrier, so the host sees the data once it sees the flag.
 __global__ void publish_kernel(const uint4* __restrict__ a, uint32_t na, const uint4* __restrict__ b, uint32_t nb,
-                               uint4* __restrict__ dst) {
+                               uint4* __restrict__ dst, volatile uint32_t* flag, uint32_t seq) {
     pdl_wait();
     for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) dst[i] = a[i];
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[na + i] = b[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = seq;
 }
 
 __global__ void write_header_kernel(WsHeader h, WsHeader* dst) {
@@ -146,30 +153,68 @@ __global__ void write_header_kernel(WsHeader h, WsHeader* dst) {
 int host_map_ensure(size_t bytes) {
     if (g_map.size >= bytes) return PS_OK;
     if (g_map.h) cudaFreeHost(g_map.h);
+    const uint32_t seq = g_map.seq;
     g_map = HostMap();
+    g_map.seq = seq;
     void* h = nullptr;
-    PS_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    PS_CUDA(cudaHostAlloc(&h, bytes + 16, cudaHostAllocMapped | cudaHostAllocPortable));
     void* d = nullptr;
     PS_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    memset(h, 0, bytes + 16);
     g_map.h = (uint8_t*)h;
     g_map.d = (uint8_t*)d;
     g_map.size = bytes;
     return PS_OK;
 }
 
-// Copies device ranges a (and b) to host a_out (b_out) and synchronizes the
-// stream.  Device sources are 16-byte aligned workspace regions; whole 16-byte
-// words are moved (16-byte PCIe writes), only `bytes` are returned.
-int publish(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out, cudaStream_t s) {
+// Device ranges a (and b) to host memory, in two halves so that the host can
+// enqueue more work before it waits: publish_begin enqueues the copy and
+// returns its sequence number; publish_wait spins on the flag word (no stream
+// synchronization: later work may already be queued behind the copy) and
+// returns the bytes.  Sources are 16-byte aligned workspace regions; whole
+// 16-byte words are moved (16-byte PCIe writes).
+struct Pending {
+    uint32_t seq = 0;
+    size_t abytes = 0, bbytes = 0;
+    void* a_out = nullptr;
+    void* b_out = nullptr;
+};
+int publish_begin(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out,
+                  cudaStream_t s, Pending& pend) {
     const size_t a16 = (abytes + 15) / 16, b16 = (bbytes + 15) / 16;
     int rc = host_map_ensure((a16 + b16) * 16);
     if (rc) return rc;
+    const uint32_t seq = ++g_map.seq;
+    volatile uint32_t* dflag = reinterpret_cast<volatile uint32_t*>(g_map.d + g_map.size);
     PS_CUDA(launch_k(publish_kernel, 1, 128, 0, s, (const uint4*)a, (uint32_t)a16, (const uint4*)b, (uint32_t)b16,
-                     (uint4*)g_map.d));
-    PS_CUDA(cudaStreamSynchronize(s));
-    memcpy(a_out, g_map.h, abytes);
-    if (bbytes) memcpy(b_out, g_map.h + a16 * 16, bbytes);
+                     (uint4*)g_map.d, dflag, seq));
+    pend.seq = seq;
+    pend.abytes = abytes;
+    pend.bbytes = bbytes;
+    pend.a_out = a_out;
+    pend.b_out = b_out;
     return PS_OK;
+}
+int publish_wait(const Pending& pend, cudaStream_t s) {
+    const volatile uint32_t* flag = reinterpret_cast<const volatile uint32_t*>(g_map.h + g_map.size);
+    for (uint32_t spins = 1; *flag != pend.seq; ++spins) {
+        if ((spins & 1023u) == 0) {  // a failed stream never raises the flag
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e != cudaSuccess && e != cudaErrorNotReady) PS_CUDA(e);
+            if (e == cudaSuccess && *flag != pend.seq) return fail(PS_EINVARIANT, "publish flag not raised");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const size_t a16 = (pend.abytes + 15) / 16;
+    memcpy(pend.a_out, g_map.h, pend.abytes);
+    if (pend.bbytes) memcpy(pend.b_out, g_map.h + a16 * 16, pend.bbytes);
+    return PS_OK;
+}
+int publish(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out, cudaStream_t s) {
+    Pending pend;
+    int rc = publish_begin(a, abytes, a_out, b, bbytes, b_out, s, pend);
+    if (rc) return rc;
+    return publish_wait(pend, s);
 }
 
 // leading Summary fields the host needs at each synchronization point
@@ -288,23 +333,24 @@ T* at(uint8_t* ws, uint64_t off) {
 
 inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)std::max<uint64_t>(1, cdiv(n, t)); }
 
-// End of the tree phase: one publish of the summary and the stage chunk
-// offsets (the host schedules the merges from them), then the chunk map.
-int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s) {
+// End of the tree phase: the chunk -> node map (its size is read on the
+// device), then one publish of the summary and the stage chunk offsets (the
+// host schedules the merges from them).  The publish is only enqueued here;
+// tree_wait() collects it, so the caller can queue leaf formation first.
+int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s, Pending& pend) {
     Summary* sum = at<Summary>(ws, L.sum);
-    {
-        int rc = publish(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
-                         info.stage_chunk, s);
-        if (rc) return rc;
-    }
-    const uint32_t nnodes = info.s.nmain + info.s.nspine_nodes;
-    if (nnodes && info.total_chunks() > 0) {
-        const uint32_t total = info.total_chunks();
-        if (total > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
-        launch_k(tree_chunk_map_kernel, grid_for(total, 256), 256, 0, s, (const Node*)at<Node>(ws, L.nodes), nnodes,
-                 total, at<uint32_t>(ws, L.chunk2node));
-        PS_LAUNCH_CHECK();
-    }
+    launch_k(tree_chunk_map_kernel, CHUNK_MAP_CTAS, 256, 0, s, (const Node*)at<Node>(ws, L.nodes), (const Summary*)sum,
+             (const uint32_t*)at<uint32_t>(ws, L.stage_chunk), (uint32_t)std::min<uint64_t>(L.chunks_max, 0xFFFFFFFFull),
+             at<uint32_t>(ws, L.chunk2node));
+    PS_LAUNCH_CHECK();
+    return publish_begin(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
+                         info.stage_chunk, s, pend);
+}
+
+int tree_wait(const Layout& L, TreeInfo& info, cudaStream_t s, const Pending& pend) {
+    int rc = publish_wait(pend, s);
+    if (rc) return rc;
+    if (info.total_chunks() > L.chunks_max) return fail(PS_ENOMEM, "merge chunk table exceeds workspace bound");
     if (info.s.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
     if (info.s.err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(info.s.err) + ")");
     return PS_OK;
@@ -313,13 +359,14 @@ int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s) {
 // Builds the merge tree of the run boundaries b[0..r] (device, already in
 // place) for an array of n elements.  Leaves leaf parities when leafpar != 0.
 int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int strict, int slack_mode,
-               uint8_t* leafpar, TreeInfo& info, cudaStream_t s, uint32_t cap = CHUNK_CAP) {
+               uint8_t* leafpar, TreeInfo& info, cudaStream_t s, Pending& pend, uint32_t cap = CHUNK_CAP) {
     Summary* sum = at<Summary>(ws, L.sum);
     uint32_t* err = &sum->err;
     const uint32_t* b = at<uint32_t>(ws, L.b);
     uint8_t* P = at<uint8_t>(ws, L.P);
     const uint32_t log2k = k == 4 ? 2 : 1;
-    const uint32_t padded = (uint32_t)L.lev_size[0];
+    // P over [0, padded): r + 1 boundaries and 0xFF up to the next multiple of 32
+    const uint32_t padded = (uint32_t)align_up((uint64_t)r + 1, 32);
     static const bool no_small_tree = getenv("PS_NO_SMALL_TREE") != nullptr;  // A/B: multi-kernel path
     if (r <= TREE_SMALL_R && !no_small_tree) {
         // the whole build in one CTA (tree_small_kernel), then one publish
@@ -367,7 +414,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
         a.sum = sum;
         PS_CUDA(launch_k(tree_small_kernel, 1, CLS_THREADS, 0, s, a));
         launch_counter()++;
-        return finish_tree(ws, L, info, s);
+        return finish_tree(ws, L, info, s, pend);
     }
     // T1 powers (array over 0..padded) with min-tree level 1, T2 the other levels
     int32_t* Dd = at<int32_t>(ws, L.Dd);
@@ -442,7 +489,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, nodes, cb, nmax, (const Summary*)sum,
              at<uint32_t>(ws, L.stage_chunk));
     PS_LAUNCH_CHECK();
-    return finish_tree(ws, L, info, s);
+    return finish_tree(ws, L, info, s, pend);
 }
 
 // Runs one batch of disjoint merge nodes [nlo, nhi) whose chunks are
@@ -601,6 +648,9 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M)
         return fail(PS_EINVAL, "min_run_len > " + std::to_string(MAX_FORM_M) + " is not supported on device yet");
     const bool argsort = cfg.values_mode == PS_VALUES_ARGSORT;
+    // PS_DEBUG_STAGES=s (measurement only): enqueue the first s merge stages;
+    // -1 / -2 / -3: stop after run detection / the tree / leaf formation
+    static const int stage_limit = getenv("PS_DEBUG_STAGES") ? atoi(getenv("PS_DEBUG_STAGES")) : 1 << 30;
     // data-dependent counters: comparisons / moves on request; copy-smaller's
     // buffer and scan counters always (both need a sync after the merges)
     const bool counting = cfg.count_comparisons != 0;
@@ -676,22 +726,24 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     if (h.err) return fail(PS_EINVARIANT, "run detection invariant violated (flags " + std::to_string(h.err) + ")");
     const uint32_t r = h.r;
     if (r < 1 || r + 2 > L.rmax) return fail(PS_EINVARIANT, "run count out of range: " + std::to_string(r));
+    if (stage_limit == -1) return PS_OK;
 
     // ---- N2: merge tree --------------------------------------------------------
     uint8_t* leafpar = at<uint8_t>(ws, L.leafpar);
     TreeInfo info;
     memset(&info.s, 0, sizeof(info.s));
     uint32_t nnodes = 0;
+    Pending tree_pend;  // the tree summary, collected after leaf formation is queued
     const int ph_tree = prof.begin(1, -1, 0, 0, 0);
     if (r >= 2) {
         int rc = build_tree(ws, L, r, (uint64_t)n, cfg.k, cfg.strict_merge_down, slack_mode_of(cfg.variant), leafpar,
-                            info, s, cut_cap<K>());
+                            info, s, tree_pend, cut_cap<K>());
         if (rc) return rc;
-        nnodes = info.s.nmain + info.s.nspine_nodes;
     } else {
         PS_CUDA(cudaMemsetAsync(leafpar, 0, 1, s));
     }
     prof.end(ph_tree);
+    if (stage_limit == -2) return PS_OK;
 
     // ---- N1 pass 2: leaves -----------------------------------------------------
     Bufs<K> bufs;
@@ -721,6 +773,12 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         prof.end(ph);
     }
 
+    if (r >= 2) {
+        int rc = tree_wait(L, info, s, tree_pend);
+        if (rc) return rc;
+        nnodes = info.s.nmain + info.s.nspine_nodes;
+    }
+    if (stage_limit == -3) return PS_OK;
     {
         int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s);
         if (rc) return rc;
@@ -739,7 +797,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         int stage = 0;
         auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint64_t cost, uint32_t nsmall,
                              uint32_t small_max) -> int {
-            if (nhi <= nlo) return PS_OK;
+            if (nhi <= nlo || stage >= stage_limit) return PS_OK;
             const int ph = prof.begin(4, stage, nhi - nlo, c1 - c0, 2 * (int64_t)cost * rec_bytes);
             int rc2 = mr.stage(nlo, nhi, c0, c1, nsmall, small_max, &prof, stage);
             prof.end(ph);
@@ -953,11 +1011,7 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
         nd.arity = (uint8_t)arity;
         nd.parity = (uint8_t)parity;
         nd.probe = 0;
-        const uint32_t size = pos[arity] - pos[0];
-        uint32_t nch = size <= SMALL_KERNEL_MAX ? 0 : 1;
-        if (size > cap)
-            for (uint32_t a = 0; a < arity; ++a) nch += (pos[a + 1] - pos[a] - 1) / (cap / arity);
-        nd.nchunks = nch;
+        nd.nchunks = node_chunks(nd, cap, SMALL_KERNEL_MAX);
         return nd;
     };
     std::vector<std::vector<Node>> levels;
@@ -1176,7 +1230,10 @@ int ps_tree_from_profile(const int64_t* lengths, int64_t r, int32_t k, int32_t s
     TreeInfo info;
     memset(&info.s, 0, sizeof(info.s));
     if (r >= 2) {
-        int rc = build_tree(ws, L, (uint32_t)r, n, k, strict_merge_down, 0, nullptr, info, s);
+        Pending pend;
+        int rc = build_tree(ws, L, (uint32_t)r, n, k, strict_merge_down, 0, nullptr, info, s, pend);
+        if (rc) return rc;
+        rc = tree_wait(L, info, s, pend);
         if (rc) return rc;
     }
     int rc = write_header(ws, L, (int64_t)n, 1, k, 0, (uint32_t)r, info.s.nmain, info.s.nspine_nodes, s);

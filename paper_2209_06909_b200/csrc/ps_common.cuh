@@ -76,6 +76,21 @@ struct Node {
 };
 static_assert(sizeof(Node) == 40, "Node layout");
 
+// Cut spacing of a node's runs (ps_merge.cuh): cap / arity, so that a chunk
+// holds <= cap records.  (Finer cuts for the single-node merge_down stages were
+// measured: no gain, their time is the partition search and the first load.)
+PS_DEV __host__ uint32_t node_spacing(const Node& nd, uint32_t cap) { return cap / nd.arity; }
+// chunks of a node: 0 for the small-node kernel, else 1 + its cut points
+PS_DEV __host__ uint32_t node_chunks(const Node& nd, uint32_t cap, uint32_t small_max) {
+    const uint32_t w = nd.arity, size = nd.pos[w] - nd.pos[0];
+    if (size <= small_max) return 0;
+    const uint32_t S = node_spacing(nd, cap);
+    uint32_t nch = 1;
+    if (size > w * S)
+        for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / S;
+    return nch;
+}
+
 // Device -> host summary, read once after the tree is built.
 struct Summary {
     uint32_t r;              // runs
@@ -127,6 +142,31 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+
+// Barrier over all CTAs of a grid whose CTAs are co-resident (persistent
+// grids of <= one CTA per SM).  ctr is zeroed before the launch; the k-th
+// barrier of a launch waits for target = k * gridDim.x arrivals.  A bounded
+// spin turns a missing CTA into ERR_BARRIER instead of a hang.
+PS_DEV void grid_barrier(uint32_t* ctr, uint32_t target, uint32_t* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        for (uint32_t spins = 0;; ++spins) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(100);
+            if (spins > (1u << 23)) {
+                atomicOr(err, ERR_BARRIER);
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 
 PS_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 PS_DEV uint32_t warp_id() { return threadIdx.x >> 5; }

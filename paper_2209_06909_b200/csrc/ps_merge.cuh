@@ -171,7 +171,7 @@ PS_DEV void partition_chunk(const Bufs<K>& bufs, const Node* __restrict__ nodes,
     }
     q -= 1;
     const uint32_t w = nd.arity;
-    const uint32_t S = cut_cap<K>() / w;
+    const uint32_t S = node_spacing(nd, cut_cap<K>());
     const K* src = bufs.kb(nd.parity ^ 1);
     uint32_t L[4];
 #pragma unroll
@@ -287,29 +287,6 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     const uint32_t c = c0 + blockIdx.x * 8 + warp_id();
     if (c >= c1) return;
     partition_chunk<K>(bufs, nodes, chunk2node, c, cuts);
-}
-
-// Barrier over all CTAs of a grid whose CTAs are co-resident (the persistent
-// pipe grid: <= one CTA per SM).  ctr is zeroed before the launch.  A bounded
-// spin turns a missing CTA into ERR_BARRIER instead of a hang.
-PS_DEV void grid_barrier(uint32_t* ctr, uint32_t nblocks, uint32_t* err) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        for (uint32_t spins = 0;; ++spins) {
-            uint32_t v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (v >= nblocks) break;
-            __nanosleep(100);
-            if (spins > (1u << 23)) {
-                atomicOr(err, ERR_BARRIER);
-                break;
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -875,6 +852,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 for (int t = 0; t < 5; ++t) nd.pos[t] = 0;
             }
             const uint32_t tot = (en.x - st.x) + (en.y - st.y) + (en.z - st.z) + (en.w - st.w);
+            // records per unit of this chunk's node (arity * cut spacing <= cut_cap)
+            const uint32_t ucap = xv ? (uint32_t)nd.arity * node_spacing(nd, cut_cap<K>()) : cut_cap<K>();
             // segment starts (node changes) and inclusive prefixes over the batch:
             // PT records, PC records + 2 VT per segment (pass layout slack), PS segments
             const uint32_t nid_prev = __shfl_up_sync(PS_FULL, nid, 1);
@@ -898,12 +877,13 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 const uint32_t nid_u = __shfl_sync(PS_FULL, nid, u);
                 const uint32_t XTu = __shfl_sync(PS_FULL, XT, u), XCu = __shfl_sync(PS_FULL, XC, u);
                 const uint32_t XSu = __shfl_sync(PS_FULL, XS, u), sgsu = __shfl_sync(PS_FULL, sgs, u);
+                const uint32_t ucapu = __shfl_sync(PS_FULL, ucap, u);
                 const bool same = nid == nid_u;
                 const uint32_t sumT = PT - XTu;
                 const uint32_t sumC = PC - XCu + (sgsu ? 0u : 2 * VT);
                 const uint32_t nsg = PS - XSu + (sgsu ? 0u : 1u);
                 const bool ok = lane >= u && lane < nvalid &&
-                                (same ? sumT <= cut_cap<K>() : (sumC <= LY::CAP && nsg <= MAXSEG));
+                                (same ? sumT <= ucapu : (sumC <= LY::CAP && nsg <= MAXSEG));
                 const uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
                 const uint32_t runlen = __ffs(~bal) ? __ffs(~bal) - 1 : 32 - u;
                 const uint32_t V = u + max(runlen, 1u) - 1;

@@ -178,9 +178,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_seq_kernel(const T* in, T* 
 // blockDim * ITEMS items with a running carry.  items: blockDim * ITEMS
 // elements of shared memory, sw: 32.  Ends with a CTA barrier.
 template <class T, class Op, int ITEMS>
-PS_DEV void cta_scan(const T* in, T* out, int64_t n, bool reverse, bool exclusive, T* total_out, T* items, T* sw) {
+PS_DEV void cta_scan(const T* in, T* out, int64_t n, bool reverse, bool exclusive, T* total_out, T* items, T* sw,
+                     T carry = Op::id()) {
     Op op;
-    T carry = Op::id();
     const int TB = (int)blockDim.x * ITEMS;
     for (int64_t base = 0; base < n; base += TB) {
         for (int i = threadIdx.x; i < TB; i += blockDim.x) {

@@ -425,11 +425,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         nd.parity = (uint8_t)(depth & 1);
         const uint32_t w = nd.arity;
         const uint32_t size = nd.pos[w] - nd.pos[0];
-        uint32_t nch = size <= SMALL_KERNEL_MAX ? 0 : 1;
-        if (size > cap) {
-            const uint32_t spacing = cap / w;
-            for (uint32_t a = 0; a < w; ++a) nch += (nd.pos[a + 1] - nd.pos[a] - 1) / spacing;
-        }
+        const uint32_t nch = node_chunks(nd, cap, SMALL_KERNEL_MAX);
         nd.nchunks = nch;
         nodes[i] = nd;
         if (nch_out) nch_out[i] = nch;
@@ -594,28 +590,37 @@ __global__ void tree_nchunks_kernel(const Node* __restrict__ nodes, uint32_t nma
     if (i < nmax) out[i] = i < node_count(sum, nmax) ? nodes[i].nchunks : 0u;
 }
 
-// chunk -> node map by binary search over the nodes' chunk_base.
-__global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, uint32_t nnodes, uint32_t total_chunks,
+// chunk -> node map by binary search over the nodes' chunk_base; the node and
+// chunk counts are read on the device (grid-stride over CHUNK_MAP_CTAS CTAs).
+constexpr uint32_t CHUNK_MAP_CTAS = 4 * 148;
+__global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, const Summary* __restrict__ sum,
+                                      const uint32_t* __restrict__ stage_chunk, uint32_t chunks_max,
                                       uint32_t* __restrict__ chunk2node) {
     pdl_wait();
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= total_chunks) return;
-    uint32_t lo = 0, hi = nnodes;  // find last node with chunk_base <= c
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (nodes[mid].chunk_base <= c)
-            lo = mid;
-        else
-            hi = mid;
+    const uint32_t nnodes = sum->nmain + sum->nspine_nodes;
+    const uint32_t total = stage_chunk[NPOW + 2 + MAX_SPINE];
+    if (nnodes == 0 || total > chunks_max) return;  // (the host fails on the published total)
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nnodes;  // find last node with chunk_base <= c
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (nodes[mid].chunk_base <= c)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        chunk2node[c] = lo;
     }
-    chunk2node[c] = lo;
 }
 
 // ---------------------------------------------------------------------------
 // The whole tree build (T1-T5) for r <= TREE_SMALL_R boundaries in ONE CTA of
 // CLS_THREADS threads: the phases of the multi-kernel path back to back with
 // CTA barriers instead of ~20 dependent launches.
-constexpr uint32_t TREE_SMALL_R = 1024;  // measured: wins at r = 491, loses at r = 4059
+#ifndef PS_TREE_SMALL_R
+#define PS_TREE_SMALL_R 1024
+#endif
+constexpr uint32_t TREE_SMALL_R = PS_TREE_SMALL_R;
 
 struct TreeSmallArgs {
     const uint32_t* b;
