@@ -68,8 +68,7 @@ typedef struct {
 
 /* SortStats, statskit.py:75-98 (scalar fields).  comparisons / moves are
  * data-dependent counters of the reference's sequential kernels; they are
- * computed when ps_config.count_comparisons is set and reported when *_valid
- * is 1 (comparisons of the "4way-nosentinel" stages kernels are not). */
+ * computed when ps_config.count_comparisons is set (then *_valid is 1). */
 typedef struct {
     int64_t comparisons;
     int64_t merge_cost;

@@ -849,10 +849,9 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         st->scan_writes = n + cw;
     }
     if (counting) {
-        // comparisons: detection + extension + merges; the stages kernels'
-        // 3/4-way merges are not counted
-        st->comparisons_valid = !(cfg.variant == PS_VARIANT_4WAY_NOSENTINEL && m34 > 0);
-        st->comparisons = st->comparisons_valid ? (int64_t)c.comparisons : -1;
+        // comparisons: detection + extension + merges
+        st->comparisons_valid = 1;
+        st->comparisons = (int64_t)c.comparisons;
         // moves: reversals + insertions, then per merge 2 * size (buffer out and
         // back), + 1 for a stages merge, copied + written for copy-smaller
         int64_t mv = (int64_t)c.moves;

@@ -213,8 +213,8 @@ PS_DEV void partition_chunk(const Bufs<K>& bufs, const Node* __restrict__ nodes,
 //     compares while both sides hold records, min(MX, MY) + 1, and the refills
 //     of a side while both its runs hold records: the side's outputs before its
 //     first run ends.
-// Variant ids follow ps_variant; 3/4-way nodes of the stages kernels (4) are
-// not counted.
+// Variant ids follow ps_variant; 3/4-way nodes of the stages kernels (4): see
+// the simulation below.
 template <class K>
 __global__ void __launch_bounds__(256) merge_counters_kernel(Bufs<K> bufs, const Node* __restrict__ nodes, uint32_t nlo,
                                                              uint32_t nhi, int variant, Summary* sum) {
@@ -222,8 +222,7 @@ __global__ void __launch_bounds__(256) merge_counters_kernel(Bufs<K> bufs, const
     const uint32_t idx = nlo + blockIdx.x * 8 + warp_id();
     unsigned long long cmp = 0, wr = 0;
     const Node nd = nodes[idx < nhi ? idx : nlo];
-    // the stages kernels' 3/4-way nodes (variant 4) are not counted
-    if (idx < nhi && (variant != 4 || nd.arity == 2)) {
+    if (idx < nhi) {
         const uint32_t w = nd.arity, T = nd.pos[w] - nd.pos[0];
         const K* src = bufs.kb(nd.parity ^ 1);
         uint32_t L[4], e[4], g[4][3];
@@ -257,6 +256,66 @@ __global__ void __launch_bounds__(256) merge_counters_kernel(Bufs<K> bufs, const
                 cmp = min(e[0], e[1]) + 1;
                 wr = e[0] + 1;
             }
+        } else if (variant == 4) {
+            // stages kernels (merges.py:337-545): a tournament over the live runs
+            // until the first of them ends, then again over the rest, then a
+            // 2-way stage.  In a tournament every output costs its z compare plus
+            // the refetch compare of its side when that side holds two runs,
+            // except while the other side's pending head is the last record of
+            // its run (safe = 0): then the output costs the unfetch + refetch of
+            // both sides, 2 + [four] compares; the run-ending output costs none.
+            // Merged positions: mpos(c, i) of record i of run c; cnt(x, c) = run c
+            // records before run x's last (merged position e[x]).
+            auto slot = [](uint32_t c, uint32_t a) { return c < a ? c : c - 1; };
+            auto before_last = [&](uint32_t x, uint32_t c) -> uint32_t {
+                return c == x ? L[x] - 1 : g[x][slot(c, x)];
+            };
+            auto mpos = [&](uint32_t c, uint32_t i) -> int64_t {
+                const uint32_t b0 = c == 0 ? 1 : 0, b1 = c <= 1 ? 2 : 1, b2 = c == 3 ? 2 : 3;
+                uint32_t h[3];
+                warp_count3<K>(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
+                               b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < c, b1 < c, b2 < c, w - 1,
+                               src[(uint64_t)nd.pos[c] + i], h);
+                return (int64_t)i + h[0] + (w > 2 ? h[1] : 0) + (w > 3 ? h[2] : 0);
+            };
+            uint32_t alive[4] = {0, 1, 2, 3}, na = w;
+            int64_t os = 0;
+            int32_t bprev = -1;
+            while (na >= 3) {
+                const bool four = na == 4;
+                uint32_t be = alive[0];
+                for (uint32_t i = 1; i < na; ++i) be = e[alive[i]] < e[be] ? alive[i] : be;
+                const int64_t oe = e[be];
+                cmp += 2 + (four ? 1 : 0) + (uint64_t)(oe - os);
+                if (four) {
+                    cmp += (uint64_t)(oe - os);
+                } else {
+                    for (uint32_t i = 0; i < 2; ++i) {  // left-side outputs in [os, oe)
+                        const uint32_t c = alive[i];
+                        cmp += before_last(be, c) - (bprev < 0 ? 0u : before_last((uint32_t)bprev, c));
+                    }
+                }
+                for (uint32_t i = 0; i < na; ++i) {
+                    const uint32_t b = alive[i];
+                    const bool left = i < 2;
+                    if (!four && !left) continue;  // a right-side pending head costs the same either way
+                    // q: merged position of the last record of b's side before b's last
+                    int64_t q = -1;
+                    if (L[b] >= 2) q = mpos(b, L[b] - 2);
+                    const int32_t sib = left ? (int32_t)alive[1 - i] : (int32_t)alive[5 - i];
+                    const uint32_t gc = before_last(b, (uint32_t)sib);
+                    if (gc >= 1) q = max(q, mpos((uint32_t)sib, gc - 1));
+                    const int64_t lo = max(q, os - 1), hi = min((int64_t)e[b], oe);
+                    if (hi > lo + 1) cmp += (uint64_t)(hi - lo - 1);
+                }
+                uint32_t k2 = 0;  // drop the ended run, keep the order
+                for (uint32_t i = 0; i < na; ++i)
+                    if (alive[i] != be) alive[k2++] = alive[i];
+                na = k2;
+                bprev = (int32_t)be;
+                os = oe + 1;
+            }
+            if (na == 2) cmp += (uint64_t)(min(e[alive[0]], e[alive[1]]) - os + 1);
         } else {
             const uint32_t MX = max(e[0], e[1]), MY = w == 4 ? max(e[2], e[3]) : e[2];
             // side X outputs before its first run ends: g[0][0] = run 1 before run 0's last
