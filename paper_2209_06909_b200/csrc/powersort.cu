@@ -127,22 +127,29 @@ struct WsHeader {
 struct HostMap {
     uint8_t* h = nullptr;
     uint8_t* d = nullptr;
-    size_t size = 0;    // data bytes; a 16-byte flag word follows
+    size_t size = 0;
     uint32_t seq = 0;   // last publish sequence number
 };
 thread_local HostMap g_map;
 
-// Copies whole 16-byte words to mapped host memory, then raises the flag word
-// to seq: every thread fences its writes at system scope before the CTA
-// barrier, so the host sees the data once it sees the flag.
-__global__ void publish_kernel(const uint4* __restrict__ a, uint32_t na, const uint4* __restrict__ b, uint32_t nb,
-                               uint4* __restrict__ dst, volatile uint32_t* flag, uint32_t seq) {
+// Copies the 32-bit words of a || b (each zero-padded to 16 bytes) to mapped
+// host memory, three per 16-byte store with the sequence number as the fourth:
+// a 16-byte store arrives whole, so the host knows every word once every store
+// carries seq.  (No system-scope fence: it would wait behind the bulk host
+// copies other streams keep on the link.)
+__global__ void publish_kernel(const uint32_t* __restrict__ a, uint32_t na, const uint32_t* __restrict__ b,
+                               uint32_t nb, uint4* __restrict__ dst, uint32_t seq) {
     pdl_wait();
-    for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) dst[i] = a[i];
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[na + i] = b[i];
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) *flag = seq;
+    const uint32_t nw = na + nb, ns = (nw + 2) / 3;
+    for (uint32_t q = threadIdx.x; q < ns; q += blockDim.x) {
+        uint32_t v[3];
+#pragma unroll
+        for (uint32_t t = 0; t < 3; ++t) {
+            const uint32_t w = 3 * q + t;
+            v[t] = w < na ? a[w] : (w < nw ? b[w - na] : 0u);
+        }
+        dst[q] = make_uint4(v[0], v[1], v[2], seq);
+    }
 }
 
 __global__ void write_header_kernel(WsHeader h, WsHeader* dst) {
@@ -157,10 +164,10 @@ int host_map_ensure(size_t bytes) {
     g_map = HostMap();
     g_map.seq = seq;
     void* h = nullptr;
-    PS_CUDA(cudaHostAlloc(&h, bytes + 16, cudaHostAllocMapped | cudaHostAllocPortable));
+    PS_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
     void* d = nullptr;
     PS_CUDA(cudaHostGetDevicePointer(&d, h, 0));
-    memset(h, 0, bytes + 16);
+    memset(h, 0, bytes);
     g_map.h = (uint8_t*)h;
     g_map.d = (uint8_t*)d;
     g_map.size = bytes;
@@ -168,11 +175,10 @@ int host_map_ensure(size_t bytes) {
 }
 
 // Device ranges a (and b) to host memory, in two halves so that the host can
-// enqueue more work before it waits: publish_begin enqueues the copy and
-// returns its sequence number; publish_wait spins on the flag word (no stream
+// enqueue more work before it waits: publish_begin enqueues the copy;
+// publish_wait spins until every store carries the sequence number (no stream
 // synchronization: later work may already be queued behind the copy) and
-// returns the bytes.  Sources are 16-byte aligned workspace regions; whole
-// 16-byte words are moved (16-byte PCIe writes).
+// unpacks the bytes.  Sources are 16-byte aligned workspace regions.
 struct Pending {
     uint32_t seq = 0;
     size_t abytes = 0, bbytes = 0;
@@ -181,13 +187,13 @@ struct Pending {
 };
 int publish_begin(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out,
                   cudaStream_t s, Pending& pend) {
-    const size_t a16 = (abytes + 15) / 16, b16 = (bbytes + 15) / 16;
-    int rc = host_map_ensure((a16 + b16) * 16);
+    const size_t na = (abytes + 15) / 16 * 4, nb = (bbytes + 15) / 16 * 4;
+    const size_t ns = (na + nb + 2) / 3;
+    int rc = host_map_ensure(ns * 16);
     if (rc) return rc;
     const uint32_t seq = ++g_map.seq;
-    volatile uint32_t* dflag = reinterpret_cast<volatile uint32_t*>(g_map.d + g_map.size);
-    PS_CUDA(launch_k(publish_kernel, 1, 128, 0, s, (const uint4*)a, (uint32_t)a16, (const uint4*)b, (uint32_t)b16,
-                     (uint4*)g_map.d, dflag, seq));
+    PS_CUDA(launch_k(publish_kernel, 1, 256, 0, s, (const uint32_t*)a, (uint32_t)na, (const uint32_t*)b,
+                     (uint32_t)nb, (uint4*)g_map.d, seq));
     pend.seq = seq;
     pend.abytes = abytes;
     pend.bbytes = bbytes;
@@ -196,18 +202,27 @@ int publish_begin(const void* a, size_t abytes, void* a_out, const void* b, size
     return PS_OK;
 }
 int publish_wait(const Pending& pend, cudaStream_t s) {
-    const volatile uint32_t* flag = reinterpret_cast<const volatile uint32_t*>(g_map.h + g_map.size);
-    for (uint32_t spins = 1; *flag != pend.seq; ++spins) {
-        if ((spins & 1023u) == 0) {  // a failed stream never raises the flag
+    const size_t na = (pend.abytes + 15) / 16 * 4, nb = (pend.bbytes + 15) / 16 * 4;
+    const size_t ns = (na + nb + 2) / 3;
+    const volatile uint32_t* hw = reinterpret_cast<const volatile uint32_t*>(g_map.h);
+    auto arrived = [&]() {
+        for (size_t q = ns; q-- > 0;)  // the last stores are the likeliest to be missing
+            if (hw[4 * q + 3] != pend.seq) return false;
+        return true;
+    };
+    for (uint32_t spins = 1; !arrived(); ++spins) {
+        if ((spins & 255u) == 0) {  // a failed stream never delivers
             const cudaError_t e = cudaStreamQuery(s);
             if (e != cudaSuccess && e != cudaErrorNotReady) PS_CUDA(e);
-            if (e == cudaSuccess && *flag != pend.seq) return fail(PS_EINVARIANT, "publish flag not raised");
+            if (e == cudaSuccess && !arrived()) return fail(PS_EINVARIANT, "published summary did not arrive");
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
-    const size_t a16 = (pend.abytes + 15) / 16;
-    memcpy(pend.a_out, g_map.h, pend.abytes);
-    if (pend.bbytes) memcpy(pend.b_out, g_map.h + a16 * 16, pend.bbytes);
+    auto word = [&](size_t w) -> uint32_t { return hw[4 * (w / 3) + (w % 3)]; };
+    std::vector<uint32_t> tmp(na + nb);
+    for (size_t w = 0; w < na + nb; ++w) tmp[w] = word(w);
+    memcpy(pend.a_out, tmp.data(), pend.abytes);
+    if (pend.bbytes) memcpy(pend.b_out, tmp.data() + na, pend.bbytes);
     return PS_OK;
 }
 int publish(const void* a, size_t abytes, void* a_out, const void* b, size_t bbytes, void* b_out, cudaStream_t s) {
@@ -230,6 +245,7 @@ struct Layout {
     // offsets
     uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
         minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts, bars, tile_first,
+        nodes_tmp, hist2, hist2_off, hist2_tot,
         scantmp_u32, scantmp_i32, total;
 };
 
@@ -262,7 +278,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
         P = cdiv(P, TSCAN_FAN);
     }
     uint64_t big = std::max<uint64_t>({L.rmax + MAX_SPINE + 2, L.ngroups + 2, (uint64_t)NPOW * cdiv(L.rmax, CLS_THREADS) + 2,
-                                       L.rmax});
+                                       (uint64_t)NSTAGE * cdiv(L.rmax + MAX_SPINE, FIN_THREADS) + 2, L.rmax});
     L.scan_tmp = scan_tmp_elems(big);
 
     uint64_t off = 0;
@@ -306,9 +322,13 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.hist_tot = take(16);
     L.spine = take(MAX_SPINE * 4);
     L.nodes = take((L.rmax + MAX_SPINE) * sizeof(Node));
+    L.nodes_tmp = take((L.rmax + MAX_SPINE) * sizeof(Node));
+    L.hist2 = take(((uint64_t)NSTAGE * cdiv(L.rmax + MAX_SPINE, FIN_THREADS) + 2) * 4);
+    L.hist2_off = take(((uint64_t)NSTAGE * cdiv(L.rmax + MAX_SPINE, FIN_THREADS) + 2) * 4);
+    L.hist2_tot = take(16);
     L.nch = take((L.rmax + MAX_SPINE + 2) * 4);
     L.chunk_base = take((L.rmax + MAX_SPINE + 2) * 4);
-    L.stage_chunk = take((NPOW + 3 + MAX_SPINE) * 4);
+    L.stage_chunk = take((NSTAGE + 2) * 4);
     L.chunk2node = take(L.chunks_max * 4);
     L.scantmp_u32 = take(L.scan_tmp * 4);
     L.scantmp_i32 = take(L.scan_tmp * 4);
@@ -319,11 +339,10 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
 // Host copy of the summary plus the per-stage chunk ranges.
 struct TreeInfo {
     Summary s;
-    // chunk_base at level offsets [0..NPOW], at spine nodes [NPOW+1+i], total [NPOW+2+MAX_SPINE]
-    uint32_t stage_chunk[NPOW + 3 + MAX_SPINE];
-    uint32_t level_chunk(uint32_t p) const { return stage_chunk[p]; }
-    uint32_t spine_chunk(uint32_t i) const { return stage_chunk[NPOW + 1 + i]; }
-    uint32_t total_chunks() const { return stage_chunk[NPOW + 2 + MAX_SPINE]; }
+    // chunk_base at the stage offsets [0..NSTAGE], total [NSTAGE+1]
+    uint32_t stage_chunk[NSTAGE + 2];
+    uint32_t level_chunk(uint32_t h) const { return stage_chunk[h]; }
+    uint32_t total_chunks() const { return stage_chunk[NSTAGE + 1]; }
 };
 
 template <class T>
@@ -406,6 +425,11 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
         a.htot = at<uint32_t>(ws, L.hist_tot);
         a.spine = at<uint32_t>(ws, L.spine);
         a.nodes = at<Node>(ws, L.nodes);
+        a.nodes_tmp = at<Node>(ws, L.nodes_tmp);
+        a.hist2 = at<uint32_t>(ws, L.hist2);
+        a.hoff2 = at<uint32_t>(ws, L.hist2_off);
+        a.htot2 = at<uint32_t>(ws, L.hist2_tot);
+        a.nblocks_f = (uint32_t)cdiv(r + MAX_SPINE, CLS_THREADS);
         a.leafpar = leafpar;
         a.nmax = r + MAX_SPINE;
         a.nch = at<uint32_t>(ws, L.nch);
@@ -459,7 +483,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     uint32_t* hoff = at<uint32_t>(ws, L.hist_off);
     uint32_t* htot = at<uint32_t>(ws, L.hist_tot);
     uint32_t* spine = at<uint32_t>(ws, L.spine);
-    Node* nodes = at<Node>(ws, L.nodes);
+    Node* nodes = at<Node>(ws, L.nodes_tmp);  // regrouped by height into L.nodes at the end
     launch_k(tree_classify_kernel<0>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
@@ -470,7 +494,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
-    launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum);
+    launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum, mt);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan2<int32_t, OpSum<int32_t>>(Dd, Dd, Sd, Sd, (int64_t)r + 1, false, false,
@@ -482,11 +506,22 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_LAUNCH_CHECK();
     uint32_t* nch = at<uint32_t>(ws, L.nch);
     uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
-    launch_k(tree_nodes_finalize_kernel, grid_for(nmax, 256), 256, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, nch);
+    uint32_t* hist2 = at<uint32_t>(ws, L.hist2);
+    uint32_t* hoff2 = at<uint32_t>(ws, L.hist2_off);
+    uint32_t* htot2 = at<uint32_t>(ws, L.hist2_tot);
+    const uint32_t nfb = (uint32_t)cdiv(nmax, FIN_THREADS);
+    launch_k(tree_nodes_finalize_kernel, nfb, FIN_THREADS, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, hist2, nfb);
+    PS_LAUNCH_CHECK();
+    // T6: regroup the nodes by merge stage
+    PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist2, hoff2, (int64_t)NSTAGE * nfb, false, true,
+                                                   at<uint32_t>(ws, L.scantmp_u32), htot2, s)));
+    Node* final_nodes = at<Node>(ws, L.nodes);
+    launch_k(tree_stage_scatter_kernel, nfb, FIN_THREADS, 0, s, (const Node*)nodes, final_nodes, nmax, nfb,
+             (const uint32_t*)hoff2, (const uint32_t*)htot2, sum, nch);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nmax, false, true, at<uint32_t>(ws, L.scantmp_u32),
                                                    cb + nmax, s)));
-    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, nodes, cb, nmax, (const Summary*)sum,
+    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, final_nodes, cb, nmax, (const Summary*)sum,
              at<uint32_t>(ws, L.stage_chunk));
     PS_LAUNCH_CHECK();
     return finish_tree(ws, L, info, s, pend);
@@ -804,14 +839,11 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             stage++;
             return rc2;
         };
-        for (int p = (int)NPOW - 1; p >= 1; --p) {
-            rc = run_stage(info.s.level_off[p], info.s.level_off[p + 1], info.level_chunk(p), info.level_chunk(p + 1),
-                           info.s.level_cost[p], info.s.level_small[p], info.s.level_small_max[p]);
-            if (rc) return rc;
-        }
-        for (uint32_t i = 0; i < info.s.nspine_nodes; ++i) {
-            rc = run_stage(info.s.nmain + i, info.s.nmain + i + 1, info.spine_chunk(i), info.spine_chunk(i + 1),
-                           info.s.spine_cost[i], info.s.spine_small[i], SMALL_NODE);
+        // one launch per merge stage (T6): power levels, higher first, with the
+        // merge_down nodes one stage after their last input
+        for (uint32_t h = 1; h < NSTAGE; ++h) {
+            rc = run_stage(info.s.level_off[h], info.s.level_off[h + 1], info.level_chunk(h), info.level_chunk(h + 1),
+                           info.s.level_cost[h], info.s.level_small[h], info.s.level_small_max[h]);
             if (rc) return rc;
         }
     }
@@ -1182,15 +1214,17 @@ int ps_result_trace(const void* workspace, int64_t* rows, int64_t cap) {
                            cudaMemcpyDeviceToHost));
     // main-loop merges execute when boundary R arrives, higher powers first
     // (policy.py:250-259); then _merge_down in sequence (policy.py:146-175).
-    std::vector<uint32_t> idx(h.nmain);
-    for (uint32_t i = 0; i < h.nmain; ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
+    // (the node table is grouped by height, T6: the order is rebuilt here)
+    std::vector<uint32_t> idx, spine;
+    for (uint32_t i = 0; i < nn; ++i) (nodes[i].flags & 1 ? spine : idx).push_back(i);
+    std::sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
         const Node &x = nodes[a], &y = nodes[b];
         const uint32_t ex = x.pos[x.arity], ey = y.pos[y.arity];
         if (ex != ey) return ex < ey;
         return x.power > y.power;
     });
-    for (uint32_t i = 0; i < h.nspine_nodes; ++i) idx.push_back(h.nmain + i);
+    std::sort(spine.begin(), spine.end(), [&](uint32_t a, uint32_t b) { return nodes[a].order < nodes[b].order; });
+    idx.insert(idx.end(), spine.begin(), spine.end());
     for (uint32_t i = 0; i < nn; ++i) {
         const Node& x = nodes[idx[i]];
         int64_t* row = rows + 7 * i;

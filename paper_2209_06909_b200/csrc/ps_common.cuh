@@ -49,6 +49,7 @@ static_assert(SMALL_KERNEL_MAX <= SMALL_NODE, "small-kernel threshold exceeds it
 constexpr uint32_t INF32 = 0xFFFFFFFFu;
 constexpr uint32_t MAX_SPINE = 256;
 constexpr uint32_t NPOW = 64;  // power buckets (powers are <= 33 for n <= 2^31)
+constexpr uint32_t NSTAGE = 128;  // merge stages: NPOW - power, merge_down nodes after their inputs (< 2^7)
 
 // Error flags raised on the device (bitmask in Summary.err).
 enum : uint32_t {
@@ -101,7 +102,7 @@ struct Summary {
     uint32_t max_stack;      // max_stack_height
     uint32_t total_chunks;
     uint32_t pad0;
-    uint32_t level_off[NPOW + 1];  // node offsets per power bucket (ascending power)
+    uint32_t level_off[NSTAGE + 1];  // node offsets per power bucket, then (T6) per merge stage
     unsigned long long merge_cost;
     unsigned long long merges[5];      // by arity
     unsigned long long scan_slack;     // sum of per-merge slack (variant-specific)
@@ -113,11 +114,9 @@ struct Summary {
     unsigned long long moves;
     unsigned long long cs_copied;
     unsigned long long cs_written;
-    unsigned long long level_cost[NPOW];     // merge cost per power bucket
-    unsigned long long spine_cost[MAX_SPINE]; // merge cost per merge_down node
-    uint32_t level_small[NPOW];               // nodes <= SMALL_NODE per power bucket
-    uint32_t level_small_max[NPOW];           // largest small node per power bucket
-    uint32_t spine_small[MAX_SPINE];
+    unsigned long long level_cost[NSTAGE];     // merge cost per merge stage
+    uint32_t level_small[NSTAGE];               // nodes <= SMALL_NODE per stage
+    uint32_t level_small_max[NSTAGE];           // largest small node per stage
 };
 
 // Programmatic dependent launch (PDL).  Every kernel is launched with

@@ -310,15 +310,38 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
 }
 
 // T4: the spine and _merge_down (policy.py:146-175): staged by the CTA, replayed by one thread.
+// min of level 0 over [lo, hi) of a 32-ary min tree: partial groups at each
+// level, whole groups one level up
+PS_DEV uint32_t range_min(const MinTree& t, uint32_t lo, uint32_t hi) {
+    uint32_t m = 0xFF;
+    for (uint32_t L = 0; lo < hi; ++L) {
+        const uint8_t* a = t.lev[L];
+        const uint32_t lo2 = (lo + 31) & ~31u, hi2 = hi & ~31u;
+        if (L + 1 >= t.nlev || lo2 >= hi2) {
+            for (uint32_t x = lo; x < hi; ++x) m = min(m, (uint32_t)a[x]);
+            break;
+        }
+        for (uint32_t x = lo; x < lo2; ++x) m = min(m, (uint32_t)a[x]);
+        for (uint32_t x = hi2; x < hi; ++x) m = min(m, (uint32_t)a[x]);
+        lo = lo2 >> 5;
+        hi = hi2 >> 5;
+    }
+    return m;
+}
+
+// Merge stage of a main-loop node: its power level, higher powers first.
+PS_DEV uint32_t main_stage(uint32_t power) { return NPOW - power; }
+
 PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                            uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, int32_t* __restrict__ Ddiff,
-                           Summary* sum) {
+                           Summary* sum, const MinTree& mt) {
     // the stack entries are staged and sorted by the CTA, their run starts are
     // gathered in parallel; one thread then replays _merge_down from shared memory
     __shared__ uint32_t s_list[MAX_SPINE];
     __shared__ uint32_t s_beta[MAX_SPINE + 2];  // beta[1] = 0, beta[h] = s_{h-1}; [H+1] = first run_begin
     __shared__ uint32_t s_bval[MAX_SPINE + 2];  // b[beta[h]]
     __shared__ uint32_t s_br;
+    __shared__ uint8_t s_key[MAX_SPINE + 2];  // merge stage of stack entry h's subtree (0: a single run)
     const uint32_t t = threadIdx.x;
     uint32_t H = sum->nspine;
     if (H > MAX_SPINE) {
@@ -335,15 +358,31 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
     for (uint32_t h = t + 1; h <= H + 1; h += blockDim.x)
         s_beta[h] = h == 1 ? 0u : (h <= H ? s_list[h - 2] : (H ? s_list[H - 1] : 0u));
     __syncthreads();
-    for (uint32_t h = t + 1; h <= H + 1; h += blockDim.x) s_bval[h] = b[s_beta[h]];
+    for (uint32_t h = t + 1; h <= H + 1; h += blockDim.x) {
+        s_bval[h] = b[s_beta[h]];
+        // entry h spans boundaries [beta_h, end); its subtree's root is the main
+        // node of the smallest power strictly inside
+        const uint32_t lo = s_beta[h] + 1, hi = h <= H ? s_beta[h + 1] : r;
+        s_key[h] = (uint8_t)(lo < hi ? main_stage(range_min(mt, lo, hi)) : 0u);
+    }
     if (t == 0) s_br = b[r];
     __syncthreads();
     if (t != 0) return;
-    const uint32_t nmain = sum->level_off[NPOW];
+    const uint32_t nmain = sum->nmain;
     uint32_t nn = 0;
     uint32_t height = H;
     uint32_t run_begin = H + 1;  // index into s_beta / s_bval
+    uint32_t cur_key = s_key[H + 1];  // stage of the accumulated last run
     auto emit = [&](const uint32_t* hh, uint32_t w) {
+        // a merge_down node runs after the last of its inputs (earliest stage here)
+        uint32_t key = cur_key;
+        for (uint32_t i = 0; i + 1 < w; ++i) key = max(key, (uint32_t)s_key[hh[i]]);
+        key += 1;
+        if (key >= NSTAGE) {
+            atomicOr(&sum->err, ERR_SPINE);
+            key = NSTAGE - 1;
+        }
+        cur_key = key;
         Node nd;
         for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = 0;
         for (uint32_t i = 0; i < w; ++i) nd.pos[i] = s_bval[hh[i]];
@@ -351,7 +390,7 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
         nd.arity = (uint8_t)w;
         nd.parity = 0;
         nd.power = 0;
-        nd.flags = 1;
+        nd.flags = (uint8_t)(1u | (key << 1));
         nd.probe = s_beta[hh[1]];
         nd.chunk_base = 0;
         nd.nchunks = 0;
@@ -396,13 +435,20 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
             }
         }
     }
+    // as late as possible: the chain ends at the root's stage, each node one
+    // stage before its consumer (>= its earliest stage, which is at least one
+    // less per step), so the chain shares the last main-loop launches
+    for (uint32_t i = 0; i < nn; ++i) {
+        const uint32_t key = cur_key - (nn - 1 - i);
+        nodes[nmain + i].flags = (uint8_t)(1u | (key << 1));
+    }
     sum->nspine_nodes = nn;
 }
 __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                                   uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
-                                  int32_t* __restrict__ Ddiff, Summary* sum) {
+                                  int32_t* __restrict__ Ddiff, Summary* sum, MinTree mt) {
     pdl_wait();
-    tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum);
+    tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum, mt);
 }
 
 // T5: per-node depth/parity, chunk counts and merge statistics; leaf parity.
@@ -414,21 +460,40 @@ PS_DEV uint32_t node_count(const Summary* sum, uint32_t nmax) {
     return c < nmax ? c : nmax;
 }
 
+// ---- T6: the merge schedule ---------------------------------------------------
+// Every node carries a merge stage (flags >> 1): a main-loop node its power
+// level (main_stage, higher powers first), a merge_down node one stage after
+// the last of its inputs (tree_spine_cta).  Children always come in earlier
+// stages, so the merge_down chain shares the main-loop levels' launches instead
+// of running as a tail of single-node launches.  (Any topological order is
+// valid: a node writes buffer depth & 1 over its own range, which only its
+// ancestors read afterwards.)  Nodes are regrouped by stage, one launch each.
+constexpr uint32_t FIN_THREADS = 256;
+
+// T5: per-node depth/parity, merge stage, chunk counts, merge statistics and
+// per-stage statistics; the block's stage histogram (hist[h * nblocks + blk])
+// for the stable regrouping.
 PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch_out) {
+                                int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ hist,
+                                uint32_t nblocks) {
+    __shared__ uint32_t s_hh[NSTAGE];
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t i = i0 + threadIdx.x;
+    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) s_hh[t] = 0;
+    __syncthreads();
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0, copied = 0;
+    uint32_t key = 0xFFFFFFFFu, sz = 0, sm = 0;
     if (i < nnodes) {
         Node nd = nodes[i];
         const int32_t depth = S[nd.probe] - 1;
         nd.parity = (uint8_t)(depth & 1);
         const uint32_t w = nd.arity;
         const uint32_t size = nd.pos[w] - nd.pos[0];
-        const uint32_t nch = node_chunks(nd, cap, SMALL_KERNEL_MAX);
-        nd.nchunks = nch;
+        nd.nchunks = node_chunks(nd, cap, SMALL_KERNEL_MAX);
+        if (!(nd.flags & 1)) nd.flags = (uint8_t)(main_stage(nd.power) << 1);  // (spine: set by tree_spine_cta)
+        const uint32_t stage = nd.flags >> 1;
         nodes[i] = nd;
-        if (nch_out) nch_out[i] = nch;
+        atomicAdd(&s_hh[stage], 1u);
         cost = size;
         if (w == 2) copied = min(nd.pos[1] - nd.pos[0], nd.pos[2] - nd.pos[1]);  // copy-smaller's buffer
         m2 = w == 2;
@@ -436,24 +501,12 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         m4 = w == 4;
         slack = slack_mode == 0 ? w : (slack_mode == 1 ? (w == 2 ? 0 : 1) : 0);
         if (depth < 0) atomicOr(&sum->err, ERR_CHAIN);
-        if (nd.flags & 1) {
-            sum->spine_cost[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size;
-            sum->spine_small[nd.order < MAX_SPINE ? nd.order : MAX_SPINE - 1] = size <= SMALL_KERNEL_MAX;
-        }
+        key = stage;
+        sz = size;
+        sm = size <= SMALL_KERNEL_MAX;
     }
-    if (nch_out && i >= nnodes && i < nmax) nch_out[i] = 0;  // scan padding
-    // per-level cost / small counts: one atomic per distinct power per warp
-    // (main nodes are level-sorted, so a warp mostly holds one power)
+    // per-stage cost / small counts: one atomic per distinct stage per warp
     {
-        uint32_t key = 0xFFFFFFFFu, sz = 0, sm = 0;
-        if (i < nnodes) {
-            const Node& nd = nodes[i];
-            if (!(nd.flags & 1)) {
-                key = nd.power;
-                sz = nd.pos[nd.arity] - nd.pos[0];
-                sm = sz <= SMALL_KERNEL_MAX;
-            }
-        }
         const uint32_t grp = __match_any_sync(PS_FULL, key);
         const uint32_t gsz = __reduce_add_sync(grp, sz), gsm = __reduce_add_sync(grp, sm);
         const uint32_t gmx = __reduce_max_sync(grp, sm ? sz : 0u);
@@ -496,30 +549,84 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
             atomicAdd(dst, t);
         }
     }
-    __syncthreads();  // s_red is reused by the next call
+    const uint32_t blk = i0 / blockDim.x;
+    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) hist[(uint64_t)t * nblocks + blk] = s_hh[t];
+    __syncthreads();  // s_red / s_hh are reused by the next call
 }
-__global__ void tree_nodes_finalize_kernel(Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                           int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch) {
+__global__ void __launch_bounds__(FIN_THREADS) tree_nodes_finalize_kernel(
+    Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S, int slack_mode, uint32_t cap,
+    Summary* sum, uint32_t* __restrict__ hist, uint32_t nblocks) {
     pdl_wait();
-    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, nch);
+    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, hist, nblocks);
 }
 
-// chunk_base at the node indices the host schedules stages by: level offsets
-// (out[0..NPOW]), spine nodes (out[NPOW+1+i], i <= nspine_nodes) and the total
-// (out[NPOW+2+MAX_SPINE]); cb has nnodes+1 entries.
+// T6: stable scatter of block blk's nodes into their stage buckets (hoff =
+// exclusive scan of the block histograms), with the chunk counts in the new
+// order (zero padding up to nmax for the chunk scan).  Block 0 also writes the
+// stage offsets level_off[h] (the host's schedule).
+PS_DEV void tree_stage_scatter_block(uint32_t i0, const Node* __restrict__ src, Node* __restrict__ dst,
+                                      uint32_t nmax, uint32_t nblocks, const uint32_t* __restrict__ hoff,
+                                      const uint32_t* __restrict__ htot, Summary* sum,
+                                      uint32_t* __restrict__ nch_out, uint32_t (*whist)[NSTAGE]) {
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    const uint32_t nnodes = node_count(sum, nmax);
+    const uint32_t blk = i0 / blockDim.x;
+    for (uint32_t t = tid; t < 32 * NSTAGE; t += blockDim.x) (&whist[0][0])[t] = 0;
+    __syncthreads();
+    const uint32_t i = i0 + tid;
+    const bool valid = i < nnodes;
+    Node nd;
+    uint32_t h = 0xFFFFFFFFu;
+    if (valid) {
+        nd = src[i];
+        h = nd.flags >> 1;
+    }
+    const uint32_t peers = __match_any_sync(PS_FULL, h);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+    if (valid && rank == 0) whist[warp][h] = __popc(peers);
+    __syncthreads();
+    if (tid < NSTAGE) {
+        uint32_t acc = 0;
+        for (uint32_t w = 0; w < 32; ++w) {
+            const uint32_t x = whist[w][tid];
+            whist[w][tid] = acc;
+            acc += x;
+        }
+    }
+    __syncthreads();
+    if (valid) {
+        const uint32_t slot = hoff[(uint64_t)h * nblocks + blk] + whist[warp][h] + rank;
+        dst[slot] = nd;
+        nch_out[slot] = nd.nchunks;
+    }
+    if (i >= nnodes && i < nmax) nch_out[i] = 0;
+    if (blk == 0) {
+        if (tid < NSTAGE) sum->level_off[tid] = hoff[(uint64_t)tid * nblocks];
+        if (tid == 0) sum->level_off[NSTAGE] = *htot;
+    }
+    __syncthreads();  // whist is reused by the next call
+}
+__global__ void __launch_bounds__(FIN_THREADS) tree_stage_scatter_kernel(
+    const Node* __restrict__ src, Node* __restrict__ dst, uint32_t nmax, uint32_t nblocks,
+    const uint32_t* __restrict__ hoff, const uint32_t* __restrict__ htot, Summary* sum,
+    uint32_t* __restrict__ nch_out) {
+    pdl_wait();
+    __shared__ uint32_t whist[32][NSTAGE];
+    tree_stage_scatter_block(blockIdx.x * blockDim.x, src, dst, nmax, nblocks, hoff, htot, sum, nch_out, whist);
+}
+
+// chunk_base at the node indices the host schedules stages by: the stage
+// offsets (out[0..NSTAGE]) and the total (out[NSTAGE+1]); cb has nnodes+1
+// entries.
 PS_DEV void tree_stage_chunks_cta(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum, uint32_t nmax,
                                    uint32_t* __restrict__ out) {
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t t = threadIdx.x;
-    if (t <= NPOW) {
-        const uint32_t i = sum->level_off[t];
-        out[t] = cb[i < nnodes ? i : nnodes];
+    for (uint32_t h = t; h <= NSTAGE; h += blockDim.x) {
+        const uint32_t i = sum->level_off[h];
+        out[h] = cb[i < nnodes ? i : nnodes];
     }
-    for (uint32_t i = t; i <= MAX_SPINE; i += blockDim.x) {
-        const uint32_t j = sum->nmain + i;
-        out[NPOW + 1 + i] = cb[j < nnodes ? j : nnodes];
-    }
-    if (t == 0) out[NPOW + 2 + MAX_SPINE] = cb[nnodes];
+    if (t == 0) out[NSTAGE + 1] = cb[nnodes];
 }
 __global__ void tree_stage_chunks_kernel(const uint32_t* __restrict__ cb, const Summary* __restrict__ sum,
                                          uint32_t nmax, uint32_t* __restrict__ out) {
@@ -598,7 +705,7 @@ __global__ void tree_chunk_map_kernel(const Node* __restrict__ nodes, const Summ
                                       uint32_t* __restrict__ chunk2node) {
     pdl_wait();
     const uint32_t nnodes = sum->nmain + sum->nspine_nodes;
-    const uint32_t total = stage_chunk[NPOW + 2 + MAX_SPINE];
+    const uint32_t total = stage_chunk[NSTAGE + 1];
     if (nnodes == 0 || total > chunks_max) return;  // (the host fails on the published total)
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
         uint32_t lo = 0, hi = nnodes;  // find last node with chunk_base <= c
@@ -649,11 +756,18 @@ struct TreeSmallArgs {
     uint32_t* cb;
     uint32_t* stage_chunk;
     Summary* sum;
+    // T6: classification writes nodes_tmp, the stage scatter writes nodes
+    Node* nodes_tmp;
+    uint32_t* hist2;
+    uint32_t* hoff2;
+    uint32_t* htot2;
+    uint32_t nblocks_f;                     // finalize blocks of blockDim nodes
 };
 
 __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a) {
     pdl_wait();
     __shared__ uint32_t s_items[CLS_THREADS * 4];
+    static_assert(CLS_THREADS * 4 >= 32 * NSTAGE, "s_items doubles as the stage scatter's histogram");
     __shared__ uint32_t s_sw[32];
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     uint32_t* err = &a.sum->err;
@@ -676,15 +790,15 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a
     __syncthreads();
     for (uint32_t vb = 0; vb < a.nblocks; ++vb)
         tree_classify_block<0>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, a.hist, nullptr, a.Dd, a.Sd, a.spine,
-                               a.nodes, a.sum);
+                               a.nodes_tmp, a.sum);
     cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.hist, a.hoff, (int64_t)NPOW * a.nblocks, false, true, a.htot, s_items,
                                            s_sw);
     tree_level_offsets_cta(a.hoff, a.htot, a.nblocks, a.sum);
     __syncthreads();
     for (uint32_t vb = 0; vb < a.nblocks; ++vb)
         tree_classify_block<1>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, nullptr, a.hoff, a.Dd, a.Sd, a.spine,
-                               a.nodes, a.sum);
-    tree_spine_cta(a.b, a.r, a.k, a.strict, a.spine, a.nodes, a.Dd, a.sum);
+                               a.nodes_tmp, a.sum);
+    tree_spine_cta(a.b, a.r, a.k, a.strict, a.spine, a.nodes_tmp, a.Dd, a.sum, a.mt);
     __syncthreads();
     cta_scan<int32_t, OpSum<int32_t>, 4>(a.Dd, a.Dd, (int64_t)a.r + 1, false, false, nullptr,
                                          reinterpret_cast<int32_t*>(s_items), reinterpret_cast<int32_t*>(s_sw));
@@ -708,7 +822,13 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a
     }
     __syncthreads();
     for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
-        tree_finalize_block(i0, a.nodes, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum, a.nch);
+        tree_finalize_block(i0, a.nodes_tmp, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum, a.hist2, a.nblocks_f);
+    __syncthreads();
+    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.hist2, a.hoff2, (int64_t)NSTAGE * a.nblocks_f, false, true, a.htot2,
+                                           s_items, s_sw);
+    for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
+        tree_stage_scatter_block(i0, a.nodes_tmp, a.nodes, a.nmax, a.nblocks_f, a.hoff2, a.htot2, a.sum, a.nch,
+                                 reinterpret_cast<uint32_t(*)[NSTAGE]>(s_items));  // (32 x NSTAGE words)
     __syncthreads();
     cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.nch, a.cb, a.nmax, false, true, a.cb + a.nmax, s_items, s_sw);
     {
