@@ -44,24 +44,38 @@ __global__ void __launch_bounds__(256) rd_types_kernel(const K* __restrict__ a, 
     const uint32_t g = blockIdx.x;
     const uint64_t G = (uint64_t)g * GROUP;
     const uint32_t lane = lane_id(), warp = warp_id();
-#pragma unroll 1
-    for (int round = 0; round < 2; ++round) {
-        const uint32_t wbase = warp * 64 + round * 32;
-        const uint64_t p0 = G + 32ull * wbase;
-        K carry = (p0 >= 1 && p0 - 1 < n) ? a[p0 - 1] : K(0);
-        uint32_t myword = 0;
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-            const uint64_t p = p0 + 32ull * i + lane;
-            K x = (p < n) ? a[p] : K(0);
-            K xp = shfl_up(x, 1);
-            if (lane == 0) xp = carry;
-            bool bit = (p >= 1) && (p < n) && key_le(xp, x);
-            uint32_t word = __ballot_sync(PS_FULL, bit);
-            carry = shfl(x, 31);
-            if ((int)lane == i) myword = word;
+    // each lane loads 16 bytes (EPL keys) per step: a warp step covers KPI keys
+    // = EPL type words, gathered from 32 / EPL lanes each (the keys are 16-byte
+    // aligned, ps_sort checks it)
+    constexpr uint32_t EPL = 16 / sizeof(K), KPI = 32 * EPL, LPW = 32 / EPL;
+    static_assert(TILE % KPI == 0, "a warp's tile is whole steps");
+    const uint64_t p0 = G + (uint64_t)warp * TILE;
+    K carry = (p0 >= 1 && p0 - 1 < n) ? a[p0 - 1] : K(0);
+#pragma unroll 4
+    for (uint32_t it = 0; it < TILE / KPI; ++it) {
+        const uint64_t q0 = p0 + (uint64_t)it * KPI + lane * EPL;
+        K x[EPL];
+        if (q0 + EPL <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + q0);
+            memcpy(x, &v, 16);
+        } else {
+#pragma unroll
+            for (uint32_t e = 0; e < EPL; ++e) x[e] = q0 + e < n ? a[q0 + e] : K(0);
         }
-        sw[wbase + lane] = myword;
+        K prev = shfl_up(x[EPL - 1], 1);
+        if (lane == 0) prev = carry;
+        uint32_t nib = 0;
+#pragma unroll
+        for (uint32_t e = 0; e < EPL; ++e) {
+            const uint64_t q = q0 + e;
+            const bool bit = q >= 1 && q < n && key_le(e == 0 ? prev : x[e - 1], x[e]);
+            nib |= (uint32_t)bit << e;
+        }
+        carry = shfl(x[EPL - 1], 31);
+        uint32_t wv = nib << (EPL * (lane % LPW));
+#pragma unroll
+        for (uint32_t d = 1; d < LPW; d <<= 1) wv |= __shfl_xor_sync(PS_FULL, wv, d);
+        if (lane % LPW == 0) sw[warp * (TILE / 32) + it * EPL + lane / LPW] = wv;
     }
     __syncthreads();
     uint32_t best = INF32;
