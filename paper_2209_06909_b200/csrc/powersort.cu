@@ -655,9 +655,6 @@ int validate_cfg(const ps_config* cfg) {
         return fail(PS_EINVAL, "variant implements k=" + std::to_string(vk) + ", but config asks for k=" +
                                    std::to_string(cfg->k));
     if (cfg->min_run_len < 1) return fail(PS_EINVAL, "min_run_len must be >= 1");
-    if (cfg->min_run_len > (int64_t)MAX_FORM_M && cfg->min_run_len < (int64_t)1 << 40) {
-        // windows longer than MAX_FORM_M are not staged yet
-    }
     return PS_OK;
 }
 
@@ -680,8 +677,6 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     const Layout L = make_layout((uint64_t)n, sizeof(K), m, true);
     if (wsb < L.total)
         return fail(PS_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
-    if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M)
-        return fail(PS_EINVAL, "min_run_len > " + std::to_string(MAX_FORM_M) + " is not supported on device yet");
     const bool argsort = cfg.values_mode == PS_VALUES_ARGSORT;
     // PS_DEBUG_STAGES=s (measurement only): enqueue the first s merge stages;
     // -1 / -2 / -3: stop after run detection / the tree / leaf formation
@@ -805,6 +800,17 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                      ty, (uint32_t)m, tile_first, counting ? sum : nullptr);
         }
         PS_LAUNCH_CHECK();
+        if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M) {
+            // windows longer than a tile's staging capacity: one CTA per window
+            const size_t bsm = big_window_smem_bytes<K>();
+            if (argsort)
+                launch_k(form_big_windows_kernel<K, true>, BIGW_CTAS, BIGW_THREADS, bsm, s, bufs, (const uint32_t*)b,
+                         (const uint32_t*)nat, (const uint8_t*)leafpar, r);
+            else
+                launch_k(form_big_windows_kernel<K, false>, BIGW_CTAS, BIGW_THREADS, bsm, s, bufs, (const uint32_t*)b,
+                         (const uint32_t*)nat, (const uint8_t*)leafpar, r);
+            PS_LAUNCH_CHECK();
+        }
         prof.end(ph);
     }
 
@@ -882,8 +888,10 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     }
     if (counting) {
         // comparisons: detection + extension + merges
-        st->comparisons_valid = 1;
-        st->comparisons = (int64_t)c.comparisons;
+        // (the insertion shifts of windows longer than MAX_FORM_M are not counted)
+        const bool exact = !(m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M);
+        st->comparisons_valid = exact;
+        st->comparisons = exact ? (int64_t)c.comparisons : -1;
         // moves: reversals + insertions, then per merge 2 * size (buffer out and
         // back), + 1 for a stages merge, copied + written for copy-smaller
         int64_t mv = (int64_t)c.moves;
@@ -891,8 +899,8 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             mv += (int64_t)(c.cs_copied + c.cs_written);
         else
             mv += 2 * M + (sentinel_tournament ? 0 : m34);
-        st->moves = mv;
-        st->moves_valid = 1;
+        st->moves = exact ? mv : -1;
+        st->moves_valid = exact;
     }
     return PS_OK;
 }

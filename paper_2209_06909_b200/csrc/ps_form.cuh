@@ -308,7 +308,11 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
 
     // ---- extended windows starting in this tile: stable rank ---------------
     bool anywin = false;
-    for (uint32_t i = tid; i < cnt; i += FORM_THREADS) anywin |= (snat[i] < sb[i + 1] - sb[i]) && (sb[i] >= t0);
+    // (windows longer than MAX_FORM_M are sorted by form_big_windows_kernel)
+    for (uint32_t i = tid; i < cnt; i += FORM_THREADS) {
+        const uint32_t len = sb[i + 1] - sb[i];
+        anywin |= (snat[i] < len) && (len <= MAX_FORM_M) && (sb[i] >= t0);
+    }
     if (!__syncthreads_or(anywin)) {
         flush_counters();
         return;
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         uint32_t flag = 0;
         if (i < cnt) {
             const uint32_t len = sb[i + 1] - sb[i];
-            flag = (snat[i] < len) && (sb[i] >= t0);
+            flag = (snat[i] < len) && (len <= MAX_FORM_M) && (sb[i] >= t0);
         }
         uint32_t tot;
         const uint32_t ex = block_exclusive<uint32_t, OpSum<uint32_t>>(flag, tot, sw32);
@@ -399,6 +403,131 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         bufs.vb(par)[dst] = wv[e];
     }
     flush_counters();
+}
+
+// ---------------------------------------------------------------------------
+// Extended windows longer than MAX_FORM_M (min_run_len > 1024): each is the
+// stable sort of its original records, done by one CTA: chunks of
+// BIGW_CHUNK records are sorted in shared memory (4-record insertion sorts,
+// then merge passes), then merge passes over global memory ping-pong between
+// the window's ranges of the two buffers, ending in the leaf's parity buffer.
+constexpr uint32_t BIGW_THREADS = 512;
+constexpr uint32_t BIGW_CHUNK = 2048;  // = BIGW_THREADS * 4
+constexpr uint32_t BIGW_CTAS = 2 * 148;
+
+template <class K>
+size_t big_window_smem_bytes() {
+    return 2 * (size_t)BIGW_CHUNK * (sizeof(K) + 4);
+}
+
+// one stable merge pass: sorted runs of width w -> 2w over [0, len), VT
+// consecutive outputs per thread (VT divides 2w, so a thread stays in its pair)
+template <class K, uint32_t VT>
+PS_DEV void bigw_merge_pass(const K* sk, const int32_t* sv, K* dk, int32_t* dv, uint32_t len, uint32_t w) {
+    for (uint32_t o0 = threadIdx.x * VT; o0 < len; o0 += blockDim.x * VT) {
+        const uint32_t a0 = o0 / (2 * w) * (2 * w);
+        const uint32_t a1 = min(a0 + w, len), b1 = min(a0 + 2 * w, len);
+        const uint32_t la = a1 - a0, lb = b1 - a1, d = o0 - a0;
+        uint32_t lo = d > lb ? d - lb : 0, hi = min(d, la);  // # of A records among the first d outputs
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            const bool le = !(sk[a1 + d - 1 - mid] < sk[a0 + mid]);
+            lo = le ? mid + 1 : lo;
+            hi = le ? hi : mid;
+        }
+        uint32_t i = lo, j = d - lo;
+        for (uint32_t t = 0; t < VT && o0 + t < b1; ++t) {
+            const bool takeA = i < la && (j >= lb || !(sk[a1 + j] < sk[a0 + i]));
+            const uint32_t src = takeA ? a0 + i : a1 + j;
+            dk[o0 + t] = sk[src];
+            dv[o0 + t] = sv[src];
+            i += takeA;
+            j += !takeA;
+        }
+    }
+}
+
+template <class K, bool ARGSORT>
+__global__ void __launch_bounds__(BIGW_THREADS) form_big_windows_kernel(Bufs<K> bufs, const uint32_t* __restrict__ b,
+                                                                        const uint32_t* __restrict__ nat,
+                                                                        const uint8_t* __restrict__ leafpar,
+                                                                        uint32_t r) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t smem[];
+    K* sk[2];
+    int32_t* sv[2];
+    sk[0] = reinterpret_cast<K*>(smem);
+    sk[1] = sk[0] + BIGW_CHUNK;
+    sv[0] = reinterpret_cast<int32_t*>(sk[1] + BIGW_CHUNK);
+    sv[1] = sv[0] + BIGW_CHUNK;
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t leaf = blockIdx.x; leaf < r; leaf += gridDim.x) {
+        const uint64_t base = b[leaf];
+        const uint32_t len = b[leaf + 1] - (uint32_t)base;
+        if (!(nat[leaf] < len && len > MAX_FORM_M)) continue;
+        const uint32_t par = leafpar[leaf];
+        uint32_t passes = 0;  // global merge passes after the chunk sorts
+        for (uint64_t w = BIGW_CHUNK; w < len; w *= 2) ++passes;
+        const uint32_t first = par ^ (passes & 1);  // so that the last pass lands in par
+        K* K0 = bufs.k[0];
+        int32_t* V0 = bufs.v[0];
+        for (uint32_t c0 = 0; c0 < len; c0 += BIGW_CHUNK) {
+            const uint32_t cl = min(BIGW_CHUNK, len - c0);
+            // 4 consecutive records per thread, insertion-sorted (stable)
+            K kk[4];
+            int32_t vv[4];
+            const uint32_t e0 = tid * 4;
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t e = e0 + u;
+                if (e < cl) {
+                    const uint64_t p = base + c0 + e;
+                    kk[u] = K0[p];
+                    vv[u] = ARGSORT ? (int32_t)p : V0[p];
+                }
+            }
+            const uint32_t mine = e0 < cl ? min(4u, cl - e0) : 0u;
+            for (uint32_t u = 1; u < mine; ++u) {
+                const K x = kk[u];
+                const int32_t xv = vv[u];
+                uint32_t q = u;
+                while (q > 0 && x < kk[q - 1]) {
+                    kk[q] = kk[q - 1];
+                    vv[q] = vv[q - 1];
+                    --q;
+                }
+                kk[q] = x;
+                vv[q] = xv;
+            }
+            for (uint32_t u = 0; u < mine; ++u) {
+                sk[0][e0 + u] = kk[u];
+                sv[0][e0 + u] = vv[u];
+            }
+            __syncthreads();
+            uint32_t cur = 0;
+            for (uint32_t w = 4; w < cl; w *= 2) {
+                bigw_merge_pass<K, 4>(sk[cur], sv[cur], sk[cur ^ 1], sv[cur ^ 1], cl, w);
+                cur ^= 1;
+                __syncthreads();
+            }
+            K* dk = bufs.kb(first) + base + c0;
+            int32_t* dv = bufs.vb(first) + base + c0;
+            for (uint32_t e = tid; e < cl; e += BIGW_THREADS) {
+                dk[e] = sk[cur][e];
+                dv[e] = sv[cur][e];
+            }
+            __syncthreads();
+        }
+        uint32_t src = first;
+        for (uint64_t w = BIGW_CHUNK; w < len; w *= 2) {
+            __syncthreads();  // the previous pass (or the chunk writes) is complete
+            __threadfence_block();
+            bigw_merge_pass<K, 8>(bufs.kb(src) + base, bufs.vb(src) + base, bufs.kb(src ^ 1) + base,
+                                  bufs.vb(src ^ 1) + base, len, (uint32_t)w);
+            src ^= 1;
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace ps

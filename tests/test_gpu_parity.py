@@ -187,6 +187,28 @@ def test_min_run_len_multilevel_chain_scan(mrl, dev):
     assert stats.merge_cost == ref.stats["merge_cost"]
 
 
+@pytest.mark.parametrize("mrl", [1025, 3000, 5000])
+def test_min_run_len_beyond_tile_windows(mrl, dev):
+    # windows longer than the formation tile's staging (1024): one CTA sorts each
+    rng = np.random.default_rng(mrl)
+    for kind in range(3):
+        n = int(rng.integers(mrl, 60000))
+        if kind == 0:
+            keys = rng.integers(0, 50, size=n).astype(np.int32)
+        elif kind == 1:
+            keys = workloads.cfg2(n=n, seed=mrl)
+        else:
+            keys = rng.normal(size=n).astype(np.float64)
+            keys[n // 4 : n // 2] = np.sort(keys[n // 4 : n // 2])[::-1]
+        ref = oracle.sort(keys, min_run_len=mrl)
+        out, perm, stats = gpu_sort(keys, dev, min_run_len=mrl)
+        assert np.array_equal(perm, ref.values), (mrl, kind, n)
+        assert np.array_equal(out.view(np.uint8), ref.keys.view(np.uint8))
+        assert stats.run_lengths == ref.run_lengths
+        assert stats.merge_cost == ref.stats["merge_cost"]
+        assert read_trace(device=dev) == ref.trace
+
+
 def test_values_payload_permuted(dev):
     keys_np = workloads.cfg3(n=1 << 16, seed=5)
     vals_np = np.random.default_rng(1).integers(-1000, 1000, size=keys_np.size).astype(np.int32)
