@@ -356,12 +356,14 @@ inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)std::max<uin
 // device), then one publish of the summary and the stage chunk offsets (the
 // host schedules the merges from them).  The publish is only enqueued here;
 // tree_wait() collects it, so the caller can queue leaf formation first.
-int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s, Pending& pend) {
+int finish_tree(uint8_t* ws, const Layout& L, TreeInfo& info, cudaStream_t s, Pending& pend, bool chunk_map = true) {
     Summary* sum = at<Summary>(ws, L.sum);
-    launch_k(tree_chunk_map_kernel, CHUNK_MAP_CTAS, 256, 0, s, (const Node*)at<Node>(ws, L.nodes), (const Summary*)sum,
-             (const uint32_t*)at<uint32_t>(ws, L.stage_chunk), (uint32_t)std::min<uint64_t>(L.chunks_max, 0xFFFFFFFFull),
-             at<uint32_t>(ws, L.chunk2node));
-    PS_LAUNCH_CHECK();
+    if (chunk_map) {  // (the multi-kernel path builds it in tree_chunks_kernel)
+        launch_k(tree_chunk_map_kernel, CHUNK_MAP_CTAS, 256, 0, s, (const Node*)at<Node>(ws, L.nodes),
+                 (const Summary*)sum, (const uint32_t*)at<uint32_t>(ws, L.stage_chunk),
+                 (uint32_t)std::min<uint64_t>(L.chunks_max, 0xFFFFFFFFull), at<uint32_t>(ws, L.chunk2node));
+        PS_LAUNCH_CHECK();
+    }
     return publish_begin(sum, sizeof(Summary), &info.s, at<uint32_t>(ws, L.stage_chunk), sizeof(info.stage_chunk),
                          info.stage_chunk, s, pend);
 }
@@ -489,12 +491,11 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist, hoff, (int64_t)NPOW * nblocks, false, true,
                                                    at<uint32_t>(ws, L.scantmp_u32), htot, s)));
-    launch_k(tree_level_offsets_kernel, 1, 128, 0, s, hoff, htot, nblocks, sum);
-    PS_LAUNCH_CHECK();
     launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
                                                             spine, nodes, sum);
     PS_LAUNCH_CHECK();
-    launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum, mt);
+    launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum, mt, (const uint32_t*)hoff,
+             (const uint32_t*)htot, nblocks);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan2<int32_t, OpSum<int32_t>>(Dd, Dd, Sd, Sd, (int64_t)r + 1, false, false,
@@ -502,15 +503,15 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     // node-indexed kernels run over the bound nmax and read the node count on the device
     const uint32_t nmax = r + MAX_SPINE;
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
-    launch_k(tree_stack_max_kernel, grid_for(r + 1, 256), 256, 0, s, Sd, r, sum, (uint32_t)stack_cap, Dd, leafpar);
-    PS_LAUNCH_CHECK();
     uint32_t* nch = at<uint32_t>(ws, L.nch);
     uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
     uint32_t* hist2 = at<uint32_t>(ws, L.hist2);
     uint32_t* hoff2 = at<uint32_t>(ws, L.hist2_off);
     uint32_t* htot2 = at<uint32_t>(ws, L.hist2_tot);
     const uint32_t nfb = (uint32_t)cdiv(nmax, FIN_THREADS);
-    launch_k(tree_nodes_finalize_kernel, nfb, FIN_THREADS, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, hist2, nfb);
+    static_assert(FIN_THREADS == 256, "finalize blocks also cover the r + 1 stack heights");
+    launch_k(tree_nodes_finalize_kernel, nfb, FIN_THREADS, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, hist2, nfb,
+             (const int32_t*)Sd, r, (uint32_t)stack_cap, leafpar);
     PS_LAUNCH_CHECK();
     // T6: regroup the nodes by merge stage
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist2, hoff2, (int64_t)NSTAGE * nfb, false, true,
@@ -521,10 +522,11 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nmax, false, true, at<uint32_t>(ws, L.scantmp_u32),
                                                    cb + nmax, s)));
-    launch_k(tree_copy_chunk_base_kernel, grid_for(nmax, 256), 256, 0, s, final_nodes, cb, nmax, (const Summary*)sum,
-             at<uint32_t>(ws, L.stage_chunk));
+    launch_k(tree_chunks_kernel, CHUNK_MAP_CTAS, 256, 0, s, final_nodes, (const uint32_t*)cb, nmax, sum,
+             at<uint32_t>(ws, L.stage_chunk), (uint32_t)std::min<uint64_t>(L.chunks_max, 0xFFFFFFFFull),
+             at<uint32_t>(ws, L.chunk2node));
     PS_LAUNCH_CHECK();
-    return finish_tree(ws, L, info, s, pend);
+    return finish_tree(ws, L, info, s, pend, false);
 }
 
 // Runs one batch of disjoint merge nodes [nlo, nhi) whose chunks are

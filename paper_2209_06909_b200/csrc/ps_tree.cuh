@@ -329,6 +329,9 @@ PS_DEV uint32_t range_min(const MinTree& t, uint32_t lo, uint32_t hi) {
     return m;
 }
 
+PS_DEV void tree_level_offsets_cta(const uint32_t* __restrict__ blockOff, const uint32_t* __restrict__ total,
+                                   uint32_t nblocks, Summary* sum);
+
 // Merge stage of a main-loop node: its power level, higher powers first.
 PS_DEV uint32_t main_stage(uint32_t power) { return NPOW - power; }
 
@@ -444,10 +447,15 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
     }
     sum->nspine_nodes = nn;
 }
+// (also the power-bucket offsets and nmain, from the scanned histograms)
 __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                                   uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
-                                  int32_t* __restrict__ Ddiff, Summary* sum, MinTree mt) {
+                                  int32_t* __restrict__ Ddiff, Summary* sum, MinTree mt,
+                                  const uint32_t* __restrict__ hoff, const uint32_t* __restrict__ htot,
+                                  uint32_t nblocks) {
     pdl_wait();
+    tree_level_offsets_cta(hoff, htot, nblocks, sum);
+    __syncthreads();
     tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum, mt);
 }
 
@@ -553,10 +561,28 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
     for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) hist[(uint64_t)t * nblocks + blk] = s_hh[t];
     __syncthreads();  // s_red / s_hh are reused by the next call
 }
+// (grid over nmax >= r + 1 threads: also the max stack height from the
+// stack-height prefix H and the leaf parities from the depths S)
 __global__ void __launch_bounds__(FIN_THREADS) tree_nodes_finalize_kernel(
     Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S, int slack_mode, uint32_t cap,
-    Summary* sum, uint32_t* __restrict__ hist, uint32_t nblocks) {
+    Summary* sum, uint32_t* __restrict__ hist, uint32_t nblocks, const int32_t* __restrict__ H, uint32_t r,
+    uint32_t stack_cap, uint8_t* __restrict__ leafpar) {
     pdl_wait();
+    {
+        const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        if (leafpar && j - 1 < r) {
+            const uint32_t jl = j - 1;
+            const int32_t a = jl == 0 ? 0 : S[jl];
+            const int32_t c = jl + 1 >= r ? 0 : S[jl + 1];
+            leafpar[jl] = (uint8_t)((a > c ? a : c) & 1);
+        }
+        int32_t v = (j < r) ? H[j] : 0;
+        for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
+        if (lane_id() == 0 && v > 0) {
+            atomicMax(&sum->max_stack, (uint32_t)v);
+            if ((uint32_t)v > stack_cap) atomicOr(&sum->err, ERR_STACK);
+        }
+    }
     tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, hist, nblocks);
 }
 
@@ -687,6 +713,32 @@ __global__ void tree_copy_chunk_base_kernel(Node* __restrict__ nodes, const uint
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < node_count(sum, nmax)) nodes[i].chunk_base = base[i];
     if (blockIdx.x == 0) tree_stage_chunks_cta(base, sum, nmax, stage_chunk);
+}
+
+// chunk_base into the nodes, the stage chunk offsets (block 0) and the chunk
+// -> node map (the last node whose chunk base is <= c, searched in cb), grid-
+// stride over CHUNK_MAP_CTAS CTAs; the counts are read on the device.
+__global__ void tree_chunks_kernel(Node* __restrict__ nodes, const uint32_t* __restrict__ cb, uint32_t nmax,
+                                   Summary* sum, uint32_t* __restrict__ stage_chunk, uint32_t chunks_max,
+                                   uint32_t* __restrict__ chunk2node) {
+    pdl_wait();
+    const uint32_t nn = node_count(sum, nmax);
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    for (uint32_t i = gt; i < nn; i += gs) nodes[i].chunk_base = cb[i];
+    if (blockIdx.x == 0) tree_stage_chunks_cta(cb, sum, nmax, stage_chunk);
+    const uint32_t total = cb[nn];
+    if (nn == 0 || total > chunks_max) return;  // (the host fails on the published total)
+    for (uint32_t c = gt; c < total; c += gs) {
+        uint32_t lo = 0, hi = nn;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cb[mid] <= c)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        chunk2node[c] = lo;
+    }
 }
 
 // nchunks per node, zero for the padding up to nmax (the scan runs over nmax)
