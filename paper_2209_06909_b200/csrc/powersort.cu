@@ -720,27 +720,37 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         launch_k(rd_tables_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
                                                    err);
         PS_LAUNCH_CHECK();
-        uint64_t span = GROUP;
-        std::vector<uint64_t> spans(L.tab_levels);
-        for (uint64_t l = 0; l < L.tab_levels; ++l) {
-            spans[l] = span;
-            if (l + 1 < L.tab_levels) {
-                launch_k(rd_compose_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
-                    at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
-                    at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
-                PS_LAUNCH_CHECK();
-                span *= TSCAN_FAN;
-            }
-        }
-        const uint64_t top = L.tab_levels - 1;
-        launch_k(rd_top_kernel, 1, 32, fan_smem, s, at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
-                                       (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
-        PS_LAUNCH_CHECK();
-        for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
-            launch_k(rd_down_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
-                at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
-                at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
+        const size_t c2smem = rd_chain2_smem((uint32_t)L.lvlP[0], (uint32_t)m);
+        if (L.tab_levels == 2 && c2smem <= 64 * 1024) {  // (bigger: one SM staging every table loses)
+            // two levels: compose, top and down in one CTA
+            PS_CUDA(cudaFuncSetAttribute(rd_chain2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem));
+            launch_k(rd_chain2_kernel, 1, (unsigned)(32 * cdiv(L.lvlP[0], TSCAN_FAN)), c2smem, s,
+                     (const uint64_t*)at<uint64_t>(ws, L.lvl_tab[0]), (uint32_t)L.lvlP[0], (const uint32_t*)Ft,
+                     (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[0]), b, sum, err);
             PS_LAUNCH_CHECK();
+        } else {
+            uint64_t span = GROUP;
+            std::vector<uint64_t> spans(L.tab_levels);
+            for (uint64_t l = 0; l < L.tab_levels; ++l) {
+                spans[l] = span;
+                if (l + 1 < L.tab_levels) {
+                    launch_k(rd_compose_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
+                        at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], span, Ft, (uint64_t)n, (uint32_t)m,
+                        at<uint64_t>(ws, L.lvl_tab[l + 1]), err);
+                    PS_LAUNCH_CHECK();
+                    span *= TSCAN_FAN;
+                }
+            }
+            const uint64_t top = L.tab_levels - 1;
+            launch_k(rd_top_kernel, 1, 32, fan_smem, s, at<uint64_t>(ws, L.lvl_tab[top]), (uint32_t)L.lvlP[top], spans[top], Ft,
+                                           (uint64_t)n, (uint32_t)m, at<uint64_t>(ws, L.lvl_ent[top]), b, sum, err);
+            PS_LAUNCH_CHECK();
+            for (int64_t l = (int64_t)top - 1; l >= 0; --l) {
+                launch_k(rd_down_kernel, (unsigned)L.lvlP[l + 1], 32, fan_smem, s, 
+                    at<uint64_t>(ws, L.lvl_tab[l]), (uint32_t)L.lvlP[l], spans[l], Ft, (uint64_t)n, (uint32_t)m,
+                    at<uint64_t>(ws, L.lvl_ent[l + 1]), at<uint64_t>(ws, L.lvl_ent[l]), err);
+                PS_LAUNCH_CHECK();
+            }
         }
         launch_k(rd_emit_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
                  at<uint64_t>(ws, L.lvl_ent[0]), b, nat, at<uint32_t>(ws, L.tile_first), err);

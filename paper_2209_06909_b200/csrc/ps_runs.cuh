@@ -372,6 +372,83 @@ __global__ void __launch_bounds__(32) rd_down_kernel(const uint64_t* __restrict_
     }
 }
 
+// Two-level chain scan in one CTA (TSCAN_FAN < P <= TSCAN_FAN^2 group tables):
+// warp w composes group tables [32w, 32w+32) into a level-1 table, thread 0
+// walks the level-1 tables from (0, 0) (the top: run count, b[r] = n), then
+// lane 0 of each warp walks its group tables from its level-1 entry and writes
+// the group entries (the compose / top / down kernels' work, one launch).
+// Dynamic smem: (nw + 1) * TSCAN_FAN * (m+1) uint64, nw = ceil(P / TSCAN_FAN).
+__global__ void __launch_bounds__(1024) rd_chain2_kernel(const uint64_t* __restrict__ in, uint32_t P,
+                                                         const uint32_t* __restrict__ Ft, uint64_t n, uint32_t m,
+                                                         uint64_t* __restrict__ entries, uint32_t* __restrict__ b,
+                                                         Summary* sum, uint32_t* err) {
+    pdl_wait();
+    extern __shared__ uint64_t sm[];
+    __shared__ uint64_t s_F[TSCAN_FAN * TSCAN_FAN];
+    __shared__ uint64_t s_up[TSCAN_FAN];
+    const uint32_t M1 = m + 1, lane = lane_id(), w = warp_id(), nw = blockDim.x / 32;
+    uint64_t* s_tab = sm + (uint64_t)w * TSCAN_FAN * M1;
+    uint64_t* s_l1 = sm + (uint64_t)nw * TSCAN_FAN * M1;
+    const uint32_t j0 = w * TSCAN_FAN;
+    const uint32_t cnt = P > j0 ? min(TSCAN_FAN, P - j0) : 0u;
+    const uint64_t* src = in + (uint64_t)j0 * M1;
+    for (uint32_t base = 0; base < cnt * M1; base += 8 * 32) {  // 8 independent loads per lane
+        uint64_t v[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            v[u] = i < cnt * M1 ? src[i] : 0;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t i = base + u * 32 + lane;
+            if (i < cnt * M1) s_tab[i] = v[u];
+        }
+    }
+    for (uint32_t k = lane; k < cnt; k += 32) s_F[j0 + k] = Ft[((uint64_t)(j0 + k) * GROUP) / TILE];
+    __syncwarp();
+    const uint64_t t0 = (uint64_t)j0 * GROUP;
+    if (cnt) {
+        for (uint32_t e = lane; e < M1; e += 32) {
+            uint64_t x = e < m ? t0 + e : s_F[j0];
+            uint64_t c = 0;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const uint64_t tk = t0 + (uint64_t)k * GROUP;
+                tab_apply(s_tab + k * M1, tk, tk + GROUP, s_F[j0 + k], m, n, x, c, err);
+            }
+            s_l1[w * M1 + e] = pack_xc((uint32_t)x, (uint32_t)c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t P1 = (P + TSCAN_FAN - 1) / TSCAN_FAN;
+        const uint64_t span1 = (uint64_t)GROUP * TSCAN_FAN;
+        uint64_t x = 0, c = 0;
+        for (uint32_t j = 0; j < P1; ++j) {
+            s_up[j] = pack_xc((uint32_t)x, (uint32_t)c);
+            const uint64_t tj = (uint64_t)j * span1;
+            tab_apply(s_l1 + j * M1, tj, tj + span1, s_F[j * TSCAN_FAN], m, n, x, c, err);
+        }
+        if (x != n) atomicOr(err, ERR_CHAIN);
+        sum->r = (uint32_t)c;
+        b[c] = (uint32_t)n;
+    }
+    __syncthreads();
+    if (lane == 0 && cnt) {
+        const uint64_t v = s_up[w];
+        uint64_t x = unpack_x(v), c = unpack_c(v);
+        for (uint32_t k = 0; k < cnt; ++k) {
+            entries[j0 + k] = pack_xc((uint32_t)x, (uint32_t)c);
+            const uint64_t tk = t0 + (uint64_t)k * GROUP;
+            tab_apply(s_tab + k * M1, tk, tk + GROUP, s_F[j0 + k], m, n, x, c, err);
+        }
+    }
+}
+inline size_t rd_chain2_smem(uint32_t P, uint32_t m) {
+    const size_t nw = (P + TSCAN_FAN - 1) / TSCAN_FAN;
+    return (nw + 1) * TSCAN_FAN * (size_t)(m + 1) * 8;
+}
+
 // ---------------------------------------------------------------------------
 // RD2c: emit the run boundaries b[c] and natural lengths nat[c].
 // Dynamic smem: TILES_PER_GROUP * (m+1) uint64 (the group's tile tables).
