@@ -389,7 +389,9 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     // P over [0, padded): r + 1 boundaries and 0xFF up to the next multiple of 32
     const uint32_t padded = (uint32_t)align_up((uint64_t)r + 1, 32);
     static const bool no_small_tree = getenv("PS_NO_SMALL_TREE") != nullptr;  // A/B: multi-kernel path
-    if (r <= TREE_SMALL_R && !no_small_tree) {
+    // A/B: PS_TREE_SMALL_R=x moves the one-CTA / multi-kernel crossover
+    static const uint32_t small_r = getenv("PS_TREE_SMALL_R") ? (uint32_t)atoi(getenv("PS_TREE_SMALL_R")) : TREE_SMALL_R;
+    if (r <= small_r && !no_small_tree) {
         // the whole build in one CTA (tree_small_kernel), then one publish
         TreeSmallArgs a;
         memset(&a, 0, sizeof(a));
@@ -794,8 +796,8 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     bufs.k[1] = at<K>(ws, L.k1);
     bufs.v[1] = at<int32_t>(ws, L.v1);
     {
-        const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M));
-        const unsigned grid = grid_for((uint64_t)n, FORM_TILE);
+        const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M), net_windows(m, counting));
+        const unsigned grid = grid_for((uint64_t)n, (uint64_t)FORM_TILE * FORM_TPC);
         static_assert(FORM_TILE == TILE, "leaf formation tiles are run detection's chain tiles");
         // per-tile first leaf, written by rd_emit_kernel (tiled detector only)
         const uint32_t* tile_first = m <= MAX_M_TILED ? at<uint32_t>(ws, L.tile_first) : nullptr;
@@ -812,6 +814,28 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                      ty, (uint32_t)m, tile_first, counting ? sum : nullptr);
         }
         PS_LAUNCH_CHECK();
+        if (net_windows(m, counting)) {
+            // extended windows: a register sorting network per window (ps_form.cuh)
+            const unsigned wg = grid_for(r, FORM_THREADS);  // a warp per 32 leaves
+            auto go = [&](auto kern, size_t wsm) -> int {
+                PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+                launch_k(kern, wg, FORM_THREADS, wsm, s, bufs, (const uint32_t*)b, (const uint32_t*)nat,
+                         (const uint8_t*)leafpar, r);
+                return PS_OK;
+            };
+            if (argsort) {
+                if (m <= 8) go(form_windows_kernel<K, 8, true>, form_windows_smem<K, 8>());
+                else if (m <= 16) go(form_windows_kernel<K, 16, true>, form_windows_smem<K, 16>());
+                else if (m <= 24) go(form_windows_kernel<K, 24, true>, form_windows_smem<K, 24>());
+                else go(form_windows_kernel<K, 32, true>, form_windows_smem<K, 32>());
+            } else {
+                if (m <= 8) go(form_windows_kernel<K, 8, false>, form_windows_smem<K, 8>());
+                else if (m <= 16) go(form_windows_kernel<K, 16, false>, form_windows_smem<K, 16>());
+                else if (m <= 24) go(form_windows_kernel<K, 24, false>, form_windows_smem<K, 24>());
+                else go(form_windows_kernel<K, 32, false>, form_windows_smem<K, 32>());
+            }
+            PS_LAUNCH_CHECK();
+        }
         if (m > MAX_FORM_M && (uint64_t)n > MAX_FORM_M) {
             // windows longer than a tile's staging capacity: one CTA per window
             const size_t bsm = big_window_smem_bytes<K>();

@@ -18,7 +18,12 @@ namespace ps {
 
 constexpr uint32_t FORM_TILE = 2048;
 constexpr uint32_t FORM_THREADS = 256;
+constexpr uint32_t FORM_TPC = 4;  // detection tiles per leaf-formation CTA
 constexpr uint32_t MAX_FORM_M = 1024;
+// PS_NO_NET=1 (A/B builds): short windows take the rank loop too
+#ifndef PS_NO_NET
+#define PS_NO_NET 0
+#endif
 
 template <class K>
 struct Bufs {
@@ -34,11 +39,12 @@ struct Bufs {
 //   wlist[FORM_TILE+1] u32 (window leaf ids), woff[FORM_TILE+2] u32,
 //   wk[FORM_TILE+MAX_M] K, wv[...] i32
 template <class K>
-size_t form_smem_bytes(uint32_t m) {
+size_t form_smem_bytes(uint32_t m, bool net) {
     size_t s = 0;
     s += (FORM_TILE + 2) * 4;
     s += (FORM_TILE + 1) * 4;
     s += ((FORM_TILE + 1) + 15) / 16 * 16;
+    if (net) return s;  // windows go to form_windows_kernel: no staging
     s += (FORM_TILE + 1) * 4;
     s += (FORM_TILE + 2) * 4;
     s = (s + 15) / 16 * 16;
@@ -47,6 +53,179 @@ size_t form_smem_bytes(uint32_t m) {
     s += cap * 4;
     s += (cap * 2 + 15) / 16 * 16;  // window index of every staged element
     return s;
+}
+
+// ---------------------------------------------------------------------------
+// Short extended windows (min_run_len <= 32): one thread sorts a whole window
+// in registers with Batcher's odd-even merge-sort network over (key, offset)
+// pairs.  The offset breaks key ties, so the network's output is the stable
+// sort of the window's original elements -- the leaf extend_run's insertion
+// sort produces (runs.py:50-82).  Padding lanes (offset >= len)
+// hold the largest key and a larger offset, so they sort past the window.
+template <int S>
+struct OddEvenNet {
+    int cnt = 0;
+    int a[S * 8] = {};
+    int b[S * 8] = {};
+    constexpr OddEvenNet() {
+        for (int p = 1; p < S; p <<= 1)
+            for (int k = p; k >= 1; k >>= 1)
+                for (int j = k % p; j + k < S; j += 2 * k)
+                    for (int i = 0; i < k && i + j + k < S; ++i)
+                        if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+                            a[cnt] = i + j;
+                            b[cnt] = i + j + k;
+                            ++cnt;
+                        }
+    }
+};
+static_assert(OddEvenNet<32>().cnt == 191, "Batcher network size for 32 inputs");
+
+// The power-of-two network restricted to L real inputs: wires L.. carry the
+// padding (larger than every input), so a comparator whose upper wire is
+// padding is a no-op and one whose lower wire is padding is a fixed swap --
+// a relabelling of physical registers.  Only real-vs-real comparators remain
+// (L = 24: 132 of 191); sorted wire j ends in physical register out[j].
+template <int L>
+struct PrunedNet {
+    static constexpr int P = L <= 8 ? 8 : L <= 16 ? 16 : 32;
+    int cnt = 0;
+    int a[P * 8] = {};
+    int b[P * 8] = {};
+    int out[P] = {};
+    constexpr PrunedNet() {
+        const OddEvenNet<P> net{};
+        int map[P] = {};
+        bool real[P] = {};
+        for (int w = 0; w < P; ++w) {
+            map[w] = w;
+            real[w] = w < L;
+        }
+        for (int c = 0; c < net.cnt; ++c) {
+            const int x = net.a[c], y = net.b[c];
+            if (!real[y]) continue;
+            if (!real[x]) {
+                const int t = map[x];
+                map[x] = map[y];
+                map[y] = t;
+                real[x] = true;
+                real[y] = false;
+                continue;
+            }
+            a[cnt] = map[x];
+            b[cnt] = map[y];
+            ++cnt;
+        }
+        for (int w = 0; w < P; ++w) out[w] = map[w];
+    }
+};
+static_assert(OddEvenNet<16>().cnt == 63, "Batcher network size for 16 inputs");
+
+template <class K>
+PS_DEV K key_pad();
+template <>
+PS_DEV int32_t key_pad<int32_t>() { return 0x7FFFFFFF; }
+template <>
+PS_DEV int64_t key_pad<int64_t>() { return 0x7FFFFFFFFFFFFFFFll; }
+template <>
+PS_DEV float key_pad<float>() { return __int_as_float(0x7F800000); }
+template <>
+PS_DEV double key_pad<double>() { return __longlong_as_double(0x7FF0000000000000ll); }
+
+// Sorts k[0..S) (padding past the window) carrying the original offsets o[].
+template <class K, int S>
+PS_DEV void net_sort(K (&k)[S], uint32_t (&o)[S]) {
+    constexpr PrunedNet<S> net{};
+#pragma unroll
+    for (int c = 0; c < net.cnt; ++c) {
+        const int x = net.a[c], y = net.b[c];
+        const K kx = k[x], ky = k[y];
+        const uint32_t ox = o[x], oy = o[y];
+        const bool sw = (ky < kx) || (!(kx < ky) && oy < ox);
+        k[x] = sw ? ky : kx;
+        k[y] = sw ? kx : ky;
+        o[x] = sw ? oy : ox;
+        o[y] = sw ? ox : oy;
+    }
+}
+
+// Extended windows go to form_windows_kernel when they fit a network and no
+// CountingOrder counters are requested (those need the rank loop's shifts).
+__host__ __device__ inline bool net_windows(uint64_t m, bool counting) { return !PS_NO_NET && m <= 32 && !counting; }
+
+template <class K, int S>
+constexpr size_t form_windows_smem() {
+    return (size_t)(FORM_THREADS / 32) * 32 * (S + 1) * (sizeof(K) + 4);
+}
+
+// A warp per 32 consecutive leaves; each extended window (natural length <
+// leaf length) is sorted by its lane's network, natural leaves are left to
+// form_leaves_kernel.  Windows move through a per-warp shared-memory
+// transpose (row w = window w, stride S+1 elements: conflict-free lane rows),
+// so global loads and stores are one coalesced instruction per window.
+template <class K, int S, bool ARGSORT>
+__global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs, const uint32_t* __restrict__ b,
+                                                                    const uint32_t* __restrict__ nat,
+                                                                    const uint8_t* __restrict__ leafpar, uint32_t r) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr uint32_t RW = S + 1;
+    const uint32_t lane = lane_id(), warp = warp_id();
+    K* sk = reinterpret_cast<K*>(smem) + (size_t)warp * 32 * RW;
+    uint32_t* so = reinterpret_cast<uint32_t*>(reinterpret_cast<K*>(smem) + (size_t)(FORM_THREADS / 32) * 32 * RW) +
+                   (size_t)warp * 32 * RW;
+    const uint32_t i = (blockIdx.x * (FORM_THREADS / 32) + warp) * 32 + lane;
+    uint32_t b0 = 0, len = 0, par = 0;
+    if (i < r) {
+        b0 = b[i];
+        const uint32_t l = b[i + 1] - b0;
+        if (nat[i] < l) {
+            len = l;
+            par = leafpar[i];
+        }
+    }
+    if (__ballot_sync(PS_FULL, len != 0) == 0) return;
+    const K* K0 = bufs.k[0];
+    const int32_t* V0 = bufs.v[0];
+#pragma unroll 8
+    for (uint32_t w = 0; w < 32; ++w) {  // window w -> row w
+        const uint32_t bw = __shfl_sync(PS_FULL, b0, w), lw = __shfl_sync(PS_FULL, len, w);
+        if (lane < lw) sk[w * RW + lane] = K0[bw + lane];
+    }
+    __syncwarp();
+    K k[S];
+    uint32_t o[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        o[j] = (uint32_t)j;
+        k[j] = (uint32_t)j < len ? sk[lane * RW + j] : key_pad<K>();
+    }
+    net_sort<K, S>(k, o);
+    constexpr PrunedNet<S> net{};
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        sk[lane * RW + j] = k[net.out[j]];
+        so[lane * RW + j] = o[net.out[j]];
+    }
+    __syncwarp();
+    if (!ARGSORT) {  // gather every payload before any store: parity-0 leaves are formed in place
+#pragma unroll 8
+        for (uint32_t w = 0; w < 32; ++w) {
+            const uint32_t bw = __shfl_sync(PS_FULL, b0, w), lw = __shfl_sync(PS_FULL, len, w);
+            if (lane < lw) so[w * RW + lane] = (uint32_t)V0[bw + so[w * RW + lane]];
+        }
+        __syncwarp();
+    }
+#pragma unroll 8
+    for (uint32_t w = 0; w < 32; ++w) {
+        const uint32_t bw = __shfl_sync(PS_FULL, b0, w), lw = __shfl_sync(PS_FULL, len, w);
+        const uint32_t pw = __shfl_sync(PS_FULL, par, w);
+        if (lane < lw) {
+            const uint32_t ov = so[w * RW + lane];
+            bufs.kb(pw)[bw + lane] = sk[w * RW + lane];
+            bufs.vb(pw)[bw + lane] = ARGSORT ? (int32_t)(bw + ov) : (int32_t)ov;
+        }
+    }
 }
 
 // Largest j in [0, r) with b[j] <= x (b ascending, b[0] = 0 <= x), by a warp
@@ -70,7 +249,7 @@ PS_DEV uint32_t warp_last_le(const uint32_t* __restrict__ b, uint32_t r, uint32_
 }
 
 template <class K, bool ARGSORT>
-__global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs, uint64_t n,
+__global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bufs, uint64_t n,
                                                                    const uint32_t* __restrict__ b,
                                                                    const uint32_t* __restrict__ nat,
                                                                    const uint8_t* __restrict__ leafpar, uint32_t r,
@@ -94,31 +273,55 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
 
     K* const K0 = bufs.k[0];
     int32_t* const V0 = bufs.v[0];
-    const uint64_t t0 = (uint64_t)blockIdx.x * FORM_TILE;
-    const uint64_t t1 = min(t0 + FORM_TILE, n);
     const uint32_t tid = threadIdx.x;
-    if (tile_first) {
-        // leaves covering t0 and t1-1 from the per-tile table of run detection
-        if (tid == 0) {
-            const uint32_t lo = tile_first[blockIdx.x];
-            uint32_t lo2 = r - 1;
-            if (t1 < n) {
-                const uint32_t nx = tile_first[blockIdx.x + 1];  // covers t1
-                lo2 = b[nx] == t1 ? nx - 1 : nx;
+    // leaves covering positions lo_pos and hi_pos - 1 (tiles [tb, te) of run detection)
+    auto locate = [&](uint32_t tb, uint32_t te, uint64_t lo_pos, uint64_t hi_pos) {
+        __syncthreads();  // the previous tile's shared arrays are consumed
+        if (tile_first) {
+            if (tid == 0) {
+                const uint32_t lo = tile_first[tb];
+                uint32_t lo2 = r - 1;
+                if (hi_pos < n) {
+                    const uint32_t nx = tile_first[te];  // covers hi_pos
+                    lo2 = b[nx] == hi_pos ? nx - 1 : nx;
+                }
+                s_first = lo;
+                s_cnt = lo2 - lo + 1;
             }
-            s_first = lo;
-            s_cnt = lo2 - lo + 1;
+        } else if (tid < 32) {
+            // last leaf with b <= lo_pos and last leaf with b <= hi_pos-1: 32-ary warp searches
+            const uint32_t lo = warp_last_le(b, r, (uint32_t)lo_pos);
+            const uint32_t lo2 = warp_last_le(b, r, (uint32_t)(hi_pos - 1));
+            if (tid == 0) {
+                s_first = lo;
+                s_cnt = lo2 - lo + 1;
+            }
         }
-    } else if (tid < 32) {
-        // last leaf with b <= t0 and last leaf with b <= t1-1: 32-ary warp searches
-        const uint32_t lo = warp_last_le(b, r, (uint32_t)t0);
-        const uint32_t lo2 = warp_last_le(b, r, (uint32_t)(t1 - 1));
-        if (tid == 0) {
-            s_first = lo;
-            s_cnt = lo2 - lo + 1;
+        __syncthreads();
+    };
+    // A CTA covers FORM_TPC detection tiles.  When few (long) leaves cover the
+    // whole span and windows are left to form_windows_kernel, it is formed in
+    // one pass; otherwise tile by tile (the shared arrays hold one tile).
+    const bool net = net_windows(m, counters != nullptr);
+    const uint32_t ntiles = (uint32_t)((n + FORM_TILE - 1) / FORM_TILE);
+    const uint32_t tb = blockIdx.x * FORM_TPC, te = min(tb + FORM_TPC, ntiles);
+    const uint64_t span0 = (uint64_t)tb * FORM_TILE, span1 = min((uint64_t)te * FORM_TILE, n);
+    locate(tb, te, span0, span1);
+    const bool whole = net && s_cnt <= 16;
+    if (net && !whole) {
+        // spans made only of extended windows (form_windows_kernel's) have nothing to do
+        bool anynat = false;
+        for (uint32_t i = tid; i < s_cnt; i += FORM_THREADS) {
+            const uint32_t j = s_first + i;
+            anynat |= nat[j] >= b[j + 1] - b[j];
         }
+        if (!__syncthreads_or(anynat)) return;
     }
-    __syncthreads();
+    for (uint32_t tl = tb; tl < te; ++tl) {
+    const uint64_t t0 = whole ? span0 : (uint64_t)tl * FORM_TILE;
+    const uint64_t t1 = whole ? span1 : min(t0 + FORM_TILE, n);
+    if (!whole && te - tb > 1) locate(tl, tl + 1, t0, t1);
+    [&]() {
     const uint32_t first = s_first, cnt = s_cnt;
     for (uint32_t i = tid; i <= cnt; i += FORM_THREADS) sb[i] = b[first + i];
     for (uint32_t i = tid; i < cnt; i += FORM_THREADS) {
@@ -307,6 +510,10 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
     }
 
     // ---- extended windows starting in this tile: stable rank ---------------
+    if (net_windows(m, counters != nullptr)) {  // form_windows_kernel sorts them
+        flush_counters();
+        return;
+    }
     bool anywin = false;
     // (windows longer than MAX_FORM_M are sorted by form_big_windows_kernel)
     for (uint32_t i = tid; i < cnt; i += FORM_THREADS) {
@@ -403,6 +610,9 @@ __global__ void __launch_bounds__(FORM_THREADS) form_leaves_kernel(Bufs<K> bufs,
         bufs.vb(par)[dst] = wv[e];
     }
     flush_counters();
+    }();
+    if (whole) break;
+    }
 }
 
 // ---------------------------------------------------------------------------
