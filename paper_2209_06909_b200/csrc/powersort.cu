@@ -245,7 +245,7 @@ struct Layout {
     // offsets
     uint64_t header, sum, k1, v1, ty, cg, Fg, Ft, tile_tab, lvl_tab[16], lvl_ent[16], b, nat, leafpar, P,
         minlev[8], Rle, Lle, Dd, Sd, hist, hist_off, hist_tot, spine, nodes, nch, chunk_base, stage_chunk, chunk2node, cuts, bars, tile_first,
-        nodes_tmp, hist2, hist2_off, hist2_tot,
+        pdelta,
         scantmp_u32, scantmp_i32, total;
 };
 
@@ -322,10 +322,7 @@ Layout make_layout(uint64_t n, uint64_t kb, uint64_t m, bool sort_buffers, uint6
     L.hist_tot = take(16);
     L.spine = take(MAX_SPINE * 4);
     L.nodes = take((L.rmax + MAX_SPINE) * sizeof(Node));
-    L.nodes_tmp = take((L.rmax + MAX_SPINE) * sizeof(Node));
-    L.hist2 = take(((uint64_t)NSTAGE * cdiv(L.rmax + MAX_SPINE, FIN_THREADS) + 2) * 4);
-    L.hist2_off = take(((uint64_t)NSTAGE * cdiv(L.rmax + MAX_SPINE, FIN_THREADS) + 2) * 4);
-    L.hist2_tot = take(16);
+    L.pdelta = take(NPOW * 4);
     L.nch = take((L.rmax + MAX_SPINE + 2) * 4);
     L.chunk_base = take((L.rmax + MAX_SPINE + 2) * 4);
     L.stage_chunk = take((NSTAGE + 2) * 4);
@@ -429,11 +426,7 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
         a.htot = at<uint32_t>(ws, L.hist_tot);
         a.spine = at<uint32_t>(ws, L.spine);
         a.nodes = at<Node>(ws, L.nodes);
-        a.nodes_tmp = at<Node>(ws, L.nodes_tmp);
-        a.hist2 = at<uint32_t>(ws, L.hist2);
-        a.hoff2 = at<uint32_t>(ws, L.hist2_off);
-        a.htot2 = at<uint32_t>(ws, L.hist2_tot);
-        a.nblocks_f = (uint32_t)cdiv(r + MAX_SPINE, CLS_THREADS);
+        a.pdelta = at<int32_t>(ws, L.pdelta);
         a.leafpar = leafpar;
         a.nmax = r + MAX_SPINE;
         a.nch = at<uint32_t>(ws, L.nch);
@@ -487,17 +480,18 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     uint32_t* hoff = at<uint32_t>(ws, L.hist_off);
     uint32_t* htot = at<uint32_t>(ws, L.hist_tot);
     uint32_t* spine = at<uint32_t>(ws, L.spine);
-    Node* nodes = at<Node>(ws, L.nodes_tmp);  // regrouped by height into L.nodes at the end
+    Node* nodes = at<Node>(ws, L.nodes);  // written at their merge-stage slots (tree_spine_cta)
+    int32_t* pdelta = at<int32_t>(ws, L.pdelta);
     launch_k(tree_classify_kernel<0>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, hist, nullptr, Dd, Sd,
-                                                            spine, nodes, sum);
+                                                            spine, nodes, sum, (const int32_t*)pdelta);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist, hoff, (int64_t)NPOW * nblocks, false, true,
                                                    at<uint32_t>(ws, L.scantmp_u32), htot, s)));
-    launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
-                                                            spine, nodes, sum);
-    PS_LAUNCH_CHECK();
     launch_k(tree_spine_kernel, 1, 256, 0, s, b, r, k, strict, spine, nodes, Dd, sum, mt, (const uint32_t*)hoff,
-             (const uint32_t*)htot, nblocks);
+             (const uint32_t*)htot, nblocks, pdelta);
+    PS_LAUNCH_CHECK();
+    launch_k(tree_classify_kernel<1>, nblocks, CLS_THREADS, 0, s, P, Rle, Lle, b, r, k, nblocks, nullptr, hoff, Dd, Sd,
+                                                            spine, nodes, sum, (const int32_t*)pdelta);
     PS_LAUNCH_CHECK();
     // depth (inclusive prefix of Dd) and stack height (inclusive prefix of Sd)
     PS_CUDA((device_scan2<int32_t, OpSum<int32_t>>(Dd, Dd, Sd, Sd, (int64_t)r + 1, false, false,
@@ -507,24 +501,14 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     const int64_t stack_cap = (int64_t)ps_run_stack_capacity(k, (int64_t)n);
     uint32_t* nch = at<uint32_t>(ws, L.nch);
     uint32_t* cb = at<uint32_t>(ws, L.chunk_base);
-    uint32_t* hist2 = at<uint32_t>(ws, L.hist2);
-    uint32_t* hoff2 = at<uint32_t>(ws, L.hist2_off);
-    uint32_t* htot2 = at<uint32_t>(ws, L.hist2_tot);
     const uint32_t nfb = (uint32_t)cdiv(nmax, FIN_THREADS);
     static_assert(FIN_THREADS == 256, "finalize blocks also cover the r + 1 stack heights");
-    launch_k(tree_nodes_finalize_kernel, nfb, FIN_THREADS, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, hist2, nfb,
+    launch_k(tree_nodes_finalize_kernel, nfb, FIN_THREADS, 0, s, nodes, nmax, Dd, slack_mode, cap, sum, nch,
              (const int32_t*)Sd, r, (uint32_t)stack_cap, leafpar);
-    PS_LAUNCH_CHECK();
-    // T6: regroup the nodes by merge stage
-    PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(hist2, hoff2, (int64_t)NSTAGE * nfb, false, true,
-                                                   at<uint32_t>(ws, L.scantmp_u32), htot2, s)));
-    Node* final_nodes = at<Node>(ws, L.nodes);
-    launch_k(tree_stage_scatter_kernel, nfb, FIN_THREADS, 0, s, (const Node*)nodes, final_nodes, nmax, nfb,
-             (const uint32_t*)hoff2, (const uint32_t*)htot2, sum, nch);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpSum<uint32_t>>(nch, cb, nmax, false, true, at<uint32_t>(ws, L.scantmp_u32),
                                                    cb + nmax, s)));
-    launch_k(tree_chunks_kernel, CHUNK_MAP_CTAS, 256, 0, s, final_nodes, (const uint32_t*)cb, nmax, sum,
+    launch_k(tree_chunks_kernel, CHUNK_MAP_CTAS, 256, 0, s, nodes, (const uint32_t*)cb, nmax, sum,
              at<uint32_t>(ws, L.stage_chunk), (uint32_t)std::min<uint64_t>(L.chunks_max, 0xFFFFFFFFull),
              at<uint32_t>(ws, L.chunk2node));
     PS_LAUNCH_CHECK();

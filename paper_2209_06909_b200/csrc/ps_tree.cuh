@@ -233,7 +233,7 @@ PS_DEV void tree_classify_block(uint32_t vb, const uint8_t* __restrict__ P, cons
                                 uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
                                 const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff,
                                 int32_t* __restrict__ Sdiff, uint32_t* __restrict__ spine_list,
-                                Node* __restrict__ nodes, Summary* sum) {
+                                Node* __restrict__ nodes, Summary* sum, const int32_t* __restrict__ pdelta) {
     __shared__ uint32_t whist[32][NPOW];
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     for (uint32_t i = tid; i < 32 * NPOW; i += blockDim.x) (&whist[0][0])[i] = 0;
@@ -281,7 +281,8 @@ PS_DEV void tree_classify_block(uint32_t vb, const uint8_t* __restrict__ P, cons
             }
         }
     } else if (c.head) {
-        const uint32_t slot = blockOff[(uint64_t)p * nblocks + vb] + whist[warp][p] + rank;
+        // power-bucket position, moved to the node's merge stage (tree_spine_cta)
+        const uint32_t slot = blockOff[(uint64_t)p * nblocks + vb] + whist[warp][p] + rank + pdelta[p];
         Node nd;
         const uint32_t arity = c.nmem + 1;
         for (uint32_t i = 0; i < 5; ++i) nd.pos[i] = i <= arity ? b[c.bidx[i]] : 0u;
@@ -303,10 +304,10 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_classify_kernel(
     const uint8_t* __restrict__ P, const uint32_t* __restrict__ Rle, const uint32_t* __restrict__ Lle,
     const uint32_t* __restrict__ b, uint32_t r, uint32_t k, uint32_t nblocks, uint32_t* __restrict__ blockHist,
     const uint32_t* __restrict__ blockOff, int32_t* __restrict__ Ddiff, int32_t* __restrict__ Sdiff,
-    uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum) {
+    uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, Summary* sum, const int32_t* __restrict__ pdelta) {
     pdl_wait();
     tree_classify_block<PASS>(blockIdx.x, P, Rle, Lle, b, r, k, nblocks, blockHist, blockOff, Ddiff, Sdiff, spine_list,
-                              nodes, sum);
+                              nodes, sum, pdelta);
 }
 
 // T4: the spine and _merge_down (policy.py:146-175): staged by the CTA, replayed by one thread.
@@ -335,9 +336,18 @@ PS_DEV void tree_level_offsets_cta(const uint32_t* __restrict__ blockOff, const 
 // Merge stage of a main-loop node: its power level, higher powers first.
 PS_DEV uint32_t main_stage(uint32_t power) { return NPOW - power; }
 
+// T6: the merge schedule is fixed here.  Stage h holds the main nodes of power
+// NPOW - h (one contiguous power bucket, position order) followed by the
+// merge_down nodes of stage h.  Writes the stage offsets into level_off (the
+// power offsets it replaces are read first), each power bucket's shift
+// pdelta[p] for classification pass 1, and the merge_down nodes at their
+// final slots; so no regrouping pass is needed.
 PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                            uint32_t* __restrict__ spine_list, Node* __restrict__ nodes, int32_t* __restrict__ Ddiff,
-                           Summary* sum, const MinTree& mt) {
+                           Summary* sum, const MinTree& mt, int32_t* __restrict__ pdelta) {
+    __shared__ Node s_sn[MAX_SPINE];
+    __shared__ uint32_t s_nn;
+    __shared__ uint32_t s_cnt[NSTAGE + 1], s_soff[NSTAGE + 1], s_pow[NPOW + 1];
     // the stack entries are staged and sorted by the CTA, their run starts are
     // gathered in parallel; one thread then replays _merge_down from shared memory
     __shared__ uint32_t s_list[MAX_SPINE];
@@ -369,9 +379,9 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
         s_key[h] = (uint8_t)(lo < hi ? main_stage(range_min(mt, lo, hi)) : 0u);
     }
     if (t == 0) s_br = b[r];
+    for (uint32_t p = t; p <= NPOW; p += blockDim.x) s_pow[p] = sum->level_off[p];
     __syncthreads();
-    if (t != 0) return;
-    const uint32_t nmain = sum->nmain;
+    if (t == 0) {
     uint32_t nn = 0;
     uint32_t height = H;
     uint32_t run_begin = H + 1;  // index into s_beta / s_bval
@@ -398,7 +408,7 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
         nd.chunk_base = 0;
         nd.nchunks = 0;
         nd.order = nn;
-        nodes[nmain + nn] = nd;
+        s_sn[nn] = nd;
         nn++;
         atomicAdd(&Ddiff[s_beta[hh[0]] + 1], 1);
         atomicAdd(&Ddiff[r], -1);
@@ -443,20 +453,50 @@ PS_DEV void tree_spine_cta(const uint32_t* __restrict__ b, uint32_t r, uint32_t 
     // less per step), so the chain shares the last main-loop launches
     for (uint32_t i = 0; i < nn; ++i) {
         const uint32_t key = cur_key - (nn - 1 - i);
-        nodes[nmain + i].flags = (uint8_t)(1u | (key << 1));
+        s_sn[i].flags = (uint8_t)(1u | (key << 1));
     }
     sum->nspine_nodes = nn;
+    s_nn = nn;
+    }
+    __syncthreads();
+    const uint32_t nn = s_nn;
+    // nodes per stage: the power bucket NPOW - h plus the merge_down nodes of stage h
+    for (uint32_t h = t; h <= NSTAGE; h += blockDim.x) {
+        uint32_t c = 0;
+        if (h >= 1 && h < NPOW) c = s_pow[NPOW - h + 1] - s_pow[NPOW - h];
+        for (uint32_t i = 0; i < nn; ++i) c += (uint32_t)(s_sn[i].flags >> 1) == h;
+        s_cnt[h] = c;
+    }
+    __syncthreads();
+    if (t == 0) {
+        uint32_t acc = 0;
+        for (uint32_t h = 0; h <= NSTAGE; ++h) {
+            s_soff[h] = acc;
+            acc += s_cnt[h];
+        }
+    }
+    __syncthreads();
+    for (uint32_t h = t; h <= NSTAGE; h += blockDim.x) sum->level_off[h] = s_soff[h];
+    for (uint32_t p = t; p < NPOW; p += blockDim.x)
+        pdelta[p] = p >= 1 ? (int32_t)s_soff[NPOW - p] - (int32_t)s_pow[p] : 0;
+    for (uint32_t i = t; i < nn; i += blockDim.x) {
+        const uint32_t h = s_sn[i].flags >> 1;
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < i; ++j) rank += (uint32_t)(s_sn[j].flags >> 1) == h;
+        const uint32_t pm = (h >= 1 && h < NPOW) ? s_pow[NPOW - h + 1] - s_pow[NPOW - h] : 0u;
+        nodes[s_soff[h] + pm + rank] = s_sn[i];
+    }
 }
 // (also the power-bucket offsets and nmain, from the scanned histograms)
 __global__ void tree_spine_kernel(const uint32_t* __restrict__ b, uint32_t r, uint32_t k, int strict,
                                   uint32_t* __restrict__ spine_list, Node* __restrict__ nodes,
                                   int32_t* __restrict__ Ddiff, Summary* sum, MinTree mt,
                                   const uint32_t* __restrict__ hoff, const uint32_t* __restrict__ htot,
-                                  uint32_t nblocks) {
+                                  uint32_t nblocks, int32_t* __restrict__ pdelta) {
     pdl_wait();
     tree_level_offsets_cta(hoff, htot, nblocks, sum);
     __syncthreads();
-    tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum, mt);
+    tree_spine_cta(b, r, k, strict, spine_list, nodes, Ddiff, sum, mt, pdelta);
 }
 
 // T5: per-node depth/parity, chunk counts and merge statistics; leaf parity.
@@ -482,12 +522,18 @@ constexpr uint32_t FIN_THREADS = 256;
 // per-stage statistics; the block's stage histogram (hist[h * nblocks + blk])
 // for the stable regrouping.
 PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S,
-                                int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ hist,
-                                uint32_t nblocks) {
+                                int slack_mode, uint32_t cap, Summary* sum, uint32_t* __restrict__ nch) {
     __shared__ uint32_t s_hh[NSTAGE];
+    __shared__ unsigned long long s_cost[NSTAGE];
+    __shared__ uint32_t s_small[NSTAGE], s_smax[NSTAGE];
     const uint32_t nnodes = node_count(sum, nmax);
     const uint32_t i = i0 + threadIdx.x;
-    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) s_hh[t] = 0;
+    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) {
+        s_hh[t] = 0;
+        s_cost[t] = 0;
+        s_small[t] = 0;
+        s_smax[t] = 0;
+    }
     __syncthreads();
     unsigned long long cost = 0, m2 = 0, m3 = 0, m4 = 0, slack = 0, copied = 0;
     uint32_t key = 0xFFFFFFFFu, sz = 0, sm = 0;
@@ -501,6 +547,7 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         if (!(nd.flags & 1)) nd.flags = (uint8_t)(main_stage(nd.power) << 1);  // (spine: set by tree_spine_cta)
         const uint32_t stage = nd.flags >> 1;
         nodes[i] = nd;
+        nch[i] = nd.nchunks;
         atomicAdd(&s_hh[stage], 1u);
         cost = size;
         if (w == 2) copied = min(nd.pos[1] - nd.pos[0], nd.pos[2] - nd.pos[1]);  // copy-smaller's buffer
@@ -512,17 +559,22 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
         key = stage;
         sz = size;
         sm = size <= SMALL_KERNEL_MAX;
+    } else if (i < nmax) {
+        nch[i] = 0;  // (the chunk scan runs over nmax)
     }
-    // per-stage cost / small counts: one atomic per distinct stage per warp
+    // per-stage cost / small counts: shared-memory atomics per distinct stage
+    // per warp, then one global atomic per stage per block (the nodes arrive
+    // grouped by power, so most blocks touch one or two stages; per-warp global
+    // atomics on a handful of addresses serialised in L2)
     {
         const uint32_t grp = __match_any_sync(PS_FULL, key);
         const uint32_t gsz = __reduce_add_sync(grp, sz), gsm = __reduce_add_sync(grp, sm);
         const uint32_t gmx = __reduce_max_sync(grp, sm ? sz : 0u);
         if (key != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(grp) - 1)) {
-            atomicAdd(&sum->level_cost[key], (unsigned long long)gsz);
+            atomicAdd(&s_cost[key], (unsigned long long)gsz);
             if (gsm) {
-                atomicAdd(&sum->level_small[key], gsm);
-                atomicMax(&sum->level_small_max[key], gmx);
+                atomicAdd(&s_small[key], gsm);
+                atomicMax(&s_smax[key], gmx);
             }
         }
     }
@@ -557,15 +609,22 @@ PS_DEV void tree_finalize_block(uint32_t i0, Node* __restrict__ nodes, uint32_t 
             atomicAdd(dst, t);
         }
     }
-    const uint32_t blk = i0 / blockDim.x;
-    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) hist[(uint64_t)t * nblocks + blk] = s_hh[t];
+    for (uint32_t t = threadIdx.x; t < NSTAGE; t += blockDim.x) {
+        if (s_hh[t]) {
+            atomicAdd(&sum->level_cost[t], s_cost[t]);
+            if (s_small[t]) {
+                atomicAdd(&sum->level_small[t], s_small[t]);
+                atomicMax(&sum->level_small_max[t], s_smax[t]);
+            }
+        }
+    }
     __syncthreads();  // s_red / s_hh are reused by the next call
 }
 // (grid over nmax >= r + 1 threads: also the max stack height from the
 // stack-height prefix H and the leaf parities from the depths S)
 __global__ void __launch_bounds__(FIN_THREADS) tree_nodes_finalize_kernel(
     Node* __restrict__ nodes, uint32_t nmax, const int32_t* __restrict__ S, int slack_mode, uint32_t cap,
-    Summary* sum, uint32_t* __restrict__ hist, uint32_t nblocks, const int32_t* __restrict__ H, uint32_t r,
+    Summary* sum, uint32_t* __restrict__ nch, const int32_t* __restrict__ H, uint32_t r,
     uint32_t stack_cap, uint8_t* __restrict__ leafpar) {
     pdl_wait();
     {
@@ -583,62 +642,7 @@ __global__ void __launch_bounds__(FIN_THREADS) tree_nodes_finalize_kernel(
             if ((uint32_t)v > stack_cap) atomicOr(&sum->err, ERR_STACK);
         }
     }
-    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, hist, nblocks);
-}
-
-// T6: stable scatter of block blk's nodes into their stage buckets (hoff =
-// exclusive scan of the block histograms), with the chunk counts in the new
-// order (zero padding up to nmax for the chunk scan).  Block 0 also writes the
-// stage offsets level_off[h] (the host's schedule).
-PS_DEV void tree_stage_scatter_block(uint32_t i0, const Node* __restrict__ src, Node* __restrict__ dst,
-                                      uint32_t nmax, uint32_t nblocks, const uint32_t* __restrict__ hoff,
-                                      const uint32_t* __restrict__ htot, Summary* sum,
-                                      uint32_t* __restrict__ nch_out, uint32_t (*whist)[NSTAGE]) {
-    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-    const uint32_t nnodes = node_count(sum, nmax);
-    const uint32_t blk = i0 / blockDim.x;
-    for (uint32_t t = tid; t < 32 * NSTAGE; t += blockDim.x) (&whist[0][0])[t] = 0;
-    __syncthreads();
-    const uint32_t i = i0 + tid;
-    const bool valid = i < nnodes;
-    Node nd;
-    uint32_t h = 0xFFFFFFFFu;
-    if (valid) {
-        nd = src[i];
-        h = nd.flags >> 1;
-    }
-    const uint32_t peers = __match_any_sync(PS_FULL, h);
-    const uint32_t rank = __popc(peers & ((1u << lane) - 1));
-    if (valid && rank == 0) whist[warp][h] = __popc(peers);
-    __syncthreads();
-    if (tid < NSTAGE) {
-        uint32_t acc = 0;
-        for (uint32_t w = 0; w < 32; ++w) {
-            const uint32_t x = whist[w][tid];
-            whist[w][tid] = acc;
-            acc += x;
-        }
-    }
-    __syncthreads();
-    if (valid) {
-        const uint32_t slot = hoff[(uint64_t)h * nblocks + blk] + whist[warp][h] + rank;
-        dst[slot] = nd;
-        nch_out[slot] = nd.nchunks;
-    }
-    if (i >= nnodes && i < nmax) nch_out[i] = 0;
-    if (blk == 0) {
-        if (tid < NSTAGE) sum->level_off[tid] = hoff[(uint64_t)tid * nblocks];
-        if (tid == 0) sum->level_off[NSTAGE] = *htot;
-    }
-    __syncthreads();  // whist is reused by the next call
-}
-__global__ void __launch_bounds__(FIN_THREADS) tree_stage_scatter_kernel(
-    const Node* __restrict__ src, Node* __restrict__ dst, uint32_t nmax, uint32_t nblocks,
-    const uint32_t* __restrict__ hoff, const uint32_t* __restrict__ htot, Summary* sum,
-    uint32_t* __restrict__ nch_out) {
-    pdl_wait();
-    __shared__ uint32_t whist[32][NSTAGE];
-    tree_stage_scatter_block(blockIdx.x * blockDim.x, src, dst, nmax, nblocks, hoff, htot, sum, nch_out, whist);
+    tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, nch);
 }
 
 // chunk_base at the node indices the host schedules stages by: the stage
@@ -808,18 +812,12 @@ struct TreeSmallArgs {
     uint32_t* cb;
     uint32_t* stage_chunk;
     Summary* sum;
-    // T6: classification writes nodes_tmp, the stage scatter writes nodes
-    Node* nodes_tmp;
-    uint32_t* hist2;
-    uint32_t* hoff2;
-    uint32_t* htot2;
-    uint32_t nblocks_f;                     // finalize blocks of blockDim nodes
+    int32_t* pdelta;                        // per-power shift to the merge-stage order
 };
 
 __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a) {
     pdl_wait();
-    __shared__ uint32_t s_items[CLS_THREADS * 4];
-    static_assert(CLS_THREADS * 4 >= 32 * NSTAGE, "s_items doubles as the stage scatter's histogram");
+    __shared__ uint32_t s_items[CLS_THREADS * 2];  // (static shared memory: the spine stages its nodes too)
     __shared__ uint32_t s_sw[32];
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     uint32_t* err = &a.sum->err;
@@ -842,19 +840,19 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a
     __syncthreads();
     for (uint32_t vb = 0; vb < a.nblocks; ++vb)
         tree_classify_block<0>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, a.hist, nullptr, a.Dd, a.Sd, a.spine,
-                               a.nodes_tmp, a.sum);
-    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.hist, a.hoff, (int64_t)NPOW * a.nblocks, false, true, a.htot, s_items,
+                               a.nodes, a.sum, a.pdelta);
+    cta_scan<uint32_t, OpSum<uint32_t>, 2>(a.hist, a.hoff, (int64_t)NPOW * a.nblocks, false, true, a.htot, s_items,
                                            s_sw);
     tree_level_offsets_cta(a.hoff, a.htot, a.nblocks, a.sum);
     __syncthreads();
+    tree_spine_cta(a.b, a.r, a.k, a.strict, a.spine, a.nodes, a.Dd, a.sum, a.mt, a.pdelta);
+    __syncthreads();
     for (uint32_t vb = 0; vb < a.nblocks; ++vb)
         tree_classify_block<1>(vb, a.P, a.Rle, a.Lle, a.b, a.r, a.k, a.nblocks, nullptr, a.hoff, a.Dd, a.Sd, a.spine,
-                               a.nodes_tmp, a.sum);
-    tree_spine_cta(a.b, a.r, a.k, a.strict, a.spine, a.nodes_tmp, a.Dd, a.sum, a.mt);
-    __syncthreads();
-    cta_scan<int32_t, OpSum<int32_t>, 4>(a.Dd, a.Dd, (int64_t)a.r + 1, false, false, nullptr,
+                               a.nodes, a.sum, a.pdelta);
+    cta_scan<int32_t, OpSum<int32_t>, 2>(a.Dd, a.Dd, (int64_t)a.r + 1, false, false, nullptr,
                                          reinterpret_cast<int32_t*>(s_items), reinterpret_cast<int32_t*>(s_sw));
-    cta_scan<int32_t, OpSum<int32_t>, 4>(a.Sd, a.Sd, (int64_t)a.r + 1, false, false, nullptr,
+    cta_scan<int32_t, OpSum<int32_t>, 2>(a.Sd, a.Sd, (int64_t)a.r + 1, false, false, nullptr,
                                          reinterpret_cast<int32_t*>(s_items), reinterpret_cast<int32_t*>(s_sw));
     for (uint32_t j0 = 0; j0 < a.r; j0 += nt) {  // max stack height
         const uint32_t j = j0 + tid + 1;
@@ -874,15 +872,9 @@ __global__ void __launch_bounds__(CLS_THREADS) tree_small_kernel(TreeSmallArgs a
     }
     __syncthreads();
     for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
-        tree_finalize_block(i0, a.nodes_tmp, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum, a.hist2, a.nblocks_f);
+        tree_finalize_block(i0, a.nodes, a.nmax, a.Dd, a.slack_mode, a.cap, a.sum, a.nch);
     __syncthreads();
-    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.hist2, a.hoff2, (int64_t)NSTAGE * a.nblocks_f, false, true, a.htot2,
-                                           s_items, s_sw);
-    for (uint32_t i0 = 0; i0 < a.nmax; i0 += nt)
-        tree_stage_scatter_block(i0, a.nodes_tmp, a.nodes, a.nmax, a.nblocks_f, a.hoff2, a.htot2, a.sum, a.nch,
-                                 reinterpret_cast<uint32_t(*)[NSTAGE]>(s_items));  // (32 x NSTAGE words)
-    __syncthreads();
-    cta_scan<uint32_t, OpSum<uint32_t>, 4>(a.nch, a.cb, a.nmax, false, true, a.cb + a.nmax, s_items, s_sw);
+    cta_scan<uint32_t, OpSum<uint32_t>, 2>(a.nch, a.cb, a.nmax, false, true, a.cb + a.nmax, s_items, s_sw);
     {
         const uint32_t nn = node_count(a.sum, a.nmax);
         for (uint32_t i = tid; i < nn; i += nt) a.nodes[i].chunk_base = a.cb[i];
