@@ -143,6 +143,36 @@ struct ChainView {
     }
 };
 
+// Chain walk from x (absolute, in the group) while x < lim, in 32-bit offsets
+// from G.  For 3 <= m <= 32 a step whose natural run is shorter than m costs
+// one funnel shift of two change words (next = x + m, E = the first change);
+// other steps go through ChainView::next.  visit(x, e) is called per node.
+template <class F>
+PS_DEV uint64_t chain_walk(const ChainView& cv, uint64_t x, uint64_t lim, F&& visit) {
+    const uint64_t G = cv.G;
+    const uint32_t m = (uint32_t)cv.m;
+    const uint32_t n_o = (uint32_t)min(cv.n - G, (uint64_t)0xFFFFFFFFu);
+    const uint32_t lim_o = (uint32_t)(lim - G);
+    const bool fast = m >= 3 && m <= 32;
+    const uint32_t mask = fast ? (1u << (m - 1)) - 1u : 0u;
+    uint32_t xo = (uint32_t)(x - G);
+    while (xo < lim_o) {
+        const uint32_t off2 = xo + 2, w = off2 >> 5;
+        const uint32_t win = __funnelshift_r(cv.chg[w], cv.chg[w + 1], off2 & 31) & mask;
+        if (win && xo + 1 < n_o) {
+            visit(G + xo, G + off2 + (uint32_t)(__ffs(win) - 1));
+            xo = min(xo + m, n_o);
+        } else {
+            uint64_t e;
+            const uint64_t nx = cv.next(G + xo, &e);
+            visit(G + xo, e);
+            if (nx - G >= (uint64_t)lim_o) return nx;
+            xo = (uint32_t)(nx - G);
+        }
+    }
+    return G + xo;
+}
+
 // Build chg / nzn in shared memory for group g (all threads of the CTA).
 PS_DEV void build_chain_view(const uint32_t* __restrict__ ty, uint64_t n, uint32_t g, uint32_t ngroups,
                              const uint32_t* __restrict__ Fg, uint32_t* s_chg, uint16_t* s_nzn, ChainView& cv,
@@ -163,6 +193,7 @@ PS_DEV void build_chain_view(const uint32_t* __restrict__ ty, uint64_t n, uint32
         if (w == 0) chg &= ~1u;
         s_chg[w] = chg;
     }
+    if (threadIdx.x == 0) s_chg[GROUP_WORDS + 1] = 0;  // (chain_walk's window past the group)
     __syncthreads();
     // nzn: suffix "first nonzero word" -- each thread owns 2 words of 0..511,
     // word 512 handled by all (cheap), then a block suffix-min over threads.
@@ -228,7 +259,7 @@ __global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restri
                                                         uint64_t* __restrict__ tile_tab, uint32_t* __restrict__ Ft,
                                                         uint64_t* __restrict__ group_tab, uint32_t* err) {
     pdl_wait();
-    __shared__ uint32_t s_chg[GROUP_WORDS + 1];
+    __shared__ uint32_t s_chg[GROUP_WORDS + 2];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
     __shared__ uint64_t s_Ft[TILES_PER_GROUP];
     extern __shared__ uint64_t s_tab[];  // [TILES_PER_GROUP][m+1]
@@ -245,11 +276,8 @@ __global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restri
     if (lane == 0) s_Ft[w] = F_t;
     for (uint32_t e = lane; e < M1; e += 32) {
         uint64_t x = e < m ? t + e : F_t;
-        uint64_t cnt = 0;
-        while (x < lim) {
-            cnt++;
-            x = cv.next(x);
-        }
+        uint32_t cnt = 0;
+        if (x < lim) x = chain_walk(cv, x, lim, [&](uint64_t, uint64_t) { cnt++; });
         s_tab[w * M1 + e] = pack_xc((uint32_t)x, (uint32_t)cnt);
     }
     __syncthreads();
@@ -460,7 +488,7 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
                                                       uint32_t* __restrict__ b, uint32_t* __restrict__ nat,
                                                       uint32_t* __restrict__ tile_first, uint32_t* err) {
     pdl_wait();
-    __shared__ uint32_t s_chg[GROUP_WORDS + 1];
+    __shared__ uint32_t s_chg[GROUP_WORDS + 2];
     __shared__ uint16_t s_nzn[GROUP_WORDS + 2];
     __shared__ uint64_t s_entry[TILES_PER_GROUP];
     __shared__ uint64_t s_F[TILES_PER_GROUP];
@@ -483,22 +511,22 @@ __global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict
         }
     }
     __syncthreads();
-    const uint32_t w = warp_id();
-    if (lane_id() != 0) return;
+    // tile w is walked by lane w of warp 0 (one warp issues all eight walks)
+    const uint32_t w = threadIdx.x;
+    if (w >= TILES_PER_GROUP) return;
     const uint64_t t = cv.G + (uint64_t)w * TILE;
     const uint64_t lim = min(t + TILE, n);
     const uint64_t v = s_entry[w];
-    uint64_t x = unpack_x(v), c = unpack_c(v);
+    uint64_t x = unpack_x(v);
+    uint32_t c = unpack_c(v);
     // the run covering the tile's first position (leaf formation's tile = TILE)
     if (t < n) tile_first[tile0 + w] = (uint32_t)(x == t ? c : c - 1);
-    while (x < lim) {
-        uint64_t e;
-        const uint64_t nx = cv.next(x, &e);
-        b[c] = (uint32_t)x;
-        nat[c] = (uint32_t)(e - x);
-        c++;
-        x = nx;
-    }
+    if (x < lim)
+        chain_walk(cv, x, lim, [&](uint64_t p, uint64_t e) {
+            b[c] = (uint32_t)p;
+            nat[c] = (uint32_t)(e - p);
+            c++;
+        });
 }
 
 // ---------------------------------------------------------------------------

@@ -635,11 +635,18 @@ __global__ void __launch_bounds__(FIN_THREADS) tree_nodes_finalize_kernel(
             const int32_t c = jl + 1 >= r ? 0 : S[jl + 1];
             leafpar[jl] = (uint8_t)((a > c ? a : c) & 1);
         }
+        // block maximum, one atomic per block (per-warp atomics on one address serialise)
+        __shared__ int32_t s_hmax[FIN_THREADS / 32];
         int32_t v = (j < r) ? H[j] : 0;
         for (int d = 16; d; d >>= 1) v = max(v, __shfl_xor_sync(PS_FULL, v, d));
-        if (lane_id() == 0 && v > 0) {
-            atomicMax(&sum->max_stack, (uint32_t)v);
-            if ((uint32_t)v > stack_cap) atomicOr(&sum->err, ERR_STACK);
+        if (lane_id() == 0) s_hmax[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (uint32_t w = 1; w < FIN_THREADS / 32; ++w) v = max(v, s_hmax[w]);
+            if (v > 0) {
+                atomicMax(&sum->max_stack, (uint32_t)v);
+                if ((uint32_t)v > stack_cap) atomicOr(&sum->err, ERR_STACK);
+            }
         }
     }
     tree_finalize_block(blockIdx.x * blockDim.x, nodes, nmax, S, slack_mode, cap, sum, nch);
