@@ -688,7 +688,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
 
     // ---- N1 pass 1: run detection ------------------------------------------
     const int ph_rd = prof.begin(0, -1, 0, 0, n * (int64_t)sizeof(K));
-    launch_k(rd_types_kernel<K>, ngroups, 256, 0, s, keys, (uint64_t)n, ty, cg);
+    launch_k(rd_types_kernel<K>, ngroups, RD_THREADS, 0, s, keys, (uint64_t)n, ty, cg);
     PS_LAUNCH_CHECK();
     PS_CUDA((device_scan<uint32_t, OpMin<uint32_t>>(cg, Fg, ngroups, true, false, at<uint32_t>(ws, L.scantmp_u32),
                                                    nullptr, s)));
@@ -703,11 +703,14 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             PS_CUDA(cudaFuncSetAttribute(rd_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
             PS_CUDA(cudaFuncSetAttribute(rd_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fan_smem));
         }
-        launch_k(rd_tables_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
+        PS_CUDA(cudaFuncSetAttribute(rd_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PS_CUDA(cudaFuncSetAttribute(rd_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        launch_k(rd_tables_kernel, ngroups, RD_THREADS, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft, gtab,
                                                    err);
         PS_LAUNCH_CHECK();
         const size_t c2smem = rd_chain2_smem((uint32_t)L.lvlP[0], (uint32_t)m);
-        if (L.tab_levels == 2 && c2smem <= 64 * 1024) {  // (bigger: one SM staging every table loses)
+        static const size_t c2max = getenv("PS_CHAIN2_MAX") ? (size_t)atoll(getenv("PS_CHAIN2_MAX")) : 64 * 1024;
+        if (L.tab_levels == 2 && c2smem <= c2max) {  // (bigger: one SM staging every table loses)
             // two levels: compose, top and down in one CTA
             PS_CUDA(cudaFuncSetAttribute(rd_chain2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem));
             launch_k(rd_chain2_kernel, 1, (unsigned)(32 * cdiv(L.lvlP[0], TSCAN_FAN)), c2smem, s,
@@ -738,7 +741,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                 PS_LAUNCH_CHECK();
             }
         }
-        launch_k(rd_emit_kernel, ngroups, 256, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
+        launch_k(rd_emit_kernel, ngroups, RD_THREADS, smem, s, ty, (uint64_t)n, (uint32_t)m, Fg, ngroups, tile_tab, Ft,
                  at<uint64_t>(ws, L.lvl_ent[0]), b, nat, at<uint32_t>(ws, L.tile_first), err);
         PS_LAUNCH_CHECK();
     } else {

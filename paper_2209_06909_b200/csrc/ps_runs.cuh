@@ -36,11 +36,11 @@ PS_DEV uint32_t range_mask(uint64_t q0, uint64_t lo, uint64_t hi) {
 // (G, G+GROUP] (2 <= q <= n-1), INF if none.  One CTA per group; each warp
 // streams 1024 keys per round with coalesced loads, ballots give the words.
 template <class K>
-__global__ void __launch_bounds__(256) rd_types_kernel(const K* __restrict__ a, uint64_t n,
+__global__ void __launch_bounds__(RD_THREADS) rd_types_kernel(const K* __restrict__ a, uint64_t n,
                                                        uint32_t* __restrict__ ty, uint32_t* __restrict__ cg) {
     pdl_wait();
     __shared__ uint32_t sw[GROUP_WORDS];
-    __shared__ uint32_t smin[8];
+    __shared__ uint32_t smin[TILES_PER_GROUP];
     const uint32_t g = blockIdx.x;
     const uint64_t G = (uint64_t)g * GROUP;
     const uint32_t lane = lane_id(), warp = warp_id();
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) rd_types_kernel(const K* __restrict__ a, 
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t m = INF32;
-        for (int i = 0; i < 8; ++i) m = min(m, smin[i]);
+        for (uint32_t i = 0; i < TILES_PER_GROUP; ++i) m = min(m, smin[i]);
         cg[g] = m;
     }
 }
@@ -198,7 +198,8 @@ PS_DEV void build_chain_view(const uint32_t* __restrict__ ty, uint64_t n, uint32
     // nzn: suffix "first nonzero word" -- each thread owns 2 words of 0..511,
     // word 512 handled by all (cheap), then a block suffix-min over threads.
     __shared__ uint32_t s_red[32];
-    const uint32_t t = threadIdx.x;  // blockDim.x == 256
+    const uint32_t t = threadIdx.x;  // blockDim.x == GROUP_WORDS / 2
+    static_assert(RD_THREADS * 2 == GROUP_WORDS, "two change words per thread");
     const uint32_t w0 = 2 * t, w1 = 2 * t + 1;
     const uint32_t NONE = 0xFFFFu;
     uint32_t v0 = s_chg[w0] ? w0 : NONE;
@@ -216,7 +217,7 @@ PS_DEV void build_chain_view(const uint32_t* __restrict__ ty, uint64_t n, uint32
     if (lane == 0) s_red[warp] = x;
     __syncthreads();
     uint32_t after_warp = vlast;
-    for (uint32_t ww = warp + 1; ww < 8; ++ww) after_warp = min(after_warp, s_red[ww]);
+    for (uint32_t ww = warp + 1; ww < TILES_PER_GROUP; ++ww) after_warp = min(after_warp, s_red[ww]);
     uint32_t excl = __shfl_down_sync(PS_FULL, x, 1);
     if (lane == 31) excl = NONE;
     excl = min(excl, after_warp);
@@ -254,7 +255,7 @@ PS_DEV void tab_apply(const uint64_t* tab, uint64_t t, uint64_t tnext, uint64_t 
 // RD2a: per-tile transfer tables (one warp per tile, lanes over the m+1
 // candidates) and their composition into one table per group.
 // Dynamic smem: TILES_PER_GROUP * (m+1) uint64.
-__global__ void __launch_bounds__(256) rd_tables_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
+__global__ void __launch_bounds__(RD_THREADS) rd_tables_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
                                                         const uint32_t* __restrict__ Fg, uint32_t ngroups,
                                                         uint64_t* __restrict__ tile_tab, uint32_t* __restrict__ Ft,
                                                         uint64_t* __restrict__ group_tab, uint32_t* err) {
@@ -480,7 +481,7 @@ inline size_t rd_chain2_smem(uint32_t P, uint32_t m) {
 // ---------------------------------------------------------------------------
 // RD2c: emit the run boundaries b[c] and natural lengths nat[c].
 // Dynamic smem: TILES_PER_GROUP * (m+1) uint64 (the group's tile tables).
-__global__ void __launch_bounds__(256) rd_emit_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
+__global__ void __launch_bounds__(RD_THREADS) rd_emit_kernel(const uint32_t* __restrict__ ty, uint64_t n, uint32_t m,
                                                       const uint32_t* __restrict__ Fg, uint32_t ngroups,
                                                       const uint64_t* __restrict__ tile_tab,
                                                       const uint32_t* __restrict__ Ft,

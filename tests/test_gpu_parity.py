@@ -279,3 +279,34 @@ def test_float_signed_zero_and_ties(dev):
     out, perm, stats = gpu_sort(keys, dev)
     assert np.array_equal(perm, ref.values)
     assert np.array_equal(out.view(np.uint32), ref.keys.view(np.uint32))
+
+
+@pytest.mark.parametrize("name,n,mrl", [
+    ("cfg1", 1 << 14, 24),    # r ~ 680: one-CTA tree, arrays in global memory
+    ("cfg1", 1 << 17, 24),    # r ~ 5.5K: one-CTA tree, arrays in shared memory
+    ("cfg4", 1 << 18, 24),    # r ~ 5.5K with the long ascending half
+    ("cfg1", 1 << 18, 24),    # r ~ 11K: multi-kernel tree
+    ("cfg1", 1 << 16, 8),     # network windows of 8
+    ("cfg1", 1 << 16, 13),    # network windows of 16 (padded)
+    ("cfg1", 1 << 16, 30),    # network windows of 32 (padded)
+    ("cfg4", 1 << 16, 3),     # shortest fast-step windows
+])
+@pytest.mark.parametrize("dtype", ["int32", "float64"])
+def test_tree_paths_and_windows(name, n, mrl, dtype, dev):
+    keys = workloads.generate(name, n=n, seed=5)
+    if dtype == "float64":
+        keys = (keys.astype(np.float64) / 7.0).astype(np.float64)
+    ref = oracle.sort(keys, k=4, variant="4way", min_run_len=mrl)
+    out, perm, stats = gpu_sort(keys, dev, k=4, variant="4way", min_run_len=mrl)
+    assert np.array_equal(perm, ref.values)
+    assert np.array_equal(out.view(np.uint8), ref.keys.view(np.uint8))
+    for f in POLICY_FIELDS + COUNTER_FIELDS:
+        assert getattr(stats, f) == ref.stats[f], f
+    assert stats.run_lengths == ref.run_lengths
+    assert read_trace(device=dev) == ref.trace
+    # a values payload through the network windows and the in-place leaves
+    vals = torch.arange(n, dtype=torch.int32, device=dev) * 3 + 1
+    kt = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
+    stable_sort_with(kt, SortConfig(min_run_len=mrl), values=vals)
+    torch.cuda.synchronize()
+    assert np.array_equal(vals.cpu().numpy(), ref.values * 3 + 1)
