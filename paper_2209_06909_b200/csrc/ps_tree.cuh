@@ -95,7 +95,7 @@ struct MinTree {
 // bit i set iff arr[grp*32 + i] <= v
 PS_DEV uint32_t group_le_mask(const uint8_t* arr, uint32_t grp, uint32_t v) {
     const uint4* p = reinterpret_cast<const uint4*>(arr + (uint64_t)grp * 32);
-    const uint4 a = p[0], c = p[1];  // (generic loads: the one-CTA build keeps the tree in shared memory)
+    const uint4 a = __ldg(p), c = __ldg(p + 1);
     const uint32_t vv = v * 0x01010101u;
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
     uint32_t mask = 0;
