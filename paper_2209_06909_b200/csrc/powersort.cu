@@ -515,6 +515,9 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     return finish_tree(ws, L, info, s, pend, false);
 }
 
+// stages with at least this many cuts use the thin partition kernel
+constexpr uint32_t THIN_CUTS = 12000;
+
 // Runs one batch of disjoint merge nodes [nlo, nhi) whose chunks are
 // [c0, c1): small nodes by warps, big ones by partition + the TMA pipeline.
 template <class K>
@@ -587,8 +590,15 @@ struct MergeRunner {
                     bar = bars + bar_next++;  // partition fused into the pipe launch
                 } else {
                     const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
-                    launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1,
-                             cuts);
+                    // many cuts: three lanes per cut (fewer DRAM sectors); else a warp per cut
+                    static const uint32_t thin_min =
+                        getenv("PS_THIN_CUTS") ? (uint32_t)atoi(getenv("PS_THIN_CUTS")) : THIN_CUTS;
+                    if (c1 - c0 >= thin_min)
+                        launch_k(merge_partition_thin_kernel<K>, grid_for(c1 - c0, 80), 256, 0, s, bufs, nodes, c2n,
+                                 c0, c1, cuts);
+                    else
+                        launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1,
+                                 cuts);
                     PS_LAUNCH_CHECK();
                     if (prof) prof->end(pp);
                 }

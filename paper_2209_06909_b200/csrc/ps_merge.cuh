@@ -348,6 +348,72 @@ __global__ void __launch_bounds__(256) merge_partition_kernel(Bufs<K> bufs, cons
     partition_chunk<K>(bufs, nodes, chunk2node, c, cuts);
 }
 
+// Thin partition for stages with many cuts: three lanes per cut (one per other
+// run), ten cuts per warp, each lane a plain binary search.  A warp-wide 11-ary
+// search reads ~4x the DRAM sectors per search (ten probes per round past the
+// shared top of the search tree); once the cuts fill more than one wave of
+// warps the stage is bound by those sectors, not by the search depth.
+template <class K>
+__global__ void __launch_bounds__(256) merge_partition_thin_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
+                                                                   const uint32_t* __restrict__ chunk2node,
+                                                                   uint32_t c0, uint32_t c1,
+                                                                   uint4* __restrict__ cuts) {
+    pdl_wait();
+    const uint32_t lane = lane_id();
+    const uint32_t slot = lane / 3, o = lane % 3;  // lanes 30, 31 idle
+    const uint32_t c = c0 + (blockIdx.x * 8 + warp_id()) * 10 + slot;
+    const bool live = slot < 10 && c < c1;
+    uint32_t got = 0, a = 0, j = 0, w = 0, S = 0, q = 1;
+    Node nd;
+    if (live) {
+        nd = nodes[chunk2node[c]];
+        q = c - nd.chunk_base;
+        if (q > 0) {
+            q -= 1;
+            w = nd.arity;
+            S = node_spacing(nd, cut_cap<K>());
+            for (; a < w; ++a) {
+                const uint32_t nc = (nd.pos[a + 1] - nd.pos[a] - 1) / S;
+                if (q < nc) break;
+                q -= nc;
+            }
+            j = q + 1;
+            const K* src = bufs.kb(nd.parity ^ 1);
+            const K y = src[(uint64_t)nd.pos[a] + (uint64_t)j * S];
+            const uint32_t bb = o + (o >= a ? 1u : 0u);  // the o-th other run
+            if (o + 1 < w) {
+                const K* run = src + nd.pos[bb];
+                const uint32_t len = nd.pos[bb + 1] - nd.pos[bb];
+                got = bb < a ? count_pred<K, true>(run, len, y) : count_pred<K, false>(run, len, y);
+            }
+            q = 1;  // (marks a real cut below)
+        } else {
+            q = 0;
+        }
+    }
+    // gather the cut's three counts on its first lane
+    const uint32_t base = slot * 3 < 32 ? slot * 3 : 0;
+    const uint32_t g0 = __shfl_sync(PS_FULL, got, base), g1 = __shfl_sync(PS_FULL, got, base + 1),
+                   g2 = __shfl_sync(PS_FULL, got, base + 2);
+    if (!live || o != 0) return;
+    if (q == 0) {
+        cuts[c] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const uint32_t gg[3] = {g0, g1, g2};
+    uint32_t rk[4] = {0, 0, 0, 0};
+    rk[a] = j * S;
+    uint32_t mm = j - 1;
+#pragma unroll
+    for (uint32_t oo = 0; oo < 3; ++oo) {
+        if (oo + 1 >= w) break;
+        const uint32_t bb = oo + (oo >= a ? 1 : 0);
+        rk[bb] = gg[oo];
+        mm += gg[oo] ? (gg[oo] - 1) / S : 0;
+    }
+    cuts[nd.chunk_base + 1 + mm] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+}
+
 // ---------------------------------------------------------------------------
 // PTX helpers: mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP).
 PS_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
