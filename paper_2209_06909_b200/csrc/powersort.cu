@@ -575,9 +575,29 @@ struct MergeRunner {
             PS_LAUNCH_CHECK();
         }
         if (nsmall) {
-            const uint32_t G = small_group(small_max);
-            launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem, s, 
-                bufs, nodes, nlo, nhi, G);
+            // a thread per node while there are enough nodes to fill the GPU (a
+            // warp per 32 nodes); otherwise the warp-per-group kernel
+            static const bool old_small = getenv("PS_OLD_SMALL") != nullptr;  // A/B: warp-per-group kernel only
+            static const uint32_t tiny_min = getenv("PS_TINY_MIN") ? (uint32_t)atoi(getenv("PS_TINY_MIN")) : 32768u;
+            const bool use_tiny = !old_small && nsmall >= tiny_min;
+            auto tiny = [&](auto kern, size_t tsm, uint32_t warps) -> int {
+                PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+                launch_k(kern, grid_for(nhi - nlo, 32ull * warps), warps * 32, tsm, s, bufs, nodes, nlo, nhi);
+                return PS_OK;
+            };
+            if (use_tiny && small_max <= 64)
+                tiny(merge_tiny_kernel<K, 64>, merge_tiny_smem_bytes<K, 64>(), TinyCfg<K, 64>::WARPS);
+            else if (use_tiny && small_max <= 96)
+                tiny(merge_tiny_kernel<K, 96>, merge_tiny_smem_bytes<K, 96>(), TinyCfg<K, 96>::WARPS);
+            else if (use_tiny && small_max <= 128)
+                tiny(merge_tiny_kernel<K, 128>, merge_tiny_smem_bytes<K, 128>(), TinyCfg<K, 128>::WARPS);
+            else if (use_tiny && small_max <= 256)
+                tiny(merge_tiny_kernel<K, 256>, merge_tiny_smem_bytes<K, 256>(), TinyCfg<K, 256>::WARPS);
+            else {
+                const uint32_t G = small_group(small_max);
+                launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem,
+                         s, bufs, nodes, nlo, nhi, G);
+            }
             PS_LAUNCH_CHECK();
         }
         if (c1 > c0) {

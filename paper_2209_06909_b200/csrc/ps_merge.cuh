@@ -62,6 +62,9 @@ template <class K>
 PS_DEV __host__ constexpr uint32_t cut_cap() {
     return pipe_cap<K>() - pipe_vt<K>();
 }
+PS_DEV __host__ constexpr uint32_t align16c(uint32_t x) { return (x + 15u) & ~15u; }
+PS_DEV __host__ constexpr uint32_t cmax(uint32_t a, uint32_t b) { return a > b ? a : b; }
+
 // smallest cut spacing of any key type (bounds the chunk count)
 constexpr uint32_t MIN_CUT_SPACING =
     (cut_cap<int32_t>() < cut_cap<int64_t>() ? cut_cap<int32_t>() : cut_cap<int64_t>()) / MAX_WAY;
@@ -611,6 +614,131 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiny nodes (every small node of the stage <= TINY records): one node per
+// thread.  A warp stages its 32 nodes' keys as rows of TINY+1 elements (odd
+// stride: the lanes' row-wise accesses spread over the banks), each lane then
+// runs the node's stable k-way tournament sequentially (ties to the lower run,
+// as merges.py:229-269) and records the source offset of every output; the
+// store pass gathers keys from the rows and payloads from global memory, one
+// coalesced store per node and row segment.  No merge-path searches, no
+// per-node barrier: ~15 instructions per output and 32 independent merges per
+// warp, where the warp-per-node kernel spends most of its time in diagonal
+// searches for two outputs per lane.
+// 4- or 8-byte asynchronous global -> shared copy (LDGSTS)
+template <class T>
+PS_DEV void cp_async_small(T* smem_dst, const T* gmem_src) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4 or 8 bytes");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gmem_src), "n"(sizeof(T))
+                 : "memory");
+}
+
+template <class K, uint32_t TINY>
+struct TinyCfg {
+    static constexpr uint32_t RK = TINY + 1;                      // key / payload row stride (elements)
+    static constexpr uint32_t RI = (TINY + 4) & ~3u;              // offset row stride (bytes)
+    static constexpr uint32_t KEY_BYTES = align16c(32 * RK * (uint32_t)sizeof(K));
+    static constexpr uint32_t VAL_BYTES = align16c(32 * RK * 4u);
+    static constexpr uint32_t WARP_BYTES = KEY_BYTES + VAL_BYTES + align16c(32 * RI) + 32 * 16;
+    static constexpr uint32_t WARPS = cmax(1u, (uint32_t)(112 * 1024) / WARP_BYTES);  // two CTAs per SM
+};
+template <class K, uint32_t TINY>
+size_t merge_tiny_smem_bytes() {
+    return (size_t)TinyCfg<K, TINY>::WARPS * TinyCfg<K, TINY>::WARP_BYTES;
+}
+
+template <class K, uint32_t TINY>
+__global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kernel(Bufs<K> bufs,
+                                                                                  const Node* __restrict__ nodes,
+                                                                                  uint32_t nlo, uint32_t nhi) {
+    static_assert(TINY <= 256, "offsets are bytes");
+    using C = TinyCfg<K, TINY>;
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t warp = warp_id(), lane = lane_id();
+    uint8_t* wbase = smem + (size_t)warp * C::WARP_BYTES;
+    K* rows = reinterpret_cast<K*>(wbase);
+    int32_t* vrows = reinterpret_cast<int32_t*>(wbase + C::KEY_BYTES);
+    uint8_t* outi = wbase + C::KEY_BYTES + C::VAL_BYTES;
+    uint32_t* nT = reinterpret_cast<uint32_t*>(outi + align16c(32 * C::RI));  // per node: T, p0, parity
+    uint32_t* nP = nT + 32;
+    uint32_t* nR = nT + 64;
+    const uint64_t i64 = (uint64_t)nlo + ((uint64_t)blockIdx.x * C::WARPS + warp) * 32 + lane;
+    uint32_t p0 = 0, T = 0, par = 0, w = 0;
+    uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;  // run ends (row offsets); run a starts at e_{a-1}
+    if (i64 < nhi) {
+        const Node nd = nodes[(uint32_t)i64];
+        w = nd.arity;
+        p0 = nd.pos[0];
+        const uint32_t size = nd.pos[w] - p0;
+        if (size <= TINY) {  // (bigger: the pipe kernel's)
+            T = size;
+            par = nd.parity;
+            e0 = nd.pos[1] - p0;
+            e1 = w > 1 ? nd.pos[2] - p0 : T;
+            e2 = w > 2 ? nd.pos[3] - p0 : T;
+            e3 = T;
+        }
+    }
+    if (__ballot_sync(PS_FULL, T != 0) == 0) return;
+    nT[lane] = T;
+    nP[lane] = p0;
+    nR[lane] = par;
+    __syncwarp();
+    // ---- rows: every node's keys and payloads (buffer parity ^ 1) with
+    // asynchronous copies, all in flight at once; slot q = (node q / TINY,
+    // offset q % TINY), 32 consecutive slots per instruction (coalesced) ----
+    constexpr uint32_t SLOTS = 32 * TINY;
+    for (uint32_t q = lane; q < SLOTS; q += 32) {
+        const uint32_t j = q / TINY, t = q % TINY;
+        if (t < nT[j]) {
+            const uint32_t sp = nR[j] ^ 1u;
+            cp_async_small(&rows[j * C::RK + t], bufs.kb(sp) + nP[j] + t);
+            cp_async_small(&vrows[j * C::RK + t], bufs.vb(sp) + nP[j] + t);
+        }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    // ---- the lane's tournament ----
+    if (T) {
+        const K* row = rows + lane * C::RK;
+        uint8_t* oi = outi + lane * C::RI;
+        uint32_t i0 = 0, i1 = e0, i2 = e1, i3 = e2;
+        K h0 = row[0], h1 = row[i1], h2 = row[i2], h3 = row[i3];
+        for (uint32_t o = 0; o < T; ++o) {
+            const bool v0 = i0 < e0, v1 = i1 < e1, v2 = i2 < e2, v3 = i3 < e3;
+            const bool b1 = v1 && (!v0 || h1 < h0);  // ties to the lower run
+            const bool b3 = v3 && (!v2 || h3 < h2);
+            const K kl = b1 ? h1 : h0, kr = b3 ? h3 : h2;
+            const bool vl = v0 || v1, vr = v2 || v3;
+            const bool right = vr && (!vl || kr < kl);
+            const uint32_t src = right ? (b3 ? i3 : i2) : (b1 ? i1 : i0);
+            oi[o] = (uint8_t)src;
+            const K nk = row[src + 1];  // (one past a run reads its neighbour or the row's slack)
+            const bool s0 = !right && !b1, s1 = !right && b1, s2 = right && !b3, s3 = right && b3;
+            i0 += s0;
+            i1 += s1;
+            i2 += s2;
+            i3 += s3;
+            h0 = s0 ? nk : h0;
+            h1 = s1 ? nk : h1;
+            h2 = s2 ? nk : h2;
+            h3 = s3 ? nk : h3;
+        }
+    }
+    __syncwarp();
+    // ---- stores: keys and payloads from the rows, one coalesced store per node ----
+    for (uint32_t q = lane; q < SLOTS; q += 32) {
+        const uint32_t j = q / TINY, t = q % TINY;
+        if (t < nT[j]) {
+            const uint32_t sidx = outi[j * C::RI + t], pj = nR[j];
+            bufs.kb(pj)[nP[j] + t] = rows[j * C::RK + sidx];
+            bufs.vb(pj)[nP[j] + t] = vrows[j * C::RK + sidx];
+        }
+    }
+}
+
 // nodes per warp for a batch whose largest small node has `maxsz` records
 inline uint32_t small_group(uint32_t maxsz) {
     if (maxsz == 0) return 1;
@@ -658,8 +786,6 @@ PS_DEV unsigned long long gtimer() {
 // Big-node chunks: persistent, warp-specialized, TMA-bulk double-buffered.
 constexpr uint32_t PIPE_THREADS = 32 + PIPE_CONSUMERS;
 
-PS_DEV __host__ constexpr uint32_t align16c(uint32_t x) { return (x + 15u) & ~15u; }
-PS_DEV __host__ constexpr uint32_t cmax(uint32_t a, uint32_t b) { return a > b ? a : b; }
 
 // (key, value) record in shared memory: 8 bytes for 4-byte keys, 16 for 8-byte
 template <class K>

@@ -310,3 +310,37 @@ def test_tree_paths_and_windows(name, n, mrl, dtype, dev):
     stable_sort_with(kt, SortConfig(min_run_len=mrl), values=vals)
     torch.cuda.synchronize()
     assert np.array_equal(vals.cpu().numpy(), ref.values * 3 + 1)
+
+
+_TINY_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle
+from paper_2209_06909_b200 import SortConfig, stable_argsort, workloads
+from paper_2209_06909_b200.policy import check
+dev = torch.device('cuda', 0)
+for name, n, dt, mrl in (('cfg4', 1 << 18, 'int32', 24), ('cfg1', 1 << 17, 'int32', 24), ('cfg1', 1 << 17, 'int64', 8),
+                         ('cfg4', 1 << 16, 'float32', 3), ('cfg1', 1 << 16, 'int32', 2)):
+    keys = workloads.generate(name, n=n, seed=9).astype(dt)
+    ref = oracle.sort(keys, min_run_len=mrl)
+    out, perm, stats = stable_argsort(torch.from_numpy(keys).to(dev), SortConfig(min_run_len=mrl))
+    check(dev)
+    assert np.array_equal(perm.cpu().numpy(), ref.values), (name, dt, mrl)
+    assert np.array_equal(out.cpu().numpy().view(np.uint8), ref.keys.view(np.uint8)), (name, dt, mrl)
+    assert stats.merge_cost == ref.stats['merge_cost']
+print('TINY OK')
+"""
+
+
+def test_tiny_node_kernel_forced(dev):
+    # the thread-per-node merge runs only on stages with >= 32K small nodes;
+    # PS_TINY_MIN=1 (read once per process) forces it onto every small stage
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PS_TINY_MIN="1")
+    r = subprocess.run([sys.executable, "-c", _TINY_SCRIPT, repo], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "TINY OK" in r.stdout, r.stdout + r.stderr
