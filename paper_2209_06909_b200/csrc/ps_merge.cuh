@@ -640,7 +640,7 @@ struct TinyCfg {
     static constexpr uint32_t RI = (TINY + 4) & ~3u;              // offset row stride (bytes)
     static constexpr uint32_t KEY_BYTES = align16c(32 * RK * (uint32_t)sizeof(K));
     static constexpr uint32_t VAL_BYTES = align16c(32 * RK * 4u);
-    static constexpr uint32_t WARP_BYTES = KEY_BYTES + VAL_BYTES + align16c(32 * RI) + 32 * 16;
+    static constexpr uint32_t WARP_BYTES = KEY_BYTES + VAL_BYTES + align16c(32 * RI);
     static constexpr uint32_t WARPS = cmax(1u, (uint32_t)(112 * 1024) / WARP_BYTES);  // two CTAs per SM
 };
 template <class K, uint32_t TINY>
@@ -661,9 +661,6 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
     K* rows = reinterpret_cast<K*>(wbase);
     int32_t* vrows = reinterpret_cast<int32_t*>(wbase + C::KEY_BYTES);
     uint8_t* outi = wbase + C::KEY_BYTES + C::VAL_BYTES;
-    uint32_t* nT = reinterpret_cast<uint32_t*>(outi + align16c(32 * C::RI));  // per node: T, p0, parity
-    uint32_t* nP = nT + 32;
-    uint32_t* nR = nT + 64;
     const uint64_t i64 = (uint64_t)nlo + ((uint64_t)blockIdx.x * C::WARPS + warp) * 32 + lane;
     uint32_t p0 = 0, T = 0, par = 0, w = 0;
     uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;  // run ends (row offsets); run a starts at e_{a-1}
@@ -682,20 +679,19 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
         }
     }
     if (__ballot_sync(PS_FULL, T != 0) == 0) return;
-    nT[lane] = T;
-    nP[lane] = p0;
-    nR[lane] = par;
-    __syncwarp();
     // ---- rows: every node's keys and payloads (buffer parity ^ 1) with
-    // asynchronous copies, all in flight at once; slot q = (node q / TINY,
-    // offset q % TINY), 32 consecutive slots per instruction (coalesced) ----
-    constexpr uint32_t SLOTS = 32 * TINY;
-    for (uint32_t q = lane; q < SLOTS; q += 32) {
-        const uint32_t j = q / TINY, t = q % TINY;
-        if (t < nT[j]) {
-            const uint32_t sp = nR[j] ^ 1u;
-            cp_async_small(&rows[j * C::RK + t], bufs.kb(sp) + nP[j] + t);
-            cp_async_small(&vrows[j * C::RK + t], bufs.vb(sp) + nP[j] + t);
+    // asynchronous copies, all in flight at once, coalesced per node ----
+    for (uint32_t j = 0; j < 32; ++j) {  // node-major: no division, empty tails skipped
+        const uint32_t tj = __shfl_sync(PS_FULL, T, j);
+        if (tj == 0) continue;
+        const uint32_t sp = __shfl_sync(PS_FULL, par, j) ^ 1u, bj = __shfl_sync(PS_FULL, p0, j);
+        const K* gk = bufs.kb(sp) + bj;
+        const int32_t* gv = bufs.vb(sp) + bj;
+        K* rk = rows + j * C::RK;
+        int32_t* rv = vrows + j * C::RK;
+        for (uint32_t t = lane; t < tj; t += 32) {
+            cp_async_small(rk + t, gk + t);
+            cp_async_small(rv + t, gv + t);
         }
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -729,12 +725,19 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
     }
     __syncwarp();
     // ---- stores: keys and payloads from the rows, one coalesced store per node ----
-    for (uint32_t q = lane; q < SLOTS; q += 32) {
-        const uint32_t j = q / TINY, t = q % TINY;
-        if (t < nT[j]) {
-            const uint32_t sidx = outi[j * C::RI + t], pj = nR[j];
-            bufs.kb(pj)[nP[j] + t] = rows[j * C::RK + sidx];
-            bufs.vb(pj)[nP[j] + t] = vrows[j * C::RK + sidx];
+    for (uint32_t j = 0; j < 32; ++j) {
+        const uint32_t tj = __shfl_sync(PS_FULL, T, j);
+        if (tj == 0) continue;
+        const uint32_t pj = __shfl_sync(PS_FULL, par, j), bj = __shfl_sync(PS_FULL, p0, j);
+        K* dk = bufs.kb(pj) + bj;
+        int32_t* dv = bufs.vb(pj) + bj;
+        const K* rk = rows + j * C::RK;
+        const int32_t* rv = vrows + j * C::RK;
+        const uint8_t* oj = outi + j * C::RI;
+        for (uint32_t t = lane; t < tj; t += 32) {
+            const uint32_t sidx = oj[t];
+            dk[t] = rk[sidx];
+            dv[t] = rv[sidx];
         }
     }
 }
