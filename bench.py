@@ -556,16 +556,21 @@ def run_ours(args):
             if e["kind"] == "partition":
                 part_ms += e["ms"]
     K = args.steps
+    # a stage's events bracket its partition launch too (reported on its own):
+    # the merge kernels' time is the stage time minus the partition time
+    kern_ms = merge_ms - part_ms
+    if "merge" in agg:
+        agg["merge"]["ms"] -= part_ms
     per_step = {k: {"ms": v["ms"] / K, "GB": v["bytes"] / K / 1e9} for k, v in agg.items()}
-    achieved = merge_bytes / (merge_ms / 1e3) / 1e9 if merge_ms else 0.0
-    pass_gbs = merge_bytes / ((merge_ms + part_ms) / 1e3) / 1e9 if merge_ms else 0.0
+    achieved = merge_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+    pass_gbs = merge_bytes / (merge_ms / 1e3) / 1e9 if merge_ms else 0.0
     traffic = load_traffic(args.config, n)
     if traffic:
         traffic["dram_over_algorithmic"] = traffic["dram_bytes_per_step"] / (merge_bytes / K) if merge_bytes else None
     roofline = {
         "bound": "hbm",
         "kernel": "merge_pipe_kernel + merge_small_kernel (all merge launches of a step)",
-        "timing": "CUDA events around every merge stage, on the sort's stream, over a profiled repeat of the K timed steps",
+        "timing": "CUDA events around every merge stage and its partition launch, on the sort's stream, over a profiled repeat of the K timed steps; merge kernels = stage time - partition time",
         "achieved": achieved,
         "peak": peak,
         "unit": "GB/s",
