@@ -9,7 +9,10 @@ run_lengths, natural_run_lengths and the on_merge trace.
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
 
 Outputs (committed): tests/golden/sorts.json.gz, profiles.json.gz,
-powers.json.gz, cfg_full.json.  Regenerating must reproduce them bit for bit.
+powers.json.gz, cfg_full.json (its "seconds" field is the reference's run
+time).  Regenerating must reproduce the rest bit for bit.  ``make_golden.py
+harness`` writes only tests/golden/harness.json: the reference harness's
+generator outputs and per-trial seeds.
 """
 
 from __future__ import annotations
@@ -203,8 +206,29 @@ def dump(name, obj):
     print(name, len(data), "bytes")
 
 
+def make_harness():
+    # the reference harness's generators and per-trial seeds (harness.py:74-134),
+    # for the GPU harness's restatement (paper_2209_06909_b200/harness.py)
+    from powersort import harness as rh
+
+    cases = []
+    for kind, n, exp in (("random-runs", 1000, None), ("random-runs", 4099, 7), ("random-runs", 20000, 1),
+                         ("random-runs", 50000, 300), ("random-permutation", 3000, None), ("sorted", 77, None),
+                         ("reverse", 77, None)):
+        for base, trial in ((0, 0), (3, 1), (12345, 2)):
+            seed = rh.derive_seed(base, trial)
+            arr = np.asarray(rh.generate(rh.GeneratorSpec(kind, n, expected_run_len=exp, seed=seed)),
+                             dtype=np.int64)
+            cases.append({"kind": kind, "n": n, "expected_run_len": exp, "base": base, "trial": trial,
+                          "seed": seed, "sha": sha(arr), "head": arr[:8].tolist()})
+    return {"csv_header": rh.CSV_HEADER, "cases": cases}
+
+
 if __name__ == "__main__":
     assert os.path.isdir(REF), "the reference is only present in the build container"
+    if sys.argv[1:] == ["harness"]:
+        dump("harness.json", make_harness())
+        sys.exit(0)
     print("reference powersort", powersort.__version__)
     dump("sorts.json.gz", make_sorts())
     dump("profiles.json.gz", make_profiles())
