@@ -150,6 +150,11 @@ int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys
                    const int64_t* shard_n, int64_t out_begin, int64_t out_end, void* out_keys, int32_t* out_vals,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* Payloads of any width: dst row i = src row perm[i], rows
+ * of row_bytes bytes, for the permutation a PS_VALUES_ARGSORT sort returned.
+ * src and dst must not overlap.  Stream-ordered; device pointers. */
+int ps_gather_rows(const void* src, const int32_t* perm, void* dst, int64_t n, int64_t row_bytes, void* stream);
+
 /* Phase timing of ps_sort (CUDA events on the sort's stream).  Enabled per
  * host thread; ps_profile_read returns the entries of the last profiled sort.
  * kind: 0 run detection, 1 merge tree, 2 leaf formation, 3 cut partition,

@@ -34,6 +34,7 @@ EXPORTS = (
     "ps_run_stack_capacity",
     "ps_shard_merge_workspace_size",
     "ps_shard_merge",
+    "ps_gather_rows",
     "ps_profile_enable",
     "ps_profile_read",
     "ps_launch_count",
@@ -121,6 +122,8 @@ def load():
     lib.ps_node_power.restype = ctypes.c_int
     lib.ps_run_stack_capacity.argtypes = [i64, i64]
     lib.ps_run_stack_capacity.restype = i64
+    lib.ps_gather_rows.argtypes = [vp, vp, vp, i64, i64, vp]
+    lib.ps_gather_rows.restype = i32
     lib.ps_shard_merge_workspace_size.argtypes = [i32, i64]
     lib.ps_shard_merge_workspace_size.restype = sz
     lib.ps_shard_merge.argtypes = [i32, i32, vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]

@@ -1167,6 +1167,22 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
 }  // namespace
 
 // =============================================================================
+namespace {
+// dst row i = src row perm[i]: thread per (row, W-byte word), words of a row
+// consecutive across threads (coalesced stores, row-contiguous loads)
+template <class W>
+__global__ void gather_rows_kernel(const W* __restrict__ src, const int32_t* __restrict__ perm, W* __restrict__ dst,
+                                   uint64_t n, uint64_t wpr) {
+    pdl_wait();
+    const uint64_t tot = n * wpr;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < tot; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t row = t / wpr, w = t - row * wpr;
+        dst[t] = src[(uint64_t)perm[row] * wpr + w];
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* ps_last_error(void) { return g_last_error.c_str(); }
@@ -1368,6 +1384,30 @@ int64_t ps_run_stack_capacity(int64_t k, int64_t n) {
 size_t ps_shard_merge_workspace_size(int32_t nshards, int64_t slab_n) {
     if (nshards < 1 || nshards > (int32_t)MAX_SHARDS || slab_n < 0) return 0;
     return (size_t)shard_layout((uint64_t)slab_n, 8).total;
+}
+
+int ps_gather_rows(const void* src, const int32_t* perm, void* dst, int64_t n, int64_t row_bytes, void* stream) {
+    if (n < 0 || row_bytes < 1) return fail(PS_EINVAL, "n must be >= 0 and row_bytes >= 1");
+    if (n == 0) return PS_OK;
+    if (!src || !perm || !dst) return fail(PS_EINVAL, "NULL pointer argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)row_bytes;
+    const unsigned grid = (unsigned)std::min<uint64_t>(cdiv((uint64_t)n * (uint64_t)row_bytes, 256 * 4), 148 * 32);
+    if (al % 16 == 0)
+        launch_k(gather_rows_kernel<uint4>, grid, 256, 0, s, (const uint4*)src, perm, (uint4*)dst, (uint64_t)n,
+                 (uint64_t)row_bytes / 16);
+    else if (al % 8 == 0)
+        launch_k(gather_rows_kernel<uint2>, grid, 256, 0, s, (const uint2*)src, perm, (uint2*)dst, (uint64_t)n,
+                 (uint64_t)row_bytes / 8);
+    else if (al % 4 == 0)
+        launch_k(gather_rows_kernel<uint32_t>, grid, 256, 0, s, (const uint32_t*)src, perm, (uint32_t*)dst,
+                 (uint64_t)n, (uint64_t)row_bytes / 4);
+    else
+        launch_k(gather_rows_kernel<uint8_t>, grid, 256, 0, s, (const uint8_t*)src, perm, (uint8_t*)dst,
+                 (uint64_t)n, (uint64_t)row_bytes);
+    launch_counter()++;
+    PS_CUDA(cudaGetLastError());
+    return PS_OK;
 }
 
 int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys, const int32_t* const* shard_vals,

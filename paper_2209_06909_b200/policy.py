@@ -252,8 +252,9 @@ def stable_sort_with(lst, config=None, values=None):
     (policy.py:201-262).
 
     ``lst`` is a 1-D CUDA tensor (int32/int64/float32/float64), optionally
-    with an int32 ``values`` tensor permuted alongside, or a Python list
-    (numbers, or records with ``config.key``).
+    with a ``values`` tensor permuted alongside (int32 1-D: carried through
+    the merges; any other dtype or row width: gathered by the stable
+    permutation), or a Python list (numbers, or records with ``config.key``).
     """
     if config is None:
         config = SortConfig()
@@ -261,12 +262,37 @@ def stable_sort_with(lst, config=None, values=None):
     torch = _torch()
     if isinstance(lst, torch.Tensor):
         if values is not None:
-            return _sort_tensor(lst, values, config, _lib.VALUES_PERMUTE)
+            if values.dtype == torch.int32 and values.dim() == 1:
+                return _sort_tensor(lst, values, config, _lib.VALUES_PERMUTE)
+            return _sort_with_rows(lst, values, config)
         _, _, stats = stable_argsort(lst, config)
         return stats
     if isinstance(lst, list):
         return _sort_list(lst, config)
     raise ValueError("stable_sort_with expects a CUDA tensor or a list")
+
+
+def _sort_with_rows(keys, values, config):
+    """Payload of any dtype / row width (first dimension = len(keys)), permuted
+    alongside the keys: a stable argsort, then ps_gather_rows."""
+    torch = _torch()
+    if not isinstance(values, torch.Tensor) or not values.is_cuda or values.device != keys.device:
+        raise ValueError("values must be a CUDA tensor on the keys' device")
+    if values.dim() < 1 or values.shape[0] != keys.numel() or not values.is_contiguous():
+        raise ValueError("values must be contiguous with one row per key")
+    _, perm, stats = stable_argsort(keys, config)
+    n = keys.numel()
+    if n == 0:
+        return stats
+    row_bytes = values.element_size() * (values.numel() // n)
+    if row_bytes == 0:
+        return stats
+    src = values.clone()
+    lib = _lib.load()
+    with torch.cuda.device(keys.device):
+        stream = torch.cuda.current_stream(keys.device).cuda_stream
+        _lib.check(lib.ps_gather_rows(src.data_ptr(), perm.data_ptr(), values.data_ptr(), n, row_bytes, stream))
+    return stats
 
 
 def _sort_list(lst, config):

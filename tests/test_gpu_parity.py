@@ -344,3 +344,20 @@ def test_tiny_node_kernel_forced(dev):
     r = subprocess.run([sys.executable, "-c", _TINY_SCRIPT, repo], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "TINY OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("shape,dtype", [((), torch.int64), ((3,), torch.float64), ((5,), torch.uint8),
+                                         ((2, 3), torch.float32), ((), torch.int16)])
+def test_payload_rows_any_width(shape, dtype, dev):
+    # payloads wider or narrower than int32 follow the stable permutation (ps_gather_rows)
+    n = 40001
+    keys_np = workloads.generate("cfg3", n=n, seed=4)
+    order = np.argsort(keys_np, kind="stable")
+    vals = torch.arange(n * int(np.prod(shape, dtype=np.int64)), device=dev).reshape((n,) + shape).to(dtype)
+    want = vals.cpu().numpy()[order]
+    keys = torch.from_numpy(keys_np).to(dev)
+    stats = stable_sort_with(keys, SortConfig(), values=vals)
+    torch.cuda.synchronize()
+    assert np.array_equal(keys.cpu().numpy(), keys_np[order])
+    assert np.array_equal(vals.cpu().numpy(), want)
+    assert stats.merge_cost > 0
