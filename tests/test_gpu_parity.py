@@ -320,7 +320,8 @@ from paper_2209_06909_b200 import SortConfig, stable_argsort, workloads
 from paper_2209_06909_b200.policy import check
 dev = torch.device('cuda', 0)
 for name, n, dt, mrl in (('cfg4', 1 << 18, 'int32', 24), ('cfg1', 1 << 17, 'int32', 24), ('cfg1', 1 << 17, 'int64', 8),
-                         ('cfg4', 1 << 16, 'float32', 3), ('cfg1', 1 << 16, 'int32', 2)):
+                         ('cfg4', 1 << 16, 'float32', 3), ('cfg1', 1 << 16, 'int32', 2), ('cfg2', 1 << 20, 'int32', 24),
+                         ('cfg3', 1 << 19, 'int64', 24), ('cfg5', 1 << 19, 'float32', 24)):
     keys = workloads.generate(name, n=n, seed=9).astype(dt)
     ref = oracle.sort(keys, min_run_len=mrl)
     out, perm, stats = stable_argsort(torch.from_numpy(keys).to(dev), SortConfig(min_run_len=mrl))
@@ -332,15 +333,16 @@ print('TINY OK')
 """
 
 
-def test_tiny_node_kernel_forced(dev):
-    # the thread-per-node merge runs only on stages with >= 32K small nodes;
-    # PS_TINY_MIN=1 (read once per process) forces it onto every small stage
+def test_tiny_node_kernel_and_thin_partition_forced(dev):
+    # the thread-per-node merge runs only on stages with >= 32K small nodes and
+    # the thin partition only on stages with >= 12K cuts; PS_TINY_MIN=1 and
+    # PS_THIN_CUTS=1 (read once per process) force them onto every stage
     import os
     import subprocess
     import sys
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PS_TINY_MIN="1")
+    env = dict(os.environ, PS_TINY_MIN="1", PS_THIN_CUTS="1")
     r = subprocess.run([sys.executable, "-c", _TINY_SCRIPT, repo], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "TINY OK" in r.stdout, r.stdout + r.stderr
