@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs
                                                                     const uint32_t* __restrict__ nat,
                                                                     const uint8_t* __restrict__ leafpar, uint32_t r) {
     pdl_wait();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t RW = S + 1;
     const uint32_t lane = lane_id(), warp = warp_id();
     K* sk = reinterpret_cast<K*>(smem) + (size_t)warp * 32 * RW;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
                                                                    const uint32_t* __restrict__ tile_first,
                                                                    Summary* __restrict__ counters) {
     pdl_wait();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* sb = reinterpret_cast<uint32_t*>(smem);
     uint32_t* snat = sb + (FORM_TILE + 2);
     uint8_t* spar = reinterpret_cast<uint8_t*>(snat + (FORM_TILE + 1));
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(BIGW_THREADS) form_big_windows_kernel(Bufs<K> 
                                                                         const uint8_t* __restrict__ leafpar,
                                                                         uint32_t r) {
     pdl_wait();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     K* sk[2];
     int32_t* sv[2];
     sk[0] = reinterpret_cast<K*>(smem);

@@ -516,7 +516,7 @@ template <class K>
 __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
                                                                        uint32_t nlo, uint32_t nhi, uint32_t G) {
     pdl_wait();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     // per node of the group: packed start, global start, run starts (relative), size, parity
     __shared__ uint32_t s_pre[SMALL_WARPS][33];
     __shared__ uint32_t s_p0[SMALL_WARPS][32];
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
     static_assert(TINY <= 256, "offsets are bytes");
     using C = TinyCfg<K, TINY>;
     pdl_wait();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t warp = warp_id(), lane = lane_id();
     uint8_t* wbase = smem + (size_t)warp * C::WARP_BYTES;
     K* rows = reinterpret_cast<K*>(wbase);
