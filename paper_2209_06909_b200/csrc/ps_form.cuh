@@ -228,6 +228,12 @@ __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs
     }
 }
 
+// four consecutive keys: one (4-byte keys) or two (8-byte) 16-byte accesses
+template <class K>
+struct alignas(16) K4 {
+    K e[4];
+};
+
 // Largest j in [0, r) with b[j] <= x (b ascending, b[0] = 0 <= x), by a warp
 // (33-ary search: one probe per lane and round; all lanes return j).
 PS_DEV uint32_t warp_last_le(const uint32_t* __restrict__ b, uint32_t r, uint32_t x) {
@@ -386,6 +392,38 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
             const uint64_t lo = bj > t0 ? bj : t0, hi = ej < t1 ? ej : t1;
             if (!desc) {
                 if (!par && !ARGSORT) continue;  // in place already
+                // 4-element groups with 16-byte accesses (the arrays are 16-byte
+                // aligned), FORM_BATCH groups in flight per thread; the unaligned
+                // edges element by element below
+                const uint64_t lo4 = (lo + 3) & ~3ull, hi4 = hi & ~3ull;
+                const uint64_t a0 = lo4 < hi ? lo4 : hi, a1 = hi4 > a0 ? hi4 : a0;
+                for (uint64_t g0 = a0 / 4 + tid; g0 < a1 / 4; g0 += FORM_THREADS * FORM_BATCH) {
+                    K4<K> kq[FORM_BATCH];
+                    uint4 vq[FORM_BATCH];
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t g = g0 + (uint64_t)u * FORM_THREADS;
+                        if (g < a1 / 4) {
+                            if (par) kq[u] = reinterpret_cast<const K4<K>*>(K0)[g];
+                            if (!ARGSORT) vq[u] = reinterpret_cast<const uint4*>(V0)[g];
+                        }
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
+                        const uint64_t g = g0 + (uint64_t)u * FORM_THREADS;
+                        if (g < a1 / 4) {
+                            if (par) reinterpret_cast<K4<K>*>(dk)[g] = kq[u];
+                            const uint32_t q = (uint32_t)(4 * g);
+                            reinterpret_cast<uint4*>(dv)[g] = ARGSORT ? make_uint4(q, q + 1, q + 2, q + 3) : vq[u];
+                        }
+                    }
+                }
+                for (uint64_t p = tid; p < (a0 - lo) + (hi - a1); p += FORM_THREADS) {
+                    const uint64_t q = p < a0 - lo ? lo + p : a1 + (p - (a0 - lo));
+                    if (par) dk[q] = K0[q];
+                    dv[q] = ARGSORT ? (int32_t)q : V0[q];
+                }
+                continue;
                 for (uint64_t p0 = lo + tid; p0 < hi; p0 += FORM_THREADS * FORM_BATCH) {
                     K kk[FORM_BATCH];
                     int32_t vv[FORM_BATCH];
