@@ -423,27 +423,6 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
                     if (par) dk[q] = K0[q];
                     dv[q] = ARGSORT ? (int32_t)q : V0[q];
                 }
-                continue;
-                for (uint64_t p0 = lo + tid; p0 < hi; p0 += FORM_THREADS * FORM_BATCH) {
-                    K kk[FORM_BATCH];
-                    int32_t vv[FORM_BATCH];
-#pragma unroll
-                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
-                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
-                        if (p < hi) {
-                            if (par) kk[u] = K0[p];
-                            vv[u] = ARGSORT ? (int32_t)p : V0[p];
-                        }
-                    }
-#pragma unroll
-                    for (uint32_t u = 0; u < FORM_BATCH; ++u) {
-                        const uint64_t p = p0 + (uint64_t)u * FORM_THREADS;
-                        if (p < hi) {
-                            if (par) dk[p] = kk[u];
-                            dv[p] = vv[u];
-                        }
-                    }
-                }
             } else {
                 // mirrored pairs (p, s - p) belong to the owner of p <= s - p
                 const uint64_t sm = bj + ej - 1;
