@@ -1,6 +1,6 @@
 """Pinned H2D and D2H copies of the e2e workload's sizes, alone and
 concurrently on two streams: the PCIe bound of bench.py's e2e step.
-usage: python tools_copy_duplex.py"""
+usage: python tools/copy_duplex.py"""
 import torch
 dev = torch.device('cuda', 0)
 n = 1 << 24

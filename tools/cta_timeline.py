@@ -1,7 +1,7 @@
 """Per-CTA timeline of the last merge_pipe_kernel launch (PS_PIPE_TIMING build):
 start, after partition, first unit ready, consumers done, producer done (globaltimer ns).
 usage: nvcc ... -DPS_PIPE_TIMING -o /tmp/libps_timing.so;
-       PS_LIB=/tmp/libps_timing.so PS_DEBUG_STAGES=s python tools_cta_timeline.py cfg2"""
+       PS_LIB=/tmp/libps_timing.so PS_DEBUG_STAGES=s python tools/cta_timeline.py cfg2"""
 import ctypes, sys
 import numpy as np
 import torch

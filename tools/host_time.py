@@ -1,8 +1,7 @@
-"""Median time of one sort (CUDA events, L2 flushed, input restored outside
-the timed interval).  With PS_DEBUG_STAGES=s only the first s merge stages
-run, so a sweep over s gives each stage's marginal cost under PDL overlap.
-usage: PS_DEBUG_STAGES=s python tools_marginal.py [cfg2]"""
-import os, sys
+"""Host time spent inside one ps_sort call vs the device time of the same sort
+(is the host's launch rate the bottleneck?).  PS_DEBUG_STAGES limits the phases.
+usage: PS_DEBUG_STAGES=-2 python tools/host_time.py cfg2"""
+import os, sys, time
 import torch
 sys.path.insert(0, '.')
 from paper_2209_06909_b200 import SortConfig, _lib, workloads
@@ -13,18 +12,20 @@ dev = torch.device('cuda', 0)
 src = torch.from_numpy(workloads.generate(name)).to(dev)
 keys = torch.empty_like(src)
 perm = torch.empty(src.numel(), dtype=torch.int32, device=dev)
-flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-ts = []
+hs, ds = [], []
 for it in range(25):
     keys.copy_(src)
-    flush.fill_(it & 255)
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
+    t0 = time.perf_counter()
     _sort_tensor(keys, perm, SortConfig(), _lib.VALUES_ARGSORT, collect_runs=False)
+    t1 = time.perf_counter()
     b.record()
     torch.cuda.synchronize()
     if it >= 5:
-        ts.append(a.elapsed_time(b))
-ts.sort()
-print('%s stages=%s median %.1f us  min %.1f us' % (name, os.environ.get('PS_DEBUG_STAGES', 'all'),
-                                                   1e3 * ts[len(ts) // 2], 1e3 * ts[0]))
+        hs.append((t1 - t0) * 1e6)
+        ds.append(a.elapsed_time(b) * 1e3)
+hs.sort(); ds.sort()
+print('%s stages=%s host %.1f us  device %.1f us  launches/sort %s' % (
+    name, os.environ.get('PS_DEBUG_STAGES', 'all'), hs[len(hs) // 2], ds[len(ds) // 2], _lib.launch_count() if hasattr(_lib, 'launch_count') else '?'))

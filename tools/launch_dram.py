@@ -1,6 +1,6 @@
 """Per-launch time and DRAM bytes from an ncu --csv launch list captured with
 gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum.
-usage: python tools_launch_dram.py gpurun_out/pre_cfg2.csv"""
+usage: python tools/launch_dram.py gpurun_out/pre_cfg2.csv"""
 import collections, csv, sys
 
 rows = list(csv.reader(open(sys.argv[1])))

@@ -1,5 +1,5 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list (csv log).
-usage: python tools_launches.py gpurun_out/launches.csv [--seq]"""
+usage: python tools/launches.py gpurun_out/launches.csv [--seq]"""
 import collections, csv, sys
 
 rows = list(csv.reader(open(sys.argv[1])))

@@ -1,5 +1,5 @@
 """Per-source-line shared-memory wavefronts (total / ideal / excessive) of one
-ncu report launch.  usage: python tools_ncu_smem.py REPORT"""
+ncu report launch.  usage: python tools/ncu_smem.py REPORT"""
 import csv, io, subprocess, sys
 
 src = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],

@@ -1,5 +1,5 @@
 """Summarise an ncu report: stall reasons + hottest source lines of one launch.
-usage: python tools_ncu_src.py REPORT [launch_index]"""
+usage: python tools/ncu_src.py REPORT [launch_index]"""
 import collections, csv, io, subprocess, sys
 
 rep = sys.argv[1]

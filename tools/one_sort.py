@@ -1,5 +1,5 @@
 """One warm sort of a workload (for ncu captures of a single stage's kernels).
-usage: python tools_one_sort.py [cfg2]"""
+usage: python tools/one_sort.py [cfg2]"""
 import sys
 import torch
 sys.path.insert(0, '.')

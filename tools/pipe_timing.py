@@ -1,5 +1,5 @@
 """Phase cycle counters of merge_pipe_kernel (needs the PS_PIPE_TIMING build:
-   nvcc ... -DPS_PIPE_TIMING -o /tmp/libps_timing.so; PS_LIB=/tmp/libps_timing.so python tools_pipe_timing.py cfg2)"""
+   nvcc ... -DPS_PIPE_TIMING -o /tmp/libps_timing.so; PS_LIB=/tmp/libps_timing.so python tools/pipe_timing.py cfg2)"""
 import ctypes, sys
 import numpy as np
 import torch

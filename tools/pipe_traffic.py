@@ -1,6 +1,6 @@
 """Per-launch DRAM traffic of merge_pipe_kernel from an ncu csv (dram bytes +
 duration per launch) -> profiles/<tag>_pipe_traffic.json, read by bench.py for
-roofline.traffic.  usage: python tools_pipe_traffic.py CSV OUT_JSON"""
+roofline.traffic.  usage: python tools/pipe_traffic.py CSV OUT_JSON"""
 import collections, csv, json, sys
 
 rows = list(csv.reader(open(sys.argv[1])))

@@ -1,5 +1,5 @@
 """Per-stage CUDA-event profile of one sort (diagnostics; run on the GPU box).
-usage: python tools_stage_profile.py [cfg2] [n]"""
+usage: python tools/stage_profile.py [cfg2] [n]"""
 import sys
 import torch
 sys.path.insert(0, '.')
