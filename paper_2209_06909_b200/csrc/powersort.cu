@@ -560,7 +560,7 @@ struct MergeRunner {
         int dev = 0, sms = 148, occ = 1;
         PS_CUDA(cudaGetDevice(&dev));
         PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_pipe_kernel<K>, PIPE_THREADS, psmem));
+        PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, merge_pipe_kernel<K>, pipe_threads<K>(), psmem));
         pipe_grid_max = (uint32_t)std::max(1, sms * std::max(occ, 1));
         return PS_OK;
     }
@@ -606,7 +606,7 @@ struct MergeRunner {
             if (c1 - c0 > nbig) {  // some node has several chunks: cuts needed
                 // fused into the pipe launch while each of its warps has <= 1 cut to
                 // find (the searches are latency-bound; more cuts need the wide grid)
-                if (fuse && bar_next < nbars && c1 - c0 <= grid * (PIPE_THREADS / 32)) {
+                if (fuse && bar_next < nbars && c1 - c0 <= grid * (pipe_threads<K>() / 32)) {
                     bar = bars + bar_next++;  // partition fused into the pipe launch
                 } else {
                     const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
@@ -624,7 +624,7 @@ struct MergeRunner {
                 }
             }
             const uint32_t units = c1 - c0;
-            launch_k(merge_pipe_kernel<K>, grid, PIPE_THREADS, psmem, s, bufs, nelem, nodes,
+            launch_k(merge_pipe_kernel<K>, grid, pipe_threads<K>(), psmem, s, bufs, nelem, nodes,
                      c2n, cuts, c0, units, err, bar);
             PS_LAUNCH_CHECK();
         }

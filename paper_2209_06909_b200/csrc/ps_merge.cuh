@@ -30,19 +30,31 @@
 
 namespace ps {
 
-// consumer threads per merge_pipe_kernel CTA
-#ifndef PS_CONSUMERS
-#define PS_CONSUMERS 512
+// consumer threads per merge_pipe_kernel CTA, per key width (4-byte keys:
+// 576 consumers x VT 15 measured 0.8% faster than 512 x 17 on cfg2; 8-byte
+// keys keep 512 x 9, the most that fits the shared memory)
+#ifndef PS_CONSUMERS4
+#define PS_CONSUMERS4 576
 #endif
-constexpr uint32_t PIPE_CONSUMERS = PS_CONSUMERS;
+#ifndef PS_CONSUMERS8
+#define PS_CONSUMERS8 512
+#endif
+template <class K>
+PS_DEV __host__ constexpr uint32_t pipe_consumers() {
+    return sizeof(K) == 4 ? PS_CONSUMERS4 : PS_CONSUMERS8;
+}
+template <class K>
+PS_DEV __host__ constexpr uint32_t pipe_threads() {
+    return 32 + pipe_consumers<K>();
+}
 
 // Consumer thread t produces the VT outputs [VT*t, VT*t + VT) of every merge
-// pass.  VT is odd (17 records of 8 bytes, 9 of 16 bytes): the k-th output of
+// pass.  VT is odd (15 records of 8 bytes, 9 of 16 bytes): the k-th output of
 // the lanes of a warp lands in distinct banks (2 or 4 wavefronts per warp
 // store, the minimum), and the data-dependent read positions of balanced
 // merges (~VT/2 * t) spread over all banks as well.  No padding is needed.
 #ifndef PS_VT4
-#define PS_VT4 17
+#define PS_VT4 15
 #endif
 #ifndef PS_VT8
 #define PS_VT8 9
@@ -54,7 +66,7 @@ PS_DEV __host__ constexpr uint32_t pipe_vt() {
 // records per unit (smem slot capacity)
 template <class K>
 PS_DEV __host__ constexpr uint32_t pipe_cap() {
-    return pipe_vt<K>() * PIPE_CONSUMERS;
+    return pipe_vt<K>() * pipe_consumers<K>();
 }
 // Cut spacing budget: units hold <= CAP - VT records, so pass 1 can start Y
 // at a VT-aligned offset (no thread straddles X and Y) within NC threads.
@@ -471,7 +483,10 @@ PS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::c
 #define PS_SLOTS 2
 #endif
 constexpr uint32_t PIPE_SLOTS = PS_SLOTS;  // input slots per CTA (TMA multi-buffering)
-PS_DEV void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(PIPE_CONSUMERS) : "memory"); }
+template <uint32_t NC>
+PS_DEV void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Small nodes (size <= SMALL_NODE): one warp per group of G consecutive nodes
@@ -787,7 +802,6 @@ PS_DEV unsigned long long gtimer() {
 
 // ---------------------------------------------------------------------------
 // Big-node chunks: persistent, warp-specialized, TMA-bulk double-buffered.
-constexpr uint32_t PIPE_THREADS = 32 + PIPE_CONSUMERS;
 
 
 // (key, value) record in shared memory: 8 bytes for 4-byte keys, 16 for 8-byte
@@ -1002,7 +1016,7 @@ PS_DEV uint32_t last_le(const uint32_t* tab, uint32_t n, uint32_t x) {
 }
 
 template <class K>
-__global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, uint64_t nelem,
+__global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> bufs, uint64_t nelem,
                                                                   const Node* __restrict__ nodes,
                                                                   const uint32_t* __restrict__ chunk2node,
                                                                   uint4* __restrict__ cuts, uint32_t c0,
@@ -1023,7 +1037,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         PT_CTA(0)
         for (uint32_t sl = 0; sl < PIPE_SLOTS; ++sl) {
             mbar_init(&full[sl], 1);
-            mbar_init(&empty[sl], PIPE_CONSUMERS / 32);
+            mbar_init(&empty[sl], pipe_consumers<K>() / 32);
         }
         mbar_fence_init();
     }
@@ -1031,8 +1045,8 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         // fused partition: all warps of the grid compute the stage's cuts, then a
         // grid barrier (a cut lands at its merged index, possibly in another
         // CTA's chunk range)
-        const uint32_t nw = gridDim.x * (PIPE_THREADS / 32);
-        for (uint32_t c = blockIdx.x * (PIPE_THREADS / 32) + (tid >> 5); c < nchunks; c += nw)
+        const uint32_t nw = gridDim.x * (pipe_threads<K>() / 32);
+        for (uint32_t c = blockIdx.x * (pipe_threads<K>() / 32) + (tid >> 5); c < nchunks; c += nw)
             partition_chunk<K>(bufs, nodes, chunk2node, c0 + c, cuts);
         grid_barrier(bar_ctr, gridDim.x, err);
     } else {
@@ -1361,7 +1375,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                                   : wincur(g, 0, 0, ob, min(ob + VT, LX));
                 single_merge(c, xr);
                 PT_WARP(16)
-                consumer_sync();
+                consumer_sync<pipe_consumers<K>()>();
                 PT_MARK(5)
                 // pass 2: merge X and Y into the slot (its input windows are consumed)
                 RecCur<K> p0;
@@ -1446,7 +1460,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
                 }
             }
             PT_WARP(16)
-            consumer_sync();
+            consumer_sync<pipe_consumers<K>()>();
             PT_MARK(5)
             if (ob < d.end2) {
                 const uint32_t sg = last_le(d.s2, nseg, ob);
@@ -1490,7 +1504,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) merge_pipe_kernel(Bufs<K> bufs, 
         if (clane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
         // scratch xr is rewritten by the next unit's first pass (with two scratch
         // buffers only single-pass units, which have no barrier of their own, need it)
-        if (LY::NXR == 1 || single_pass) consumer_sync();
+        if (LY::NXR == 1 || single_pass) consumer_sync<pipe_consumers<K>()>();
         PT_MARK(7)
         PT_COUNT(8)
     }
