@@ -30,14 +30,14 @@
 
 namespace ps {
 
-// consumer threads per merge_pipe_kernel CTA, per key width (4-byte keys:
-// 576 consumers x VT 15 measured 0.8% faster than 512 x 17 on cfg2; 8-byte
-// keys keep 512 x 9, the most that fits the shared memory)
+// consumer threads per merge_pipe_kernel CTA, per key width (measured: 4-byte
+// keys 576 consumers x VT 15, 0.8% faster than 512 x 17 on cfg2; 8-byte keys
+// 352 x 13, 2.8% faster than 512 x 9 on cfg3)
 #ifndef PS_CONSUMERS4
 #define PS_CONSUMERS4 576
 #endif
 #ifndef PS_CONSUMERS8
-#define PS_CONSUMERS8 512
+#define PS_CONSUMERS8 352
 #endif
 template <class K>
 PS_DEV __host__ constexpr uint32_t pipe_consumers() {
@@ -49,7 +49,7 @@ PS_DEV __host__ constexpr uint32_t pipe_threads() {
 }
 
 // Consumer thread t produces the VT outputs [VT*t, VT*t + VT) of every merge
-// pass.  VT is odd (15 records of 8 bytes, 9 of 16 bytes): the k-th output of
+// pass.  VT is odd (15 records of 8 bytes, 13 of 16 bytes): the k-th output of
 // the lanes of a warp lands in distinct banks (2 or 4 wavefronts per warp
 // store, the minimum), and the data-dependent read positions of balanced
 // merges (~VT/2 * t) spread over all banks as well.  No padding is needed.
@@ -57,7 +57,7 @@ PS_DEV __host__ constexpr uint32_t pipe_threads() {
 #define PS_VT4 15
 #endif
 #ifndef PS_VT8
-#define PS_VT8 9
+#define PS_VT8 13
 #endif
 template <class K>
 PS_DEV __host__ constexpr uint32_t pipe_vt() {
