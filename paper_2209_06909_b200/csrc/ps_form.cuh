@@ -18,7 +18,10 @@ namespace ps {
 
 constexpr uint32_t FORM_TILE = 2048;
 constexpr uint32_t FORM_THREADS = 256;
-constexpr uint32_t FORM_TPC = 4;  // detection tiles per leaf-formation CTA
+#ifndef PS_FORM_TPC
+#define PS_FORM_TPC 8
+#endif
+constexpr uint32_t FORM_TPC = PS_FORM_TPC;  // detection tiles per leaf-formation CTA
 constexpr uint32_t MAX_FORM_M = 1024;
 // PS_NO_NET=1 (A/B builds): short windows take the rank loop too
 #ifndef PS_NO_NET
