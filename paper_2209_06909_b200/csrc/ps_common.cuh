@@ -15,7 +15,10 @@ namespace ps {
 
 // ---- run detection geometry --------------------------------
 constexpr uint32_t TILE = 2048;                   // positions per chain tile (one warp)
-constexpr uint32_t TILES_PER_GROUP = 8;           // tiles per CTA (a warp each)
+#ifndef PS_TPG
+#define PS_TPG 8
+#endif
+constexpr uint32_t TILES_PER_GROUP = PS_TPG;      // tiles per CTA (a warp each)
 constexpr uint32_t RD_THREADS = TILES_PER_GROUP * 32;  // run-detection CTA size
 constexpr uint32_t GROUP = TILE * TILES_PER_GROUP; // positions per CTA
 constexpr uint32_t GROUP_WORDS = GROUP / 32;      // type-bit words per CTA
