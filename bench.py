@@ -1,22 +1,29 @@
 """Benchmark: sorted keys/sec (4-way, stable) on BASELINE.json's configs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
 
+Default workload: cfg5 (n = 2^31 float32 keys in geometric ascending runs,
+int32 index payload, k = 4), the largest BASELINE config that fits one B200.
 A "step" is one full stable sort (run detection, merge tree, leaf formation,
-all merge levels) of one synthetic input resident in HBM.  Before every step
-the working array is restored from a pristine copy and L2 is flushed (a
-512 MiB write); neither is inside the timed interval, which is bracketed by
-CUDA events on the sort's stream.  ``e2e`` repeats the measurement through the
+all merge levels, the reference's SortStats counters including comparisons
+and moves) of one synthetic input resident in HBM.  Before every step the
+working array is restored from a pristine copy and L2 is flushed (a 512 MiB
+write); neither is inside the timed interval, which is bracketed by CUDA
+events on the sort's stream.  ``e2e`` repeats the measurement through the
 public API (``stable_argsort``) with the input copied from pinned host memory
 and the sorted keys + permutation copied back inside the timed interval.
 
 ``--impl reference`` times the reference algorithm's CPU restatement
 (oracle/, a C++ port of /root/reference/pkg/src/powersort, which is pure
-Python and cannot be installed on the GPU box) on the host cores: one
-independent full-size sort per thread.
+Python; the port is ~45x faster than the Python reference, so it is the
+stronger baseline) on all host cores: every step, each thread sorts its own
+bounded sample of the workload (cfg5: one 2^24-key chunk of the input each,
+whole runs; smaller configs: the whole input).
 
-Multi-GPU (torchrun, one process per GPU): every rank sorts its own shard of
-the same size (weak scaling); the time is the max over ranks.
+Multi-GPU (torchrun, one process per GPU): strong scaling of the same global
+input -- rank g holds the contiguous shard [g n/G, (g+1) n/G) -- sorted per
+shard and merged across shards over NVLink P2P (multigpu.sort_distributed);
+the time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -45,7 +52,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--keys", dest="n", type=int, default=None,
                     help="override the config size (default: the BASELINE size)")
     ap.add_argument("--k", type=int, default=4)
@@ -61,23 +68,36 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
-def config_dict(args, n, extra=None):
+def config_dict(args, n, key_dtype):
+    """The workload; identical in both arms (the driver compares them)."""
     from paper_2209_06909_b200 import workloads
 
-    d = {
+    return {
         "workload": "%s: %s" % (args.config, workloads.DESCRIPTIONS[args.config]),
         "n": n,
         "k": args.k,
         "variant": "4way" if args.k == 4 else "2way",
         "min_run_len": 24,
         "seed": args.seed,
-        "key_dtype": None,
+        "key_dtype": key_dtype,
         "payload": "int32 source index (stable argsort)",
+        "counters": "all SortStats fields, comparisons and moves included (SortConfig defaults)",
         "l2": "flushed before every step (512 MiB write); inputs restored from a pristine copy outside the timed interval",
     }
-    if extra:
-        d.update(extra)
-    return d
+
+
+def key_dtype_of(config):
+    return {"cfg1": "int32", "cfg2": "int32", "cfg3": "int64", "cfg4": "int32", "cfg5": "float32"}[config]
+
+
+def generate(args, n, lo=0, hi=None):
+    """The config's seeded input (cfg5: only the chunk-aligned slice [lo, hi))."""
+    from paper_2209_06909_b200 import workloads
+
+    if args.config == "cfg5":
+        return workloads.cfg5(n=n, seed=args.seed, lo=lo, hi=hi)
+    keys = workloads.generate(args.config, n=n, seed=args.seed)
+    return keys[lo:hi]
 
 
 def load_peaks():
@@ -168,32 +188,54 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML, 0.5 ms polling"}
 
 
-def cpu_oracle_baseline(keys_np, k, seconds):
-    """Single-thread oracle (C++ port of the reference) on the full input,
-    repeated for about `seconds`."""
+SAMPLE_N = 2**24  # cfg5 CPU sample: one generator chunk (whole runs)
+
+
+def cpu_sample(args, n, keys_np, index):
+    """The index-th bounded CPU sample of the workload: for cfg5 one 2^24-key
+    chunk of the input (the chunks are independent whole-run slices of the
+    same recipe); for the smaller configs the whole input."""
+    if args.config != "cfg5" or n <= SAMPLE_N:
+        return keys_np
+    c = index % (n // SAMPLE_N)
+    if keys_np is not None and keys_np.shape[0] == n:
+        return keys_np[c * SAMPLE_N:(c + 1) * SAMPLE_N]
+    return generate(args, n, c * SAMPLE_N, (c + 1) * SAMPLE_N)
+
+
+def cpu_oracle_baseline(args, n, keys_np, seconds):
+    """Single-thread oracle (C++ port of the reference) on bounded samples of
+    the workload, repeated for about `seconds`."""
     from oracle import oracle
 
-    variant = "4way" if k == 4 else "2way"
-    times = []
+    variant = "4way" if args.k == 4 else "2way"
+    times, keys_done = [], 0
     t_end = time.perf_counter() + seconds
+    i = 0
     while True:
+        x = cpu_sample(args, n, keys_np, i)
         t0 = time.perf_counter()
-        oracle.sort(keys_np, k=k, variant=variant, want_trace=False, want_runs=False)
+        oracle.sort(x, k=args.k, variant=variant, want_trace=False, want_runs=False)
         times.append(time.perf_counter() - t0)
+        keys_done += x.shape[0]
+        i += 1
         if time.perf_counter() > t_end or len(times) >= 20:
             break
-    n = keys_np.shape[0]
+    m = x.shape[0]
     return {
-        "value": n * len(times) / sum(times),
+        "value": keys_done / sum(times),
         "unit": UNIT,
         "cores": 1,
         "kind": "port",
-        "sample": "%d full-size sort(s) of the same %d-key input, oracle/ C++ restatement of the reference "
-                  "(single-threaded, as the reference)" % (len(times), n),
+        "sample": "%d sort(s) of %d-key %s on one thread, oracle/ C++ restatement of the reference "
+                  "(single-threaded, as the reference)" % (
+                      len(times), m, "chunks of the input (whole runs)" if m < n else "full-size inputs"),
     }
 
 
 def run_reference(args):
+    """The reference algorithm on the host cores (oracle/ C++ port): every
+    step, each of T threads sorts its own bounded sample (cpu_sample)."""
     rank, _, world = dist_env()
     if rank != 0:
         return 0
@@ -201,23 +243,29 @@ def run_reference(args):
     from paper_2209_06909_b200 import workloads
 
     n = args.n or workloads.FULL_N[args.config]
-    keys_np = workloads.generate(args.config, n=n, seed=args.seed)
+    sampled = args.config == "cfg5" and n > SAMPLE_N
+    keys_np = generate(args, n) if not sampled else None
+    m = SAMPLE_N if sampled else n
     variant = "4way" if args.k == 4 else "2way"
-    ncpu = os.cpu_count() or 1
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     try:
         import psutil
 
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 16 << 30
-    per_sort = keys_np.nbytes * 3 + n * 4 * 3 + (64 << 20)
+    per_sort = m * (8 if key_dtype_of(args.config) == "int64" else 4) * 3 + m * 4 * 3 + (64 << 20)
     threads = max(1, min(ncpu, int(avail * 0.6 // per_sort), 64))
+    nsteps = args.warmup + args.steps
+    if sampled:  # all samples generated before anything is timed
+        samples = [cpu_sample(args, n, None, i) for i in range(min(nsteps * threads, n // SAMPLE_N))]
+    else:
+        samples = [keys_np]
 
-    def one():
-        oracle.sort(keys_np, k=args.k, variant=variant, want_trace=False, want_runs=False)
-
-    def step():
-        ts = [threading.Thread(target=one) for _ in range(threads)]
+    def step(si):
+        ts = [threading.Thread(target=oracle.sort, args=(samples[(si * threads + t) % len(samples)],),
+                               kwargs=dict(k=args.k, variant=variant, want_trace=False, want_runs=False))
+              for t in range(threads)]
         t0 = time.perf_counter()
         for t in ts:
             t.start()
@@ -225,12 +273,12 @@ def run_reference(args):
             t.join()
         return time.perf_counter() - t0
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     total = 0.0
-    for _ in range(args.steps):
-        total += step()
-    value = threads * n * args.steps / total
+    for i in range(args.steps):
+        total += step(args.warmup + i)
+    value = threads * m * args.steps / total
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -243,33 +291,23 @@ def run_reference(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": str(keys_np.dtype),
+        "dtype": key_dtype_of(args.config),
         "data": "synthetic (seeded %s recipe, SURVEY 8d)" % args.config,
-        "config": config_dict(args, n, {"key_dtype": str(keys_np.dtype)}),
+        "config": config_dict(args, n, key_dtype_of(args.config)),
         "cpu_baseline": {
             "value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": "%d threads, each one independent full %d-key sort per step (oracle/ C++ restatement of "
-                      "the pure-Python reference; the algorithm is sequential, so threads run separate sorts)"
-                      % (threads, n),
+            "sample": ("%d threads, each sorting its own %d-key chunk of the %d-key input per step (%d distinct "
+                       "chunks, whole runs); a full %d-key sort does not fit %d host cores' time and memory "
+                       "budget, and its per-key CPU cost is higher (more merge levels), so this rate is an upper "
+                       "bound for the reference on the full input" % (threads, m, n, len(samples), n, threads))
+            if sampled else
+            ("%d threads, each one independent full %d-key sort per step (oracle/ C++ restatement of the "
+             "pure-Python reference; the algorithm is sequential, so threads run separate sorts)" % (threads, n)),
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
-
-
-def certificate_gpu(torch, src, keys, perm):
-    """O(n) stable-sort certificate on the device."""
-    n = src.numel()
-    p = perm.long()
-    seen = torch.zeros(n, dtype=torch.int32, device=src.device)
-    seen.index_fill_(0, p, 1)
-    assert int(seen.sum()) == n, "perm is not a permutation"
-    assert torch.equal(src[p], keys), "keys != src[perm]"
-    a, b = keys[:-1], keys[1:]
-    assert bool((a <= b).all()), "keys not sorted"
-    eq = a == b
-    assert not bool((p[:-1][eq] > p[1:][eq]).any()), "equal keys out of source order"
 
 
 def run_e2e(args, torch, dist, dev, keys_np, cfg, world, expect_keys):
@@ -332,7 +370,7 @@ def run_e2e(args, torch, dist, dev, keys_np, cfg, world, expect_keys):
     if world > 1:
         dist.barrier()
     e_ms, last = pipeline(args.steps)
-    assert np.array_equal(h_out[last].numpy(), expect_keys.cpu().numpy()), "e2e output differs"
+    assert np.array_equal(h_out[last].numpy(), expect_keys), "e2e output differs"
     te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -348,15 +386,19 @@ def run_e2e(args, torch, dist, dev, keys_np, cfg, world, expect_keys):
 
 
 def run_distributed(args):
-    """N > 1: the global input is world x n keys; rank g owns shard g (the
-    config recipe with seed + g).  One step = local sort of the shard plus the
-    NVLink cross-shard merge of this rank's slab (paper_2209_06909_b200.multigpu
-    .sort_distributed).  Weak scaling; time = max over ranks of the device
-    time between barriers."""
+    """N > 1: strong scaling of one global input (the config at its full size,
+    generated once per shard: rank g holds the contiguous shard [g N/G,
+    (g+1) N/G) of the same array for every G).  One step = local sort of the
+    shard plus the NVLink cross-shard merge of this rank's output slab
+    (paper_2209_06909_b200.multigpu.sort_distributed); time = max over ranks of
+    the device time between barriers.  The output is certified globally:
+    each slab sorted and stable, slab boundaries ordered, and the (key, index)
+    pairs of all slabs equal to those of the input (an all-reduced hash)."""
     import torch
     import torch.distributed as dist
 
     from paper_2209_06909_b200 import SortConfig, _lib, multigpu, workloads
+    from paper_2209_06909_b200.certify import distributed_certify
 
     rank, local, world = dist_env()
     backend = os.environ.get("PS_BENCH_BACKEND", "nccl")  # gloo: test mode, ranks may share a GPU
@@ -365,8 +407,9 @@ def run_distributed(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     red_dev = dev if backend == "nccl" else torch.device("cpu")
     lib = _lib.load()
-    n = args.n or workloads.FULL_N[args.config]
-    keys_np = workloads.generate(args.config, n=n, seed=args.seed + rank)
+    N = args.n or workloads.FULL_N[args.config]
+    lo, hi = multigpu.slab_bounds(N, world, rank)
+    keys_np = generate(args, N, lo, hi)
     cfg = SortConfig(k=args.k, variant="4way" if args.k == 4 else "2way")
     src = torch.from_numpy(keys_np).to(dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -385,20 +428,24 @@ def run_distributed(args):
         torch.cuda.synchronize()
         return t0.elapsed_time(t1), out
 
-    for _ in range(max(args.warmup, 1)):
+    for i in range(max(args.warmup, 1)):
         _, out = step()
+        if i == 0:
+            distributed_certify(src, lo, out[0], out[1], multigpu.slab_bounds(N, world, rank), red_dev)
     sampler = ClockSampler(dev.index)
     sampler.start()
-    launches0 = lib.ps_launch_count()
+    launches = 0
     total = 0.0
     for _ in range(args.steps):
+        l0 = lib.ps_launch_count()
         ms, out = step()
+        launches += lib.ps_launch_count() - l0
         total += ms
-    launches = lib.ps_launch_count() - launches0
     clocks = sampler.stop()
     t = torch.tensor([total], dtype=torch.float64, device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.item())
+    del out
     # e2e: pinned H2D of the shard, distributed sort, D2H of the slab (keys + global indices)
     h_in = torch.from_numpy(keys_np).pin_memory()
     e_total = 0.0
@@ -418,33 +465,30 @@ def run_distributed(args):
         if i >= max(args.warmup, 1):
             e_total += a.elapsed_time(b)
         d2h = hk.numel() * hk.element_size() + hv.numel() * 4
+        del ek, ev
     te = torch.tensor([e_total], dtype=torch.float64, device=red_dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e_total = float(te.item())
-    e2e = {"value": world * n * args.steps / (e_total / 1e3), "unit": UNIT,
+    e2e = {"value": N * args.steps / (e_total / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(keys_np.nbytes), "d2h_bytes_per_step": int(d2h),
            "ms_per_step": e_total / args.steps,
-           "api": "paper_2209_06909_b200.multigpu.sort_distributed"}
-    # certify this rank's slab: sorted, and its boundary with the next slab ordered
-    k, v = out
-    assert bool((k[:-1] <= k[1:]).all()), "slab not sorted"
+           "api": "paper_2209_06909_b200.multigpu.sort_distributed (per rank; bytes of rank 0)"}
     if rank == 0:
         line = {
             "metric": METRIC,
-            "value": world * n * args.steps / (total / 1e3),
+            "value": N * args.steps / (total / 1e3),
             "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": total / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
-            "dtype": str(keys_np.dtype),
-            "data": "synthetic (seeded %s recipe per shard, SURVEY 8d)" % args.config,
-            "config": config_dict(args, n * world, {
-                "key_dtype": str(keys_np.dtype),
-                "parallelism": "%d shards: local sort + NVLink P2P cross-shard merge (no NCCL on data)" % world}),
+            "dtype": key_dtype_of(args.config),
+            "data": "synthetic (seeded %s recipe, SURVEY 8d; the same global input for every G)" % args.config,
+            "config": config_dict(args, N, key_dtype_of(args.config)),
+            "parallelism": "%d contiguous shards: local sort + NVLink P2P cross-shard merge (no NCCL on data)" % world,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": int(launches),
@@ -459,8 +503,9 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2209_06909_b200 import SortConfig, _lib, stable_argsort, workloads
-    from paper_2209_06909_b200.policy import _sort_tensor
+    from paper_2209_06909_b200 import SortConfig, _lib, workloads
+    from paper_2209_06909_b200.certify import certify
+    from paper_2209_06909_b200.policy import _sort_tensor, check
 
     rank, local, world = dist_env()
     if world > 1:
@@ -469,7 +514,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     lib = _lib.load()
     n = args.n or workloads.FULL_N[args.config]
-    keys_np = workloads.generate(args.config, n=n, seed=args.seed + rank)
+    keys_np = generate(args, n)
     cfg = SortConfig(k=args.k, variant="4way" if args.k == 4 else "2way")
     src = torch.from_numpy(keys_np).to(dev)
     keys = torch.empty_like(src)
@@ -482,18 +527,21 @@ def run_ours(args):
         flush.fill_(1)
 
     def sort_once():
-        return _sort_tensor(keys, perm, cfg, _lib.VALUES_ARGSORT, collect_runs=False)
+        # asynchronous: the merges stay queued so the closing event follows the
+        # last kernel directly; check() below reads their invariant flags
+        return _sort_tensor(keys, perm, cfg, _lib.VALUES_ARGSORT, collect_runs=False, asynchronous=True)
 
     # warm-up (+ one certified run)
     for i in range(max(args.warmup, 1)):
         reset()
         stats = sort_once()
+        check(dev)
         if i == 0:
-            torch.cuda.synchronize()
-            certificate_gpu(torch, src, keys, perm)
+            certify(src, keys, perm)
     torch.cuda.synchronize()
 
-    # timed region: K sorts, each bracketed by events (reset/flush outside)
+    # timed region: K sorts, each bracketed by events (reset/flush and the
+    # invariant check outside)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
     if world > 1:
@@ -501,15 +549,19 @@ def run_ours(args):
     torch.cuda.synchronize()
     sampler.start()
     launches0 = lib.ps_launch_count()
+    launches = 0
     wall0 = time.perf_counter()
     for i in range(args.steps):
         reset()
         ev[i][0].record(stream)
+        l0 = lib.ps_launch_count()
         sort_once()
+        launches += lib.ps_launch_count() - l0
         ev[i][1].record(stream)
+        check(dev)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
-    launches = lib.ps_launch_count() - launches0
+    del launches0
     clocks = sampler.stop()
     # the same K steps again with per-launch CUDA events (phases, merge roofline);
     # profiling synchronizes at the end of every sort, so it stays out of the timed loop
@@ -528,18 +580,26 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     total_ms = float(t.item())
+    del flush
 
     # e2e through the public API: pinned H2D, sort, D2H of keys + permutation
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, torch, dist, dev, keys_np, cfg, world, keys)
+        # free the device-timed loop's buffers (cfg5: ~56 GB) before the e2e ring
+        from paper_2209_06909_b200.policy import _WS
+
+        expect = keys.cpu().numpy()
+        del src, keys, perm
+        _WS.buf.clear()
+        torch.cuda.empty_cache()
+        e2e = run_e2e(args, torch, dist, dev, keys_np, cfg, world, expect)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # roofline of the dominant kernel (merge_chunks) and phase breakdown
+    # roofline of the dominant kernel (the merge launches) and phase breakdown
     peak, peak_src = load_peaks()
     agg = {}
     merge_bytes = merge_ms = part_ms = 0.0
@@ -569,16 +629,20 @@ def run_ours(args):
         traffic["dram_over_algorithmic"] = traffic["dram_bytes_per_step"] / (merge_bytes / K) if merge_bytes else None
     roofline = {
         "bound": "hbm",
-        "kernel": "merge_pipe_kernel + merge_small_kernel (all merge launches of a step)",
-        "timing": "CUDA events around every merge stage and its partition launch, on the sort's stream, over a profiled repeat of the K timed steps; merge kernels = stage time - partition time",
+        "kernel": "merge_pipe_kernel + small/tiny merge kernels (all merge launches of a step)",
+        "timing": "CUDA events around every merge stage and its partition launch, on the sort's stream, over a "
+                  "profiled repeat of the K timed steps; merge kernels = stage time - partition time",
         "achieved": achieved,
         "peak": peak,
         "unit": "GB/s",
         "frac": achieved / peak if peak else None,
         "peak_source": peak_src,
+        "frac_of_8TBps": achieved / 8000.0,
         "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
         "traffic_detail": traffic,
         "algorithmic_bytes_per_step": merge_bytes / K,
+        "algorithmic_bytes_rule": "2 * merge_cost * (key bytes + 4): every merged record read once and written "
+                                  "once per merge it takes part in (SURVEY 8d)",
         "launches_per_step": merge_launches / K,
         "merge_pass_gbs_incl_partition": pass_gbs,
         "merge_pass_frac_of_8TBps": pass_gbs / 8000.0,
@@ -594,21 +658,22 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": str(keys_np.dtype),
+        "dtype": key_dtype_of(args.config),
         "data": "synthetic (seeded %s recipe, SURVEY 8d; numpy PCG64)" % args.config,
-        "config": config_dict(args, n, {"key_dtype": str(keys_np.dtype),
-                                        "parallelism": "1 GPU" if world == 1 else "%d independent shards" % world}),
+        "config": config_dict(args, n, key_dtype_of(args.config)),
+        "parallelism": "1 GPU" if world == 1 else "%d independent replicas" % world,
         "e2e": e2e,
         "roofline": roofline,
         "phases_per_step": per_step,
         "stats": {"merge_cost": stats.merge_cost, "runs": stats.runs_detected,
-                  "merges": [stats.merges2, stats.merges3, stats.merges4]},
+                  "merges": [stats.merges2, stats.merges3, stats.merges4],
+                  "comparisons": stats.comparisons, "moves": stats.moves},
         "clocks": clocks,
         "gpu_launches": int(launches),
         "wall_s_timed_loop": wall,
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_oracle_baseline(keys_np, args.k, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_oracle_baseline(args, n, keys_np, args.cpu_seconds)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

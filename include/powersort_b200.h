@@ -61,10 +61,16 @@ typedef struct {
     int64_t min_run_len;       /* >= 1 (MIN_RUN_LEN = 24, policy.py:34-36) */
     int32_t strict_merge_down; /* policy.py:146-175 */
     int32_t values_mode;       /* ps_values_mode */
-    int32_t count_comparisons; /* 1: exact comparisons / moves (CountingOrder, statskit.py:49-72);
-                                  ps_sort then synchronizes after the merges */
-    int32_t reserved;
+    int32_t count_comparisons; /* 1: exact comparisons / moves (CountingOrder, statskit.py:49-72) */
+    int32_t flags;             /* PS_FLAG_* bits; 0 = the reference's synchronous contract */
 } ps_config;
+
+/* ps_config.flags.  Without PS_FLAG_ASYNC, ps_sort returns after the merges
+ * have run and reports their device invariant flags (chunk bounds, grid
+ * barriers) as PS_EINVARIANT, like the reference's assertions.  With it,
+ * ps_sort returns once the merges are queued on `stream` (stats are already
+ * final host values) and ps_check() reports the merge-phase flags later. */
+enum { PS_FLAG_ASYNC = 1 };
 
 /* SortStats, statskit.py:75-98 (scalar fields).  comparisons / moves are
  * data-dependent counters of the reference's sequential kernels; they are
@@ -97,9 +103,10 @@ size_t ps_workspace_size(int64_t n, int32_t dtype, const ps_config* cfg);
  * `workspace` is device memory of >= ps_workspace_size() bytes; it also holds
  * the run profile and merge tree afterwards (see ps_result_*).
  * keys, values and workspace must be 16-byte aligned.
- * Returns once the merge tree is built (stats are host values); the merges
- * stay queued on `stream` like any kernel work.  ps_check() synchronizes and
- * reports merge-phase device invariants. */
+ * Returns after the merges have run and their device invariants were checked
+ * (or, with PS_FLAG_ASYNC, once they are queued on `stream`; then ps_check()
+ * synchronizes and reports merge-phase device invariants).  Concurrent sorts
+ * on different streams need separate workspaces. */
 int ps_sort(int32_t dtype, void* keys, int32_t* values, int64_t n, const ps_config* cfg, void* workspace,
             size_t workspace_bytes, ps_stats* stats, void* stream);
 

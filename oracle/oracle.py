@@ -83,6 +83,9 @@ def _load():
         lib.pso_node_power.restype = ctypes.c_int
         lib.pso_run_stack_capacity.argtypes = [ctypes.c_int64, ctypes.c_int64]
         lib.pso_run_stack_capacity.restype = ctypes.c_int64
+        lib.pso_detect_runs.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        lib.pso_detect_runs.restype = ctypes.c_int64
         _lib = lib
     return _lib
 
@@ -152,6 +155,25 @@ def sort(keys, values=None, k=4, variant="4way", min_run_len=24, strict_merge_do
     if want_trace:
         res.trace = trace_rows_to_list(rows[: count.value])
     return res
+
+
+def detect_runs(keys, min_run_len=24):
+    """The sort's run chain (run_lengths, natural_run_lengths) without sorting
+    (policy.py:241-248 over runs.py:23-82); O(n), no copy of the input."""
+    lib = _load()
+    keys = np.ascontiguousarray(keys)
+    if keys.dtype not in DTYPE_IDS:
+        raise ValueError("unsupported dtype %s" % keys.dtype)
+    n = keys.shape[0]
+    r = lib.pso_detect_runs(DTYPE_IDS[keys.dtype], keys.ctypes.data, n, min_run_len, None, None, 0)
+    if r < 0:
+        _raise(-r)
+    runs = np.zeros(max(r, 1), dtype=np.int64)
+    nat = np.zeros(max(r, 1), dtype=np.int64)
+    r2 = lib.pso_detect_runs(DTYPE_IDS[keys.dtype], keys.ctypes.data, n, min_run_len, runs.ctypes.data,
+                             nat.ctypes.data, r)
+    assert r2 == r
+    return runs[:r], nat[:r]
 
 
 def merge_cost_for_profile(lengths, k, strict_merge_down=False, want_trace=True):

@@ -686,9 +686,54 @@ void sort_impl(K* key, int32_t* val, int64_t n, int k, int variant, int64_t min_
     *out = s.st;
 }
 
+// The run chain of stable_sort_with alone (next_run, policy.py:241-248, with
+// find_first_run runs.py:23-47 and extend_run runs.py:71-82), read-only: a
+// step from `at` only reads positions >= at, and the reversal / insertion
+// sort of a run only rewrites positions before the next step's start, so the
+// chain of the unmodified input is the chain of the sort.  For inputs too big
+// for the full oracle (cfg5, n = 2^31).
+template <class K>
+int64_t detect_impl(const K* key, int64_t n, int64_t min_run_len, int64_t* run_lengths, int64_t* nat_lengths,
+                    int64_t cap) {
+    int64_t r = 0;
+    for (int64_t at = 0; at < n;) {
+        int64_t i = at + 1;
+        if (i < n) {
+            if (key[at] <= key[i]) {
+                i++;
+                while (i < n && key[i - 1] <= key[i]) i++;
+            } else {
+                i++;
+                while (i < n && !(key[i - 1] <= key[i])) i++;
+            }
+        }
+        int64_t e = i;
+        if (r < cap && nat_lengths) nat_lengths[r] = e - at;
+        if (e - at < min_run_len) e = (at + min_run_len < n) ? at + min_run_len : n;
+        if (r < cap && run_lengths) run_lengths[r] = e - at;
+        r++;
+        at = e;
+    }
+    return r;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Run profile of the input (see detect_impl); returns the run count r (the
+// arrays receive min(r, cap) entries) or -PSO_EINVAL.
+int64_t pso_detect_runs(int dtype, const void* keys, int64_t n, int64_t min_run_len, int64_t* run_lengths,
+                        int64_t* nat_lengths, int64_t cap) {
+    if (n < 0 || min_run_len < 1) return -PSO_EINVAL;
+    switch (dtype) {
+        case 0: return detect_impl((const int32_t*)keys, n, min_run_len, run_lengths, nat_lengths, cap);
+        case 1: return detect_impl((const int64_t*)keys, n, min_run_len, run_lengths, nat_lengths, cap);
+        case 2: return detect_impl((const float*)keys, n, min_run_len, run_lengths, nat_lengths, cap);
+        case 3: return detect_impl((const double*)keys, n, min_run_len, run_lengths, nat_lengths, cap);
+        default: return -PSO_EINVAL;
+    }
+}
 
 // dtype: 0 int32, 1 int64, 2 float32, 3 float64
 int pso_sort(int dtype, void* keys, int32_t* vals, int64_t n, int k, int variant, int64_t min_run_len,

@@ -19,6 +19,7 @@ PS_OK, PS_EINVAL, PS_ECUDA, PS_ENOMEM, PS_EINVARIANT, PS_EOVERFLOW = range(6)
 DTYPE_IDS = {"int32": 0, "int64": 1, "float32": 2, "float64": 3}
 VARIANT_IDS = {"2way": 0, "2way-copy-smaller": 1, "2way-nosentinel": 2, "4way": 3, "4way-nosentinel": 4}
 VALUES_PERMUTE, VALUES_ARGSORT = 0, 1
+FLAG_ASYNC = 1
 
 # Exported symbols (tests check the library exports every one of them).
 EXPORTS = (
@@ -51,7 +52,7 @@ class PsConfig(ctypes.Structure):
         ("strict_merge_down", ctypes.c_int32),
         ("values_mode", ctypes.c_int32),
         ("count_comparisons", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 

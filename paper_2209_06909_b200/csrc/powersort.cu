@@ -385,9 +385,9 @@ int build_tree(uint8_t* ws, const Layout& L, uint32_t r, uint64_t n, int k, int 
     const uint32_t log2k = k == 4 ? 2 : 1;
     // P over [0, padded): r + 1 boundaries and 0xFF up to the next multiple of 32
     const uint32_t padded = (uint32_t)align_up((uint64_t)r + 1, 32);
-    static const bool no_small_tree = getenv("PS_NO_SMALL_TREE") != nullptr;  // A/B: multi-kernel path
+    static const bool no_small_tree = knob_set("PS_NO_SMALL_TREE");  // A/B: multi-kernel path
     // A/B: PS_TREE_SMALL_R=x moves the one-CTA / multi-kernel crossover
-    static const uint32_t small_r = getenv("PS_TREE_SMALL_R") ? (uint32_t)atoi(getenv("PS_TREE_SMALL_R")) : TREE_SMALL_R;
+    static const uint32_t small_r = (uint32_t)knob("PS_TREE_SMALL_R", TREE_SMALL_R);
     if (r <= small_r && !no_small_tree) {
         // the whole build in one CTA (tree_small_kernel), then one publish
         TreeSmallArgs a;
@@ -537,6 +537,7 @@ struct MergeRunner {
     uint32_t* bars;  // grid-barrier counters, one per fused-partition pipe launch
     uint32_t nbars, bar_next;
     bool fuse;
+    static inline bool coop_pdl = true;  // cooperative launches also take PDL until the driver refuses
 
     int init(Bufs<K> b, uint64_t n, const Node* nd, const uint32_t* chunk2node, uint4* ct, uint32_t* e,
              uint32_t* bar, uint32_t nbar, cudaStream_t st) {
@@ -545,7 +546,7 @@ struct MergeRunner {
         bars = bar;
         nbars = nbar;
         bar_next = 0;
-        static const bool no_fuse = getenv("PS_NO_FUSE") != nullptr;  // A/B: stand-alone partition launches
+        static const bool no_fuse = knob_set("PS_NO_FUSE");  // A/B: stand-alone partition launches
         fuse = !no_fuse && bar != nullptr;
         if (fuse) PS_CUDA(cudaMemsetAsync(bar, 0, (size_t)nbar * 4, st));
         nodes = nd;
@@ -577,8 +578,8 @@ struct MergeRunner {
         if (nsmall) {
             // a thread per node while there are enough nodes to fill the GPU (a
             // warp per 32 nodes); otherwise the warp-per-group kernel
-            static const bool old_small = getenv("PS_OLD_SMALL") != nullptr;  // A/B: warp-per-group kernel only
-            static const uint32_t tiny_min = getenv("PS_TINY_MIN") ? (uint32_t)atoi(getenv("PS_TINY_MIN")) : 32768u;
+            static const bool old_small = knob_set("PS_OLD_SMALL");  // A/B: warp-per-group kernel only
+            static const uint32_t tiny_min = (uint32_t)knob("PS_TINY_MIN", 32768);
             const bool use_tiny = !old_small && nsmall >= tiny_min;
             auto tiny = [&](auto kern, size_t tsm, uint32_t warps) -> int {
                 PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
@@ -612,7 +613,7 @@ struct MergeRunner {
                     const int pp = prof ? prof->begin(3, stage_id, nbig, c1 - c0, 0) : -1;
                     // many cuts: three lanes per cut (fewer DRAM sectors); else a warp per cut
                     static const uint32_t thin_min =
-                        getenv("PS_THIN_CUTS") ? (uint32_t)atoi(getenv("PS_THIN_CUTS")) : THIN_CUTS;
+                        (uint32_t)knob("PS_THIN_CUTS", THIN_CUTS);
                     if (c1 - c0 >= thin_min)
                         launch_k(merge_partition_thin_kernel<K>, grid_for(c1 - c0, 80), 256, 0, s, bufs, nodes, c2n,
                                  c0, c1, cuts);
@@ -624,6 +625,28 @@ struct MergeRunner {
                 }
             }
             const uint32_t units = c1 - c0;
+            if (bar) {
+                // the fused partition's grid barrier needs every CTA resident:
+                // a cooperative launch guarantees it (also against concurrent
+                // sorts on other streams) or fails, and then the stage takes
+                // the stand-alone partition
+                cudaError_t e = launch_coop(coop_pdl, merge_pipe_kernel<K>, grid, pipe_threads<K>(), psmem, s, bufs,
+                                            nelem, nodes, c2n, cuts, c0, units, err, bar);
+                if (e != cudaSuccess && coop_pdl) {
+                    (void)cudaGetLastError();
+                    coop_pdl = false;  // this driver rejects cooperative + PDL
+                    e = launch_coop(false, merge_pipe_kernel<K>, grid, pipe_threads<K>(), psmem, s, bufs, nelem,
+                                    nodes, c2n, cuts, c0, units, err, bar);
+                }
+                if (e == cudaSuccess) {
+                    PS_LAUNCH_CHECK();
+                    return PS_OK;
+                }
+                (void)cudaGetLastError();
+                launch_k(merge_partition_kernel<K>, grid_for(c1 - c0, 8), 256, 0, s, bufs, nodes, c2n, c0, c1, cuts);
+                PS_LAUNCH_CHECK();
+                bar = nullptr;
+            }
             launch_k(merge_pipe_kernel<K>, grid, pipe_threads<K>(), psmem, s, bufs, nelem, nodes,
                      c2n, cuts, c0, units, err, bar);
             PS_LAUNCH_CHECK();
@@ -698,7 +721,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     const bool argsort = cfg.values_mode == PS_VALUES_ARGSORT;
     // PS_DEBUG_STAGES=s (measurement only): enqueue the first s merge stages;
     // -1 / -2 / -3: stop after run detection / the tree / leaf formation
-    static const int stage_limit = getenv("PS_DEBUG_STAGES") ? atoi(getenv("PS_DEBUG_STAGES")) : 1 << 30;
+    static const int stage_limit = (int)knob("PS_DEBUG_STAGES", 1 << 30);
     // data-dependent counters: comparisons / moves on request; copy-smaller's
     // buffer and scan counters always (both need a sync after the merges)
     const bool counting = cfg.count_comparisons != 0;
@@ -739,7 +762,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                                                    err);
         PS_LAUNCH_CHECK();
         const size_t c2smem = rd_chain2_smem((uint32_t)L.lvlP[0], (uint32_t)m);
-        static const size_t c2max = getenv("PS_CHAIN2_MAX") ? (size_t)atoll(getenv("PS_CHAIN2_MAX")) : 64 * 1024;
+        static const size_t c2max = (size_t)knob("PS_CHAIN2_MAX", 64 * 1024);
         if (L.tab_levels == 2 && c2smem <= c2max) {  // (bigger: one SM staging every table loses)
             // two levels: compose, top and down in one CTA
             PS_CUDA(cudaFuncSetAttribute(rd_chain2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2smem));
@@ -909,10 +932,16 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     prof.finish();  // synchronizes only while profiling
 
     // ---- N5: SortStats (statskit.py:75-98), from the tree summary ----------------
-    Summary c;  // the data-dependent counters, after the merges
-    if (need_counts) {
-        int rc = publish(sum, SUM_STATS, &c, nullptr, 0, nullptr, s);
+    // The data-dependent counters and the merge-phase invariant flags arrive
+    // after the merges (unless the caller asked for PS_FLAG_ASYNC).
+    Summary c;
+    memset(&c, 0, sizeof(c));
+    if (need_counts || !(cfg.flags & PS_FLAG_ASYNC)) {
+        int rc = publish(sum, need_counts ? SUM_STATS : SUM_HEAD, &c, nullptr, 0, nullptr, s);
         if (rc) return rc;
+        if (c.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
+        if (c.err)
+            return fail(PS_EINVARIANT, "merge-phase device invariant violated (flags " + std::to_string(c.err) + ")");
     }
     h = info.s;
     memset(st, 0, sizeof(*st));

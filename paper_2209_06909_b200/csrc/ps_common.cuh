@@ -129,6 +129,27 @@ struct Summary {
 // blocks until that predecessor has completed and its writes are visible.
 PS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Measurement knobs for A/B runs.  Only a -DPS_DEBUG_KNOBS build (tools/,
+// libpowersort_b200_debug.so) reads them from the environment; the product
+// library ignores the environment, so no variable can change what ps_sort does.
+inline long knob(const char* name, long dflt) {
+#ifdef PS_DEBUG_KNOBS
+    const char* v = getenv(name);
+    return v ? atol(v) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
+inline bool knob_set(const char* name) {
+#ifdef PS_DEBUG_KNOBS
+    return getenv(name) != nullptr;
+#else
+    (void)name;
+    return false;
+#endif
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                             Args&&... args) {
@@ -137,12 +158,32 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    static const bool pdl = getenv("PS_NO_PDL") == nullptr;  // PS_NO_PDL=1: plain stream order (A/B runs)
+    static const bool pdl = !knob_set("PS_NO_PDL");  // PS_NO_PDL=1: plain stream order (A/B runs)
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Cooperative launch (all CTAs co-resident, or the launch fails), for kernels
+// with a grid barrier; `pdl` adds programmatic stream serialization.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_coop(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -56,10 +56,11 @@ class SortConfig:
     key: Optional[Callable] = None
     strict_merge_down: bool = False
     on_merge: Optional[Callable] = None
-    #: B200 extension: compute the exact ``comparisons`` / ``moves`` counters of
-    #: the reference's CountingOrder (statskit.py:49-72); the sort then waits
-    #: for its merges.  Off: both are reported as None.
-    count_comparisons: bool = False
+    #: The exact ``comparisons`` / ``moves`` counters of the reference's
+    #: CountingOrder (statskit.py:49-72), which the reference always returns.
+    #: B200 extension: False skips their per-stage counting launches and
+    #: reports both as None.
+    count_comparisons: bool = True
 
 
 def _validated(config):
@@ -100,51 +101,63 @@ def _dtype_id(t):
 
 
 class _Workspace:
-    """Per-device workspace cache (grown on demand, torch caching allocator)."""
+    """Workspace cache, one buffer per (device, stream) (grown on demand, torch
+    caching allocator).  Sorts on different streams therefore never share
+    scratch memory and may run concurrently (SPEC.md:264 of the reference
+    allows concurrent sorts)."""
 
     def __init__(self):
         self.buf = {}
-        self.stream = {}
+
+    @staticmethod
+    def key(device, stream=None):
+        torch = _torch()
+        device = torch.device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        return (device, stream.cuda_stream)
 
     def get(self, device, nbytes):
-        """The device's workspace for use on its current stream.  A sort returns
-        with its merges still queued, so a switch of streams first orders the
-        new stream after the last one, and a grown buffer replaces the old one
-        only once the old one's work is done."""
+        """The workspace of ``device``'s current stream.  A grown buffer
+        replaces the old one only once the stream's queued work is done."""
         torch = _torch()
-        cur = self.buf.get(device)
         stream = torch.cuda.current_stream(device)
-        last = self.stream.get(device)
-        if last is not None and last != stream:
-            stream.wait_stream(last)
+        k = self.key(device, stream)
+        cur = self.buf.get(k)
         if cur is None or cur.numel() < nbytes:
-            if last is not None:
-                last.synchronize()
+            if cur is not None:
+                stream.synchronize()
             cur = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
-            self.buf[device] = cur
-        self.stream[device] = stream
+            self.buf[k] = cur
         return cur
+
+    def last(self, device=None):
+        torch = _torch()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        return self.buf.get(self.key(dev))
 
 
 _WS = _Workspace()
 
 
 def check(device=None):
-    """Waits for the last sort on ``device`` (its merges run asynchronously)
-    and raises if a device invariant was violated during them (ps_check)."""
+    """Waits for the last sort on ``device``'s current stream and raises if a
+    device invariant was violated during its merges (ps_check).  Only needed
+    after an asynchronous sort; the default sort checks before returning."""
     torch = _torch()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    ws = _WS.buf.get(dev)
+    ws = _WS.last(dev)
     if ws is None:
         return
     lib = _lib.load()
     _lib.check(lib.ps_check(ws.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
 
 
-def _cfg_struct(config, values_mode):
+def _cfg_struct(config, values_mode, asynchronous=False):
     return _lib.PsConfig(
         config.k, _lib.VARIANT_IDS[config.variant], config.min_run_len, int(bool(config.strict_merge_down)),
-        values_mode, int(bool(getattr(config, "count_comparisons", False))), 0,
+        values_mode, int(bool(getattr(config, "count_comparisons", True))),
+        _lib.FLAG_ASYNC if asynchronous else 0,
     )
 
 
@@ -161,7 +174,9 @@ def read_trace(ws=None, device=None):
     torch = _torch()
     lib = _lib.load()
     if ws is None:
-        ws = _WS.buf[torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())]
+        ws = _WS.last(device)
+        if ws is None:
+            raise ValueError("no sort has run on this device's current stream")
     r = ctypes_i64()
     nm = ctypes_i64()
     _lib.check(lib.ps_result_counts(ws.data_ptr(), r, nm))
@@ -181,10 +196,11 @@ def ctypes_i64():
     return ctypes.c_int64(0)
 
 
-def _sort_tensor(keys, values, config, values_mode, collect_runs=True):
+def _sort_tensor(keys, values, config, values_mode, collect_runs=True, asynchronous=False):
     """Core call: sorts ``keys`` (CUDA tensor) in place; ``values`` int32
     CUDA tensor permuted alongside (PERMUTE) or filled with source indices
-    (ARGSORT).  Returns SortStats."""
+    (ARGSORT).  Returns SortStats.  ``asynchronous``: return once the merges
+    are queued (PS_FLAG_ASYNC; check() reports their invariants later)."""
     torch = _torch()
     info = _validated(config)
     del info
@@ -204,11 +220,11 @@ def _sort_tensor(keys, values, config, values_mode, collect_runs=True):
         raise ValueError("values must be contiguous and on the keys' device")
     lib = _lib.load()
     dt = _dtype_id(keys)
-    cfg = _cfg_struct(config, values_mode)
+    cfg = _cfg_struct(config, values_mode, asynchronous)
     if keys.data_ptr() % 16 or values.data_ptr() % 16:
         # the C ABI needs 16-byte aligned arrays (TMA); sort aligned copies of views
         k2, v2 = keys.clone(), values.clone()
-        stats = _sort_tensor(k2, v2, config, values_mode, collect_runs)
+        stats = _sort_tensor(k2, v2, config, values_mode, collect_runs)  # synchronous
         keys.copy_(k2)
         values.copy_(v2)
         return stats
@@ -295,26 +311,85 @@ def _sort_with_rows(keys, values, config):
     return stats
 
 
+#: Reserved greatest elements (the reference's ``statskit.SENTINEL``,
+#: registered by the ``powersort`` compatibility shim): ``le(x, SENTINEL)`` is
+#: true and ``le(SENTINEL, x)`` false for every ordinary x, and comparisons
+#: against it are not counted (statskit.py:49-72).
+_SENTINELS = []
+
+
+def register_sentinel(obj):
+    """Treat ``obj`` (compared by identity) as the reference's SENTINEL."""
+    if not any(obj is x for x in _SENTINELS):
+        _SENTINELS.append(obj)
+
+
+_I64_MIN, _I64_MAX = -(2**63), 2**63 - 1
+
+
+def _list_keys(lst, keyf):
+    """The numeric key array of a Python list (policy.py:201-262 compares
+    ``key(a) <= key(b)``).  Returns (numpy keys, sentinel mask or None).
+    Integer keys must fit int64; a mix of ints and floats must be exact in
+    float64 (|int| <= 2^53), else the order could differ from Python's."""
+    sent = None
+    if _SENTINELS:
+        flags = [any(x is t for t in _SENTINELS) for x in lst]
+        if any(flags):
+            sent = np.asarray(flags, dtype=bool)
+    ks = [0 if (sent is not None and sent[i]) else (keyf(x) if keyf is not None else x)
+          for i, x in enumerate(lst)]
+    live = ks if sent is None else [k for k, f in zip(ks, sent.tolist()) if not f]
+    if all(isinstance(x, (int, np.integer)) for x in live):
+        if any(not (_I64_MIN <= int(x) <= _I64_MAX) for x in live):
+            raise ValueError("integer list keys must fit in int64")
+        arr = np.asarray([int(x) for x in ks], dtype=np.int64)
+        if sent is not None:
+            top = int(arr[~sent].max()) if (~sent).any() else 0
+            if top == _I64_MAX:
+                raise ValueError("SENTINEL needs a key value above every list key")
+            arr[sent] = top + 1
+        return arr, sent
+    if all(isinstance(x, (int, float, np.integer, np.floating)) for x in live):
+        for x in live:
+            if isinstance(x, (int, np.integer)) and abs(int(x)) > 2**53:
+                raise ValueError("mixed int/float list keys must be exact in float64 (|int| <= 2^53)")
+        arr = np.asarray([float(x) for x in ks], dtype=np.float64)
+        if np.isnan(arr).any():
+            raise ValueError("NaN keys are not supported (their order is undefined in the reference)")
+        if sent is not None:
+            if np.isposinf(arr[~sent]).any():
+                raise ValueError("SENTINEL needs a key value above every list key")
+            arr[sent] = np.inf
+        return arr, sent
+    raise ValueError("list keys must be numbers")
+
+
 def _sort_list(lst, config):
+    """Sorts a Python list in place: its keys are sorted on the device and the
+    list is reordered by the stable permutation (the reference's output,
+    SURVEY F1).  Reserved SENTINEL elements take a key above every other key
+    (they sort last, in input order); the reference then switches to the
+    variant's sentinel-free sibling (policy.py:211-214), whose counters apply."""
     torch = _torch()
     n = len(lst)
     if n == 0:
         return SortStats()
-    keyf = config.key
-    ks = [keyf(x) for x in lst] if keyf is not None else list(lst)
-    if all(isinstance(x, (int, np.integer)) and not isinstance(x, bool) for x in ks):
-        arr = np.asarray(ks, dtype=np.int64)
-    elif all(isinstance(x, (int, float, np.integer, np.floating)) for x in ks):
-        arr = np.asarray(ks, dtype=np.float64)
-    else:
-        raise ValueError("list keys must be numbers")
+    arr, sent = _list_keys(lst, config.key)
+    variant = config.variant
+    if sent is not None and VARIANTS[variant].needs_sentinel:
+        variant = VARIANTS[variant].fallback
     dev = torch.device("cuda", torch.cuda.current_device())
     keys = torch.from_numpy(arr).to(dev)
-    plain = SortConfig(config.k, config.variant, config.min_run_len, None, config.strict_merge_down,
-                       config.on_merge)
+    plain = SortConfig(config.k, variant, config.min_run_len, None, config.strict_merge_down,
+                       config.on_merge, config.count_comparisons)
     _, perm, stats = stable_argsort(keys, plain)
     order = perm.cpu().numpy()
     lst[:] = [lst[i] for i in order.tolist()]
+    if sent is not None and stats.comparisons is not None:
+        # comparisons against SENTINEL are not counted (statskit.py:64-67):
+        # the device counted them as ordinary key comparisons
+        stats.comparisons = None
     return stats
 
 

@@ -1,11 +1,13 @@
 """SortStats and the analytic counters (mirrors statskit.py:75-124 of the
 reference).
 
-Counters the B200 path computes exactly from the merge tree: merge_cost,
-buffer_cost, max_stack_height, runs_detected, merges2/3/4, scan_reads,
-scan_writes, run_lengths, natural_run_lengths.  ``comparisons`` and ``moves``
-count steps of the reference's sequential kernels; they are ``None`` until the
-device counters of SURVEY 8(f) land.
+Every counter is exact: merge_cost, buffer_cost, max_stack_height,
+runs_detected, merges2/3/4, scan_reads, scan_writes, run_lengths and
+natural_run_lengths come from the merge tree; ``comparisons`` and ``moves``
+(the reference's CountingOrder and element writes, statskit.py:49-72) from
+closed forms over a few ranks per merge computed on the device.
+They are ``None`` only when a sort was asked not to count them
+(``SortConfig(count_comparisons=False)``).
 """
 
 from __future__ import annotations

@@ -13,6 +13,7 @@ original index (int32), i.e. the reference's ``(key, index)`` records.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -111,31 +112,53 @@ def cfg4(n=FULL_N["cfg4"], seed=0):
     return np.concatenate([head, pairs.reshape(-1)]).astype(np.int32)
 
 
-def cfg5(n=FULL_N["cfg5"], seed=0, mean_len=4096, chunk=2**24):
-    """float32 uniform in [-1e6, 1e6] in ascending runs with geometric
-    lengths of mean ``mean_len``; generated in chunks of whole runs so host
-    memory stays near the output size."""
-    rng = _rng(seed)
-    lengths = _truncated_lengths(lambda size: rng.geometric(1.0 / mean_len, size=size), n)
-    out = np.empty(n, dtype=np.float32)
-    ends = np.cumsum(lengths)
-    starts = ends - lengths
-    pos = 0
-    li = 0
+CFG5_CHUNK = 2**24
+
+
+def _cfg5_chunk(c, m, seed, mean_len):
+    """Chunk c (m elements) of cfg5: its own PCG64 stream (SeedSequence([seed,
+    c])), geometric run lengths truncated at the chunk end, and each run's
+    values drawn directly in ascending order -- the order statistics of m
+    uniforms are cumulative sums of exponential spacings, normalised by one
+    extra spacing per run (no sort)."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, c]))
+    lengths = _truncated_lengths(lambda size: rng.geometric(1.0 / mean_len, size=size), m)
     r = lengths.shape[0]
-    while pos < n:
-        # whole runs covering at least `chunk` elements
-        hi = int(np.searchsorted(ends, min(n, pos + chunk), side="left")) + 1
-        hi = min(hi, r)
-        end = int(ends[hi - 1])
-        vals = rng.uniform(-1e6, 1e6, size=end - pos).astype(np.float32)
-        # sort within each run: key = run id * big + rank trick via lexsort
-        run_id = np.repeat(np.arange(li, hi), lengths[li:hi]) - li
-        order = np.lexsort((vals, run_id))
-        out[pos:end] = vals[order]
-        li = hi
-        pos = end
-    del starts
+    gaps = rng.standard_exponential(m + r)
+    cs = np.cumsum(gaps)
+    # run j occupies slots [s_j, s_j + L_j] of the spacings (L_j values + 1 gap)
+    starts = np.concatenate(([0], np.cumsum(lengths + 1)[:-1]))
+    base = np.where(starts > 0, cs[np.maximum(starts - 1, 0)], 0.0)
+    total = cs[starts + lengths] - base
+    keep = np.ones(m + r, dtype=bool)
+    keep[starts + lengths] = False
+    u = (cs[keep] - np.repeat(base, lengths)) / np.repeat(total, lengths)
+    return (-1e6 + 2e6 * u).astype(np.float32)
+
+
+def cfg5(n=FULL_N["cfg5"], seed=0, mean_len=4096, lo=0, hi=None, threads=None):
+    """float32 uniform in [-1e6, 1e6] in ascending runs with geometric lengths
+    of mean ``mean_len``.  Generated in independent chunks of 2^24 elements
+    (runs end at chunk boundaries; adjacent runs may still fuse), so any
+    chunk-aligned slice [lo, hi) -- a shard of the multi-GPU run -- is produced
+    on its own, chunks in parallel on host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    hi = n if hi is None else hi
+    C = min(CFG5_CHUNK, n)
+    if lo % C or (hi % C and hi != n) or not 0 <= lo <= hi <= n:
+        raise ValueError("cfg5 slices must be aligned to %d-element chunks" % C)
+    out = np.empty(hi - lo, dtype=np.float32)
+    chunks = list(range(lo // C, (hi + C - 1) // C))
+
+    def one(c):
+        a = c * C
+        b = min(n, a + C)
+        out[a - lo:b - lo] = _cfg5_chunk(c, b - a, seed, mean_len)
+
+    workers = threads or min(len(chunks), os.cpu_count() or 1, 32)
+    with ThreadPoolExecutor(max_workers=max(1, workers)) as ex:
+        list(ex.map(one, chunks))
     return out
 
 

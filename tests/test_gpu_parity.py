@@ -49,14 +49,15 @@ def test_golden_sorts(golden_sorts, dev):
                    strict_merge_down=case["strict"])
         if keys.size == 0:
             continue
-        out, perm, stats = gpu_sort(keys, dev, **cfg)
+        out, perm, stats = gpu_sort(keys, dev, count_comparisons=False, **cfg)
         assert perm.tolist() == case["perm"], cfg
         assert np.array_equal(out.view(np.uint8), keys[perm].view(np.uint8))
         want = case["stats"]
         for f in POLICY_FIELDS + COUNTER_FIELDS:
             assert getattr(stats, f) == want[f], (f, cfg)
         assert stats.comparisons is None and stats.moves is None
-        _, perm2, cstats = gpu_sort(keys, dev, count_comparisons=True, **cfg)
+        # the default config counts, like the reference (statskit.py:49-72)
+        _, perm2, cstats = gpu_sort(keys, dev, **cfg)
         assert perm2.tolist() == case["perm"], cfg
         assert cstats.moves == want["moves"], (cfg, keys.size)
         assert cstats.comparisons == want["comparisons"], (cfg, keys.size)
@@ -342,7 +343,12 @@ def test_tiny_node_kernel_and_thin_partition_forced(dev):
     import sys
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PS_TINY_MIN="1", PS_THIN_CUTS="1")
+    # the knobs are read only by the measurement build (-DPS_DEBUG_KNOBS)
+    sys.path.insert(0, repo)
+    import __graft_entry__
+
+    debug_lib = __graft_entry__.build_lib(debug=True)
+    env = dict(os.environ, PS_TINY_MIN="1", PS_THIN_CUTS="1", PS_LIB=debug_lib)
     r = subprocess.run([sys.executable, "-c", _TINY_SCRIPT, repo], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "TINY OK" in r.stdout, r.stdout + r.stderr
@@ -363,3 +369,60 @@ def test_payload_rows_any_width(shape, dtype, dev):
     assert np.array_equal(keys.cpu().numpy(), keys_np[order])
     assert np.array_equal(vals.cpu().numpy(), want)
     assert stats.merge_cost > 0
+
+
+def test_concurrent_sorts_on_two_streams(dev):
+    # the reference allows concurrent sorts: two host threads,
+    # each with its own stream (and so its own workspace), sorting at once;
+    # the fused-partition pipe launches are cooperative, so neither starves
+    # the other's grid barrier
+    import threading
+
+    inputs = [workloads.generate("cfg2", n=1 << 22, seed=41), workloads.generate("cfg3", n=1 << 21, seed=42),
+              workloads.generate("cfg5", n=1 << 22, seed=43), workloads.generate("cfg1", n=1 << 20, seed=44)]
+    refs = [oracle.sort(x, want_trace=False) for x in inputs]
+    errors = []
+
+    def worker(idx):
+        try:
+            s = torch.cuda.Stream(dev)
+            with torch.cuda.stream(s):
+                for rep in range(6):
+                    x = inputs[(idx + 2 * rep) % len(inputs)]
+                    ref = refs[(idx + 2 * rep) % len(inputs)]
+                    keys = torch.from_numpy(x).to(dev)
+                    out, perm, _ = stable_argsort(keys, SortConfig())
+                    s.synchronize()
+                    if not np.array_equal(perm.cpu().numpy(), ref.values):
+                        errors.append((idx, rep))
+        except Exception as e:  # noqa: BLE001
+            errors.append((idx, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_asynchronous_sorts_then_check(dev):
+    # PS_FLAG_ASYNC: ps_sort returns with the merges queued; check() reports
+    # their device invariants afterwards
+    from paper_2209_06909_b200 import _lib
+    from paper_2209_06909_b200.policy import _sort_tensor, check
+
+    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    work = []
+    for i, s in enumerate(streams):
+        x = workloads.generate("cfg2", n=1 << 21, seed=60 + i)
+        with torch.cuda.stream(s):
+            keys = torch.from_numpy(x).to(dev)
+            perm = torch.empty(x.shape[0], dtype=torch.int32, device=dev)
+            _sort_tensor(keys, perm, SortConfig(count_comparisons=False), _lib.VALUES_ARGSORT, collect_runs=False,
+                         asynchronous=True)
+        work.append((x, s, keys, perm))
+    for x, s, keys, perm in work:
+        with torch.cuda.stream(s):
+            check(dev)
+        assert np.array_equal(perm.cpu().numpy(), oracle.sort(x, want_trace=False).values)

@@ -203,3 +203,53 @@ def test_sort_distributed_two_processes_one_gpu():
     perm = np.argsort(keys, kind="stable")
     assert np.array_equal(np.concatenate([res[0][1], res[1][1]]), perm)
     assert np.array_equal(np.concatenate([res[0][0], res[1][0]]).view(np.uint32), keys[perm].view(np.uint32))
+
+
+def _certify_worker(rank, world, port, q, tamper):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_06909_b200.certify import distributed_certify
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(5)
+    N = 5000
+    keys = rng.integers(0, 300, size=N).astype(np.float32)  # many ties
+    order = np.argsort(keys, kind="stable")
+    lo, hi = multigpu.slab_bounds(N, world, rank)
+    src = torch.from_numpy(keys[lo:hi].copy())
+    t0, t1 = multigpu.slab_bounds(N, world, rank)
+    sk = torch.from_numpy(keys[order][t0:t1].copy())
+    si = torch.from_numpy(order[t0:t1].astype(np.int32))
+    if tamper == "swap" and rank == 1:
+        si[[3, 4]] = si[[4, 3]]  # breaks stability (or order) within the slab
+        sk[[3, 4]] = sk[[4, 3]]
+    if tamper == "dup" and rank == 0:
+        si[-1] = si[-2]  # duplicate index: multiset differs
+    try:
+        distributed_certify(src, lo, sk, si, (t0, t1), torch.device("cpu"))
+        q.put((rank, "ok"))
+    except AssertionError as e:
+        q.put((rank, str(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tamper", [None, "swap", "dup"])
+def test_distributed_certificate_gloo_world2(tamper):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_certify_worker, args=(r, 2, port, q, tamper)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    if tamper is None:
+        assert res == {0: "ok", 1: "ok"}
+    else:
+        assert any(v != "ok" for v in res.values()), res

@@ -105,3 +105,24 @@ def test_certificate_detects_errors():
     assert oracle.stable_argsort_certificate(keys, keys[perm], perm) is None
     bad = np.array([3, 1, 2, 0])
     assert oracle.stable_argsort_certificate(keys, keys[bad], bad) is not None
+
+
+def test_detect_runs_matches_reference_profiles(golden_sorts):
+    # the read-only run chain (used at n = 2^31, where the full oracle cannot
+    # run) against the reference's own run_lengths / natural_run_lengths
+    for case in golden_sorts:
+        keys = np.array(case["keys"], dtype=NP_DTYPE[case["dtype"]])
+        if keys.size == 0:
+            continue
+        runs, nat = oracle.detect_runs(keys, case["min_run_len"])
+        assert runs.tolist() == case["stats"]["run_lengths"]
+        assert nat.tolist() == case["stats"]["natural_run_lengths"]
+
+
+@pytest.mark.parametrize("name", workloads.CONFIGS)
+def test_detect_runs_matches_full_oracle(name):
+    keys = workloads.generate(name, n=1 << 18, seed=9)
+    for mrl in (1, 24, 300):
+        res = oracle.sort(keys, min_run_len=mrl, want_trace=False)
+        runs, nat = oracle.detect_runs(keys, mrl)
+        assert runs.tolist() == res.run_lengths and nat.tolist() == res.natural_run_lengths
