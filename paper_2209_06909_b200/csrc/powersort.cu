@@ -836,7 +836,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     bufs.k[1] = at<K>(ws, L.k1);
     bufs.v[1] = at<int32_t>(ws, L.v1);
     {
-        const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M), net_windows(m, counting));
+        const size_t smem = form_smem_bytes<K>((uint32_t)std::min<uint64_t>(m, MAX_FORM_M), net_windows(m));
         const unsigned grid = grid_for((uint64_t)n, (uint64_t)FORM_TILE * FORM_TPC);
         static_assert(FORM_TILE == TILE, "leaf formation tiles are run detection's chain tiles");
         // per-tile first leaf, written by rd_emit_kernel (tiled detector only)
@@ -854,13 +854,13 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                      ty, (uint32_t)m, tile_first, counting ? sum : nullptr);
         }
         PS_LAUNCH_CHECK();
-        if (net_windows(m, counting)) {
+        if (net_windows(m)) {
             // extended windows: a register sorting network per window (ps_form.cuh)
             const unsigned wg = grid_for(r, FORM_THREADS);  // a warp per 32 leaves
             auto go = [&](auto kern, size_t wsm) -> int {
                 PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
                 launch_k(kern, wg, FORM_THREADS, wsm, s, bufs, (const uint32_t*)b, (const uint32_t*)nat,
-                         (const uint8_t*)leafpar, r);
+                         (const uint8_t*)leafpar, r, counting ? sum : nullptr);
                 return PS_OK;
             };
             if (argsort) {

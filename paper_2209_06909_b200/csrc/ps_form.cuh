@@ -152,9 +152,9 @@ PS_DEV void net_sort(K (&k)[S], uint32_t (&o)[S]) {
     }
 }
 
-// Extended windows go to form_windows_kernel when they fit a network and no
-// CountingOrder counters are requested (those need the rank loop's shifts).
-__host__ __device__ inline bool net_windows(uint64_t m, bool counting) { return !PS_NO_NET && m <= 32 && !counting; }
+// Extended windows go to form_windows_kernel when they fit a network (it also
+// counts the insertion sort's compares and moves when asked).
+__host__ __device__ inline bool net_windows(uint64_t m) { return !PS_NO_NET && m <= 32; }
 
 template <class K, int S>
 constexpr size_t form_windows_smem() {
@@ -166,10 +166,16 @@ constexpr size_t form_windows_smem() {
 // form_leaves_kernel.  Windows move through a per-warp shared-memory
 // transpose (row w = window w, stride S+1 elements: conflict-free lane rows),
 // so global loads and stores are one coalesced instruction per window.
+//
+// With `counters`, each lane also counts its window's insertion sort
+// (runs.py:50-68): the element at offset q past the natural prefix, with s
+// earlier window elements greater than it, costs s + [s < q] compares and
+// s + 1 moves when s > 0 (statskit.py:49-72).
 template <class K, int S, bool ARGSORT>
 __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs, const uint32_t* __restrict__ b,
                                                                     const uint32_t* __restrict__ nat,
-                                                                    const uint8_t* __restrict__ leafpar, uint32_t r) {
+                                                                    const uint8_t* __restrict__ leafpar, uint32_t r,
+                                                                    Summary* __restrict__ counters) {
     pdl_wait();
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t RW = S + 1;
@@ -178,11 +184,12 @@ __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs
     uint32_t* so = reinterpret_cast<uint32_t*>(reinterpret_cast<K*>(smem) + (size_t)(FORM_THREADS / 32) * 32 * RW) +
                    (size_t)warp * 32 * RW;
     const uint32_t i = (blockIdx.x * (FORM_THREADS / 32) + warp) * 32 + lane;
-    uint32_t b0 = 0, len = 0, par = 0;
+    uint32_t b0 = 0, len = 0, par = 0, nprefix = 0;
     if (i < r) {
         b0 = b[i];
         const uint32_t l = b[i + 1] - b0;
-        if (nat[i] < l) {
+        nprefix = nat[i];
+        if (nprefix < l) {
             len = l;
             par = leafpar[i];
         }
@@ -202,6 +209,27 @@ __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs
     for (int j = 0; j < S; ++j) {
         o[j] = (uint32_t)j;
         k[j] = (uint32_t)j < len ? sk[lane * RW + j] : key_pad<K>();
+    }
+    if (counters) {
+        unsigned long long c_cmp = 0, c_mov = 0;
+#pragma unroll
+        for (int q = 1; q < S; ++q) {
+            uint32_t sh = 0;
+#pragma unroll
+            for (int f = 0; f < q; ++f) sh += (uint32_t)(k[q] < k[f]);
+            if ((uint32_t)q < len && (uint32_t)q >= nprefix) {
+                c_cmp += sh + (sh < (uint32_t)q ? 1u : 0u);
+                c_mov += sh ? sh + 1u : 0u;
+            }
+        }
+        for (int dd = 16; dd; dd >>= 1) {
+            c_cmp += __shfl_xor_sync(PS_FULL, c_cmp, dd);
+            c_mov += __shfl_xor_sync(PS_FULL, c_mov, dd);
+        }
+        if (lane == 0) {
+            if (c_cmp) atomicAdd(&counters->comparisons, c_cmp);
+            if (c_mov) atomicAdd(&counters->moves, c_mov);
+        }
     }
     net_sort<K, S>(k, o);
     constexpr PrunedNet<S> net{};
@@ -311,14 +339,15 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
     // A CTA covers FORM_TPC detection tiles.  When few (long) leaves cover the
     // whole span and windows are left to form_windows_kernel, it is formed in
     // one pass; otherwise tile by tile (the shared arrays hold one tile).
-    const bool net = net_windows(m, counters != nullptr);
+    const bool net = net_windows(m);
     const uint32_t ntiles = (uint32_t)((n + FORM_TILE - 1) / FORM_TILE);
     const uint32_t tb = blockIdx.x * FORM_TPC, te = min(tb + FORM_TPC, ntiles);
     const uint64_t span0 = (uint64_t)tb * FORM_TILE, span1 = min((uint64_t)te * FORM_TILE, n);
     locate(tb, te, span0, span1);
     const bool whole = net && s_cnt <= 16;
-    if (net && !whole) {
+    if (net && !whole && !counters) {
         // spans made only of extended windows (form_windows_kernel's) have nothing to do
+        // (unless their detection compares are counted)
         bool anynat = false;
         for (uint32_t i = tid; i < s_cnt; i += FORM_THREADS) {
             const uint32_t j = s_first + i;
@@ -530,7 +559,7 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
     }
 
     // ---- extended windows starting in this tile: stable rank ---------------
-    if (net_windows(m, counters != nullptr)) {  // form_windows_kernel sorts them
+    if (net_windows(m)) {  // form_windows_kernel sorts them
         flush_counters();
         return;
     }
