@@ -566,14 +566,86 @@ struct MergeRunner {
         return PS_OK;
     }
 
+    // the side stream of the counters and its events (sort-local; see stage())
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    bool join_pending = false;
+
+    // one side stream and event pair per host thread and device, kept for the
+    // thread's lifetime
+    struct SideRes {
+        int dev = -1;
+        cudaStream_t st = nullptr;
+        cudaEvent_t a = nullptr, b = nullptr;
+    };
+    static SideRes& side_res() {
+        thread_local SideRes r;
+        return r;
+    }
+    int use_side_stream() {
+        int dev = 0;
+        PS_CUDA(cudaGetDevice(&dev));
+        SideRes& r = side_res();
+        if (r.dev != dev) {
+            if (r.st) {  // another device: release the old set (after its work)
+                cudaStreamSynchronize(r.st);
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+                cudaStreamDestroy(r.st);
+            }
+            r = SideRes();
+            PS_CUDA(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking));
+            PS_CUDA(cudaEventCreateWithFlags(&r.a, cudaEventDisableTiming));
+            PS_CUDA(cudaEventCreateWithFlags(&r.b, cudaEventDisableTiming));
+            r.dev = dev;
+        }
+        side = r.st;
+        ev_in = r.a;
+        ev_out = r.b;
+        return PS_OK;
+    }
+    // the previous stage's counters are done before anything overwrites their inputs
+    int join() {
+        if (join_pending) {
+            PS_CUDA(cudaStreamWaitEvent(s, ev_out, 0));
+            join_pending = false;
+        }
+        return PS_OK;
+    }
+
     int stage(uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint32_t nsmall, uint32_t small_max, Prof* prof,
               int stage_id) {
         if (nhi <= nlo) return PS_OK;
+        {
+            int rc = join();
+            if (rc) return rc;
+        }
         const uint32_t nbig = (nhi - nlo) - nsmall;
-        if (count_variant >= 0) {  // before the merges overwrite nothing the counters read
-            launch_k(merge_counters_kernel<K>, grid_for(nhi - nlo, 8), 256, 0, s, bufs, nodes, nlo, nhi, count_variant,
-                     sum);
-            PS_LAUNCH_CHECK();
+        if (count_variant >= 0) {
+            // The counters read the stage's inputs, which no merge of this stage
+            // overwrites: they run on a side stream next to the stage's merges
+            // and the next stage waits for them.
+            static_assert(COUNT_SMALL == SMALL_KERNEL_MAX, "level_small counts the thread-counted nodes");
+            cudaStream_t cs = s;
+            if (side) {
+                PS_CUDA(cudaEventRecord(ev_in, s));
+                PS_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
+                cs = side;
+            }
+            if (nsmall) {
+                launch_k(merge_counters_small_kernel<K>, grid_for(nhi - nlo, 256), 256, 0, cs, bufs, nodes, nlo, nhi,
+                         count_variant, sum);
+                PS_LAUNCH_CHECK();
+            }
+            if (nbig) {
+                launch_k(merge_counters_kernel<K>, grid_for(nhi - nlo, 8), 256, 0, cs, bufs, nodes, nlo, nhi,
+                         count_variant, sum);
+                PS_LAUNCH_CHECK();
+            }
+            if (side) {
+                PS_CUDA(cudaEventRecord(ev_out, side));
+                join_pending = true;
+            }
         }
         if (nsmall) {
             // a thread per node while there are enough nodes to fill the GPU (a
@@ -911,6 +983,10 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
         if (rc) return rc;
         mr.count_variant = need_counts ? cfg.variant : -1;
         mr.sum = sum;
+        if (need_counts) {
+            rc = mr.use_side_stream();
+            if (rc) return rc;
+        }
         int stage = 0;
         auto run_stage = [&](uint32_t nlo, uint32_t nhi, uint32_t c0, uint32_t c1, uint64_t cost, uint32_t nsmall,
                              uint32_t small_max) -> int {
@@ -928,6 +1004,8 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
                            info.s.level_cost[h], info.s.level_small[h], info.s.level_small_max[h]);
             if (rc) return rc;
         }
+        rc = mr.join();  // the last counters land before the summary is read
+        if (rc) return rc;
     }
     prof.finish();  // synchronizes only while profiling
 

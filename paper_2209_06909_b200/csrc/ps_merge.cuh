@@ -217,6 +217,133 @@ PS_DEV void partition_chunk(const Bufs<K>& bufs, const Node* __restrict__ nodes,
     if (lane == 0) cuts[nd.chunk_base + 1 + mm] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
 }
 
+constexpr uint32_t COUNT_SMALL = 512;  // nodes counted by one thread
+
+// Up to three counts at once by one thread (the scalar twin of warp_count3).
+template <class K>
+PS_DEV void thread_count3(const K* r0, const K* r1, const K* r2, uint32_t l0, uint32_t l1, uint32_t l2, bool le0,
+                          bool le1, bool le2, uint32_t nsearch, K x, uint32_t* out) {
+    out[0] = nsearch > 0 ? (le0 ? count_pred<K, true>(r0, l0, x) : count_pred<K, false>(r0, l0, x)) : 0u;
+    out[1] = nsearch > 1 ? (le1 ? count_pred<K, true>(r1, l1, x) : count_pred<K, false>(r1, l1, x)) : 0u;
+    out[2] = nsearch > 2 ? (le2 ? count_pred<K, true>(r2, l2, x) : count_pred<K, false>(r2, l2, x)) : 0u;
+}
+
+// The counters of one node (see merge_counters_kernel); WARP: the whole warp
+// cooperates in every rank search (big nodes), else one thread per node.
+template <class K, bool WARP>
+PS_DEV void node_counters(const Bufs<K>& bufs, const Node& nd, int variant, unsigned long long& cmp,
+                          unsigned long long& wr) {
+    auto cnt3 = [](const K* r0, const K* r1, const K* r2, uint32_t l0, uint32_t l1, uint32_t l2, bool le0,
+                   bool le1, bool le2, uint32_t nsearch, K x, uint32_t* out) {
+        if (WARP)
+            warp_count3<K>(r0, r1, r2, l0, l1, l2, le0, le1, le2, nsearch, x, out);
+        else
+            thread_count3<K>(r0, r1, r2, l0, l1, l2, le0, le1, le2, nsearch, x, out);
+    };
+    const uint32_t w = nd.arity, T = nd.pos[w] - nd.pos[0];
+    const K* src = bufs.kb(nd.parity ^ 1);
+    uint32_t L[4], e[4], g[4][3];
+#pragma unroll
+    for (uint32_t a = 0; a < 4; ++a) L[a] = a < w ? nd.pos[a + 1] - nd.pos[a] : 0;
+#pragma unroll
+    for (uint32_t a = 0; a < 4; ++a) {
+        e[a] = 0;
+        g[a][0] = g[a][1] = g[a][2] = 0;
+        if (a >= w) continue;
+        // records of the other runs (in order) before run a's last record
+        const uint32_t b0 = a == 0 ? 1 : 0, b1 = a <= 1 ? 2 : 1, b2 = a == 3 ? 2 : 3;
+        const K y = src[(uint64_t)nd.pos[a + 1] - 1];
+        cnt3(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
+                       b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < a, b1 < a, b2 < a, w - 1, y, g[a]);
+        e[a] = L[a] - 1 + g[a][0] + (w > 2 ? g[a][1] : 0) + (w > 3 ? g[a][2] : 0);
+    }
+    if (w == 2) {
+        if (variant == 1 && L[0] > L[1]) {
+            // backward: first records' positions, f0 = run 1 before run 0's first
+            // record (strictly smaller), f1 = run 0 not after run 1's first (<=)
+            uint32_t f[3];
+            cnt3(src + nd.pos[1], src, src, L[1], 0, 0, false, false, false, 1, src[nd.pos[0]], f);
+            const uint32_t f0 = f[0];
+            uint32_t h[3];
+            cnt3(src + nd.pos[0], src, src, L[0], 0, 0, true, false, false, 1, src[nd.pos[1]], h);
+            const uint32_t f1 = h[0];
+            cmp = T - max(f0, f1);
+            wr = T - f1;
+        } else {
+            cmp = min(e[0], e[1]) + 1;
+            wr = e[0] + 1;
+        }
+    } else if (variant == 4) {
+        // stages kernels (merges.py:337-545): a tournament over the live runs
+        // until the first of them ends, then again over the rest, then a
+        // 2-way stage.  In a tournament every output costs its z compare plus
+        // the refetch compare of its side when that side holds two runs,
+        // except while the other side's pending head is the last record of
+        // its run (safe = 0): then the output costs the unfetch + refetch of
+        // both sides, 2 + [four] compares; the run-ending output costs none.
+        // Merged positions: mpos(c, i) of record i of run c; cnt(x, c) = run c
+        // records before run x's last (merged position e[x]).
+        auto slot = [](uint32_t c, uint32_t a) { return c < a ? c : c - 1; };
+        auto before_last = [&](uint32_t x, uint32_t c) -> uint32_t {
+            return c == x ? L[x] - 1 : g[x][slot(c, x)];
+        };
+        auto mpos = [&](uint32_t c, uint32_t i) -> int64_t {
+            const uint32_t b0 = c == 0 ? 1 : 0, b1 = c <= 1 ? 2 : 1, b2 = c == 3 ? 2 : 3;
+            uint32_t h[3];
+            cnt3(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
+                           b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < c, b1 < c, b2 < c, w - 1,
+                           src[(uint64_t)nd.pos[c] + i], h);
+            return (int64_t)i + h[0] + (w > 2 ? h[1] : 0) + (w > 3 ? h[2] : 0);
+        };
+        uint32_t alive[4] = {0, 1, 2, 3}, na = w;
+        int64_t os = 0;
+        int32_t bprev = -1;
+        while (na >= 3) {
+            const bool four = na == 4;
+            uint32_t be = alive[0];
+            for (uint32_t i = 1; i < na; ++i) be = e[alive[i]] < e[be] ? alive[i] : be;
+            const int64_t oe = e[be];
+            cmp += 2 + (four ? 1 : 0) + (uint64_t)(oe - os);
+            if (four) {
+                cmp += (uint64_t)(oe - os);
+            } else {
+                for (uint32_t i = 0; i < 2; ++i) {  // left-side outputs in [os, oe)
+                    const uint32_t c = alive[i];
+                    cmp += before_last(be, c) - (bprev < 0 ? 0u : before_last((uint32_t)bprev, c));
+                }
+            }
+            for (uint32_t i = 0; i < na; ++i) {
+                const uint32_t b = alive[i];
+                const bool left = i < 2;
+                if (!four && !left) continue;  // a right-side pending head costs the same either way
+                // q: merged position of the last record of b's side before b's last
+                int64_t q = -1;
+                if (L[b] >= 2) q = mpos(b, L[b] - 2);
+                const int32_t sib = left ? (int32_t)alive[1 - i] : (int32_t)alive[5 - i];
+                const uint32_t gc = before_last(b, (uint32_t)sib);
+                if (gc >= 1) q = max(q, mpos((uint32_t)sib, gc - 1));
+                const int64_t lo = max(q, os - 1), hi = min((int64_t)e[b], oe);
+                if (hi > lo + 1) cmp += (uint64_t)(hi - lo - 1);
+            }
+            uint32_t k2 = 0;  // drop the ended run, keep the order
+            for (uint32_t i = 0; i < na; ++i)
+                if (alive[i] != be) alive[k2++] = alive[i];
+            na = k2;
+            bprev = (int32_t)be;
+            os = oe + 1;
+        }
+        if (na == 2) cmp += (uint64_t)(min(e[alive[0]], e[alive[1]]) - os + 1);
+    } else {
+        const uint32_t MX = max(e[0], e[1]), MY = w == 4 ? max(e[2], e[3]) : e[2];
+        // side X outputs before its first run ends: g[0][0] = run 1 before run 0's last
+        const uint32_t CX = e[0] < e[1] ? L[0] - 1 + g[0][0] : L[1] - 1 + g[1][0];
+        // side Y: g[2][2] = run 3 before run 2's last, g[3][2] = run 2 before run 3's last
+        const uint32_t CY = w == 4 ? (e[2] < e[3] ? L[2] - 1 + g[2][2] : L[3] - 1 + g[3][2]) : 0;
+        cmp = 1 + (w == 4 ? 1 : 0) + (min(MX, MY) + 1) + CX + CY;
+    }
+    if (variant != 1) wr = 0;
+}
+
 // CountingOrder comparisons of the reference's merge kernels (merges.py:75-334)
 // and the written count of merge_2way_copy_smaller (:145-201) for the nodes of
 // one stage, from the merged positions e_a of every run's last record (and, for
@@ -237,111 +364,32 @@ __global__ void __launch_bounds__(256) merge_counters_kernel(Bufs<K> bufs, const
     const uint32_t idx = nlo + blockIdx.x * 8 + warp_id();
     unsigned long long cmp = 0, wr = 0;
     const Node nd = nodes[idx < nhi ? idx : nlo];
-    if (idx < nhi) {
-        const uint32_t w = nd.arity, T = nd.pos[w] - nd.pos[0];
-        const K* src = bufs.kb(nd.parity ^ 1);
-        uint32_t L[4], e[4], g[4][3];
-#pragma unroll
-        for (uint32_t a = 0; a < 4; ++a) L[a] = a < w ? nd.pos[a + 1] - nd.pos[a] : 0;
-#pragma unroll
-        for (uint32_t a = 0; a < 4; ++a) {
-            e[a] = 0;
-            g[a][0] = g[a][1] = g[a][2] = 0;
-            if (a >= w) continue;
-            // records of the other runs (in order) before run a's last record
-            const uint32_t b0 = a == 0 ? 1 : 0, b1 = a <= 1 ? 2 : 1, b2 = a == 3 ? 2 : 3;
-            const K y = src[(uint64_t)nd.pos[a + 1] - 1];
-            warp_count3<K>(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
-                           b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < a, b1 < a, b2 < a, w - 1, y, g[a]);
-            e[a] = L[a] - 1 + g[a][0] + (w > 2 ? g[a][1] : 0) + (w > 3 ? g[a][2] : 0);
-        }
-        if (w == 2) {
-            if (variant == 1 && L[0] > L[1]) {
-                // backward: first records' positions, f0 = run 1 before run 0's first
-                // record (strictly smaller), f1 = run 0 not after run 1's first (<=)
-                uint32_t f[3];
-                warp_count3<K>(src + nd.pos[1], src, src, L[1], 0, 0, false, false, false, 1, src[nd.pos[0]], f);
-                const uint32_t f0 = f[0];
-                uint32_t h[3];
-                warp_count3<K>(src + nd.pos[0], src, src, L[0], 0, 0, true, false, false, 1, src[nd.pos[1]], h);
-                const uint32_t f1 = h[0];
-                cmp = T - max(f0, f1);
-                wr = T - f1;
-            } else {
-                cmp = min(e[0], e[1]) + 1;
-                wr = e[0] + 1;
-            }
-        } else if (variant == 4) {
-            // stages kernels (merges.py:337-545): a tournament over the live runs
-            // until the first of them ends, then again over the rest, then a
-            // 2-way stage.  In a tournament every output costs its z compare plus
-            // the refetch compare of its side when that side holds two runs,
-            // except while the other side's pending head is the last record of
-            // its run (safe = 0): then the output costs the unfetch + refetch of
-            // both sides, 2 + [four] compares; the run-ending output costs none.
-            // Merged positions: mpos(c, i) of record i of run c; cnt(x, c) = run c
-            // records before run x's last (merged position e[x]).
-            auto slot = [](uint32_t c, uint32_t a) { return c < a ? c : c - 1; };
-            auto before_last = [&](uint32_t x, uint32_t c) -> uint32_t {
-                return c == x ? L[x] - 1 : g[x][slot(c, x)];
-            };
-            auto mpos = [&](uint32_t c, uint32_t i) -> int64_t {
-                const uint32_t b0 = c == 0 ? 1 : 0, b1 = c <= 1 ? 2 : 1, b2 = c == 3 ? 2 : 3;
-                uint32_t h[3];
-                warp_count3<K>(src + nd.pos[b0], src + nd.pos[b1], src + nd.pos[b2 < w ? b2 : 0], L[b0],
-                               b1 < w ? L[b1] : 0, b2 < w ? L[b2] : 0, b0 < c, b1 < c, b2 < c, w - 1,
-                               src[(uint64_t)nd.pos[c] + i], h);
-                return (int64_t)i + h[0] + (w > 2 ? h[1] : 0) + (w > 3 ? h[2] : 0);
-            };
-            uint32_t alive[4] = {0, 1, 2, 3}, na = w;
-            int64_t os = 0;
-            int32_t bprev = -1;
-            while (na >= 3) {
-                const bool four = na == 4;
-                uint32_t be = alive[0];
-                for (uint32_t i = 1; i < na; ++i) be = e[alive[i]] < e[be] ? alive[i] : be;
-                const int64_t oe = e[be];
-                cmp += 2 + (four ? 1 : 0) + (uint64_t)(oe - os);
-                if (four) {
-                    cmp += (uint64_t)(oe - os);
-                } else {
-                    for (uint32_t i = 0; i < 2; ++i) {  // left-side outputs in [os, oe)
-                        const uint32_t c = alive[i];
-                        cmp += before_last(be, c) - (bprev < 0 ? 0u : before_last((uint32_t)bprev, c));
-                    }
-                }
-                for (uint32_t i = 0; i < na; ++i) {
-                    const uint32_t b = alive[i];
-                    const bool left = i < 2;
-                    if (!four && !left) continue;  // a right-side pending head costs the same either way
-                    // q: merged position of the last record of b's side before b's last
-                    int64_t q = -1;
-                    if (L[b] >= 2) q = mpos(b, L[b] - 2);
-                    const int32_t sib = left ? (int32_t)alive[1 - i] : (int32_t)alive[5 - i];
-                    const uint32_t gc = before_last(b, (uint32_t)sib);
-                    if (gc >= 1) q = max(q, mpos((uint32_t)sib, gc - 1));
-                    const int64_t lo = max(q, os - 1), hi = min((int64_t)e[b], oe);
-                    if (hi > lo + 1) cmp += (uint64_t)(hi - lo - 1);
-                }
-                uint32_t k2 = 0;  // drop the ended run, keep the order
-                for (uint32_t i = 0; i < na; ++i)
-                    if (alive[i] != be) alive[k2++] = alive[i];
-                na = k2;
-                bprev = (int32_t)be;
-                os = oe + 1;
-            }
-            if (na == 2) cmp += (uint64_t)(min(e[alive[0]], e[alive[1]]) - os + 1);
-        } else {
-            const uint32_t MX = max(e[0], e[1]), MY = w == 4 ? max(e[2], e[3]) : e[2];
-            // side X outputs before its first run ends: g[0][0] = run 1 before run 0's last
-            const uint32_t CX = e[0] < e[1] ? L[0] - 1 + g[0][0] : L[1] - 1 + g[1][0];
-            // side Y: g[2][2] = run 3 before run 2's last, g[3][2] = run 2 before run 3's last
-            const uint32_t CY = w == 4 ? (e[2] < e[3] ? L[2] - 1 + g[2][2] : L[3] - 1 + g[3][2]) : 0;
-            cmp = 1 + (w == 4 ? 1 : 0) + (min(MX, MY) + 1) + CX + CY;
-        }
-        if (variant != 1) wr = 0;
-    }
+    // big nodes only (the others: merge_counters_small_kernel)
+    if (idx < nhi && nd.pos[nd.arity] - nd.pos[0] > COUNT_SMALL) node_counters<K, true>(bufs, nd, variant, cmp, wr);
     if (lane_id() != 0) cmp = wr = 0;
+    for (int dd = 16; dd; dd >>= 1) {
+        cmp += __shfl_xor_sync(PS_FULL, cmp, dd);
+        wr += __shfl_xor_sync(PS_FULL, wr, dd);
+    }
+    if (lane_id() == 0) {
+        if (cmp) atomicAdd(&sum->comparisons, cmp);
+        if (wr) atomicAdd(&sum->cs_written, wr);
+    }
+}
+
+// Nodes of at most COUNT_SMALL records: one thread per node (scalar rank
+// searches over runs that are a few cache lines long).
+template <class K>
+__global__ void __launch_bounds__(256) merge_counters_small_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
+                                                                   uint32_t nlo, uint32_t nhi, int variant,
+                                                                   Summary* sum) {
+    pdl_wait();
+    const uint32_t idx = nlo + blockIdx.x * 256 + threadIdx.x;
+    unsigned long long cmp = 0, wr = 0;
+    if (idx < nhi) {
+        const Node nd = nodes[idx];
+        if (nd.pos[nd.arity] - nd.pos[0] <= COUNT_SMALL) node_counters<K, false>(bufs, nd, variant, cmp, wr);
+    }
     for (int dd = 16; dd; dd >>= 1) {
         cmp += __shfl_xor_sync(PS_FULL, cmp, dd);
         wr += __shfl_xor_sync(PS_FULL, wr, dd);
