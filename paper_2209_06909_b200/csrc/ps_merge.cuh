@@ -874,6 +874,13 @@ constexpr uint32_t MAXSEG = 32;
 #ifndef PS_BULK_STORE
 #define PS_BULK_STORE 1
 #endif
+// PS_SOA_X=1: the first pass writes X || Y as SoA (a key array and a value
+// array) instead of (key, value) records, so the second pass's diagonal probes
+// read 4- or 8-byte keys at unit stride (fewer bank conflicts than key fields
+// of 8- or 16-byte records)
+#ifndef PS_SOA_X
+#define PS_SOA_X 1
+#endif
 
 template <class K>
 struct PipeLayout {
@@ -889,6 +896,9 @@ struct PipeLayout {
     static constexpr uint32_t SLOT = align16c(cmax(KEY_BYTES + VAL_BYTES, PADN * RECB));
     // scratch: first-pass records X || Y of every segment (or the 2-way output)
     static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
+    // SoA scratch (PS_SOA_X): keys at 0, values at XV
+    static constexpr uint32_t XV = align16c(PADN * (uint32_t)sizeof(K));
+    static_assert(XV + PADN * 4 <= SCRATCH, "SoA scratch must fit");
     static constexpr uint32_t NXR = PS_XR2 ? 2 : 1;  // scratch buffers (2: alternate by unit)
     // SoA output of a bulk-stored unit inside its slot: keys at 0, values at OV
     static constexpr uint32_t EPK = 16 / (uint32_t)sizeof(K);  // keys per 16 bytes
@@ -1042,6 +1052,29 @@ PS_DEV void single_merge_soa(RecCur<K>& c, K* outk, int32_t* outv) {
         const Rec<K> nx = c.r[takeA ? c.ia(c.i) : c.ib(c.j)];
         c.a = takeA ? nx : c.a;
         c.b = takeA ? c.b : nx;
+    }
+}
+
+// Pass into SoA outputs from SoA inputs (keys ok[t], values ov[t]).
+template <class K>
+PS_DEV void single_merge_soa(WinCur<K>& c, K* outk, int32_t* outv) {
+    if (c.o >= c.oe) return;
+    const uint32_t lo = diag_search(c);
+    c.i = lo;
+    c.j = c.o - lo;
+    c.heads();
+    K* ok = outk + c.base + c.o;
+    int32_t* ov = outv + c.base + c.o;
+#pragma unroll
+    for (uint32_t t = 0; t < pipe_vt<K>(); ++t) {
+        const bool takeA = c.i < c.la && (c.j >= c.lb || !(c.b < c.a));
+        ok[t] = takeA ? c.a : c.b;
+        ov[t] = *(takeA ? c.av + c.i : c.bv + c.j);
+        c.i += takeA;
+        c.j += !takeA;
+        const K nk = *(takeA ? c.ak + c.i : c.bk + c.j);
+        c.a = takeA ? nk : c.a;
+        c.b = takeA ? c.b : nk;
     }
 }
 
@@ -1393,6 +1426,24 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
         const bool single_pass = d.nseg == 1 && d.seg[0].w < 3;  // read before the slot is released
         uint8_t* sbase = smem + slot * LY::SLOT;
         Rec<K>* const orec = reinterpret_cast<Rec<K>*>(sbase);
+        // SoA first-pass scratch (PS_SOA_X): X || Y keys at xk, values at xv
+        K* const xk = reinterpret_cast<K*>(xr);
+        int32_t* const xv = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(xr) + LY::XV);
+        auto xcur = [&](uint32_t offa, uint32_t offb, uint32_t la, uint32_t lb, uint32_t base, uint32_t o,
+                        uint32_t oe) {
+            WinCur<K> c;
+            c.ak = xk + offa;
+            c.bk = xk + offb;
+            c.av = xv + offa;
+            c.bv = xv + offb;
+            c.la = la;
+            c.lb = lb;
+            c.o = o;
+            c.oe = oe;
+            c.base = base;
+            return c;
+        };
+        (void)xcur;
         auto wincur = [&](const PipeSeg& g, uint32_t a, uint32_t base, uint32_t o, uint32_t oe) {
             WinCur<K> c;
             c.ak = reinterpret_cast<const K*>(sbase + g.koff[a]);
@@ -1421,10 +1472,28 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
                 const bool isY = ob >= LXp;
                 WinCur<K> c = isY ? wincur(g, 2, LXp, ob - LXp, min(ob + VT - LXp, LYn))
                                   : wincur(g, 0, 0, ob, min(ob + VT, LX));
-                single_merge(c, xr);
+                if (PS_SOA_X)
+                    single_merge_soa(c, xk, xv);
+                else
+                    single_merge(c, xr);
                 PT_WARP(16)
                 consumer_sync<pipe_consumers<K>()>();
                 PT_MARK(5)
+                if (PS_SOA_X) {
+                    if (PS_BULK_STORE) {
+                        WinCur<K> q = xcur(0, LXp, LX, LYn, 0, o0, o1);
+                        single_merge_soa(q, reinterpret_cast<K*>(sbase) + (uint32_t)(out % LY::EPK),
+                                         reinterpret_cast<int32_t*>(sbase + LY::OV) + (uint32_t)(out % 4));
+                        fence_proxy_async_smem();
+                        PT_WARP(24)
+                        __syncwarp();
+                        PT_MARK(6)
+                        goto unit_done;
+                    }
+                    WinCur<K> q = xcur(0, LXp, LX, LYn, al, o0, o1);
+                    single_merge(q, orec);
+                    res = orec;
+                } else {
                 // pass 2: merge X and Y into the slot (its input windows are consumed)
                 RecCur<K> p0;
                 p0.r = xr;
@@ -1448,6 +1517,7 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
                 }
                 single_merge(p0, orec);
                 res = orec;
+                }
             } else {
                 // 2-way: merge(A, B) straight into scratch
                 WinCur<K> c = wincur(g, 0, al, o0, o1);
@@ -1504,7 +1574,10 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
                 const uint32_t o = ob - d.s1[pp];
                 if (o < Lp) {
                     WinCur<K> c = wincur(g, isY ? 2 : 0, d.s1[pp], o, min(o + VT, Lp));
-                    single_merge(c, xr);
+                    if (PS_SOA_X)
+                        single_merge_soa(c, xk, xv);
+                    else
+                        single_merge(c, xr);
                 }
             }
             PT_WARP(16)
@@ -1514,7 +1587,11 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
                 const uint32_t sg = last_le(d.s2, nseg, ob);
                 const PipeSeg& g = d.seg[sg];
                 const uint32_t o = ob - d.s2[sg];
-                if (o < g.T) {
+                if (o < g.T && PS_SOA_X) {
+                    WinCur<K> q = xcur(d.s1[2 * sg], d.s1[2 * sg + 1], g.lx, g.T - g.lx, d.s2[sg], o,
+                                       min(o + VT, g.T));
+                    single_merge(q, orec);
+                } else if (o < g.T) {
                     RecCur<K> p0;
                     p0.r = xr;
                     p0.offa = d.s1[2 * sg];
