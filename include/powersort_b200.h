@@ -145,17 +145,30 @@ int ps_node_power(int32_t k, int64_t n, int64_t b1, int64_t e1, int64_t b2, int6
 int64_t ps_run_stack_capacity(int64_t k, int64_t n);
 
 /* Multi-GPU cross-shard merge.  Every rank g of G sorted its
- * contiguous shard (ps_sort with the shard's own n); this call produces the
- * rank's slab of the globally sorted sequence, global ranks
- * [g*N/G, (g+1)*N/G), by reading the G shards directly (peer pointers over
- * NVLink P2P; no NCCL).  shard_keys[i]/shard_vals[i] are device pointers valid
- * on the current device (local or peer-mapped), shard_n[i] their lengths;
- * shard i holds global indices [sum_{j<i} shard_n[j], ...).  out_keys/out_vals
- * receive the slab.  Stable: ties ordered by shard then position. */
+ * contiguous shard (ps_sort with the shard's own n, payload = global index);
+ * this call produces the rank's slab of the globally sorted sequence, global
+ * ranks [out_begin, out_end) (normally [g*N/G, (g+1)*N/G)), in one pass that
+ * reads the G shards directly (peer pointers over NVLink P2P; no NCCL, no
+ * gathered copy).  shard_keys[i]/shard_vals[i] are device pointers valid on
+ * the current device (local or peer-mapped), shard_n[i] their lengths; shard
+ * i holds global indices [sum_{j<i} shard_n[j], ...).  shard_samples[i] is
+ * shard i's sample array (ps_shard_samples) or NULL (the samples are then
+ * read from the keys with a stride); shard_samples itself may be NULL.
+ * out_keys/out_vals receive the slab.  Stable: ties ordered by shard then
+ * position.  Stream-ordered; returns after one final synchronisation that
+ * reads the device error flags.  No reference counterpart: the reference is
+ * single-threaded; the merge is merges.py:204-275's stable
+ * k-way merge with k = G <= 8. */
 size_t ps_shard_merge_workspace_size(int32_t nshards, int64_t slab_n);
 int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys, const int32_t* const* shard_vals,
-                   const int64_t* shard_n, int64_t out_begin, int64_t out_end, void* out_keys, int32_t* out_vals,
-                   void* workspace, size_t workspace_bytes, void* stream);
+                   const void* const* shard_samples, const int64_t* shard_n, int64_t out_begin, int64_t out_end,
+                   void* out_keys, int32_t* out_vals, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Sample array of a sorted shard for ps_shard_merge: samples[i] = keys[i *
+ * stride], stride = 128 bytes of keys (32 four-byte or 16 eight-byte keys);
+ * ps_shard_sample_count gives the array length, ceil(n / stride). */
+int64_t ps_shard_sample_count(int32_t dtype, int64_t n);
+int ps_shard_samples(int32_t dtype, const void* keys, int64_t n, void* samples, void* stream);
 
 /* Payloads of any width: dst row i = src row perm[i], rows
  * of row_bytes bytes, for the permutation a PS_VALUES_ARGSORT sort returned.

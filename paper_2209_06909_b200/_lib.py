@@ -35,6 +35,8 @@ EXPORTS = (
     "ps_run_stack_capacity",
     "ps_shard_merge_workspace_size",
     "ps_shard_merge",
+    "ps_shard_sample_count",
+    "ps_shard_samples",
     "ps_gather_rows",
     "ps_profile_enable",
     "ps_profile_read",
@@ -127,8 +129,12 @@ def load():
     lib.ps_gather_rows.restype = i32
     lib.ps_shard_merge_workspace_size.argtypes = [i32, i64]
     lib.ps_shard_merge_workspace_size.restype = sz
-    lib.ps_shard_merge.argtypes = [i32, i32, vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]
+    lib.ps_shard_merge.argtypes = [i32, i32, vp, vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]
     lib.ps_shard_merge.restype = ctypes.c_int
+    lib.ps_shard_sample_count.argtypes = [i32, i64]
+    lib.ps_shard_sample_count.restype = i64
+    lib.ps_shard_samples.argtypes = [i32, vp, i64, vp, vp]
+    lib.ps_shard_samples.restype = ctypes.c_int
     lib.ps_profile_enable.argtypes = [i32]
     lib.ps_profile_enable.restype = ctypes.c_int
     lib.ps_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]

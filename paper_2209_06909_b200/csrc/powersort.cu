@@ -1081,12 +1081,23 @@ int check_impl(void* workspace, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// N6 cross-shard merge (ps_shard_merge)
+// N6 cross-shard merge (ps_shard_merge): bracketing selection of the slab's
+// ends, sample cuts, one merge launch (ps_shard.cuh).  No host round trip
+// until the final error check.
 struct ShardLayout {
-    uint64_t bounds, targets, err, lk, lv, tk, tv, nodes, c2n, cuts, bars, chunks_max, total;
+    uint64_t bounds, targets, err, plan, smp, rows, total, rows_cap, smp_cap;
 };
 
-ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
+// samples per cut for G shards: a chunk's bracketed windows, G * (m + 2) *
+// stride records, fit one unit of xm_cap records
+template <class K>
+uint32_t shard_cut_samples(uint32_t G) {
+    const int m = (int)(xm_cap<K>() / (G * xs_stride<K>())) - 2;
+    return (uint32_t)std::max(m, 1);
+}
+
+template <class K>
+ShardLayout shard_layout(uint64_t slab_n) {
     ShardLayout L;
     memset(&L, 0, sizeof(L));
     uint64_t off = 0;
@@ -1095,26 +1106,22 @@ ShardLayout shard_layout(uint64_t slab_n, uint64_t kb) {
         off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
         return o;
     };
-    L.chunks_max = 16 + cdiv(8 * slab_n, MIN_CUT_SPACING);
+    L.smp_cap = slab_n / xs_stride<K>() + MAX_SHARDS + 1;
+    L.rows_cap = slab_n / ((uint64_t)shard_cut_samples<K>(MAX_SHARDS) * xs_stride<K>()) + 2 * MAX_SHARDS + 2;
     L.bounds = take(2 * 2 * MAX_SHARDS * 8);
     L.targets = take(16);
     L.err = take(16);
-    L.lk = take(slab_n * kb);
-    L.lv = take(slab_n * 4);
-    L.tk = take(slab_n * kb);
-    L.tv = take(slab_n * 4);
-    L.nodes = take(4 * sizeof(Node));
-    L.c2n = take(L.chunks_max * 4);
-    L.cuts = take(L.chunks_max * 16);
-    L.bars = take(NBARS * 4);
+    L.plan = take(sizeof(XPlan));
+    L.smp = take(L.smp_cap * sizeof(K));
+    L.rows = take(L.rows_cap * sizeof(XRow<K>));
     L.total = off;
     return L;
 }
 
 template <class K>
 int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* const* shard_vals,
-                     const int64_t* shard_n, int64_t t0, int64_t t1, K* out_k, int32_t* out_v, uint8_t* ws,
-                     size_t wsb, cudaStream_t s) {
+                     const void* const* shard_samples, const int64_t* shard_n, int64_t t0, int64_t t1, K* out_k,
+                     int32_t* out_v, uint8_t* ws, size_t wsb, cudaStream_t s) {
     if (G < 1 || G > (int32_t)MAX_SHARDS) return fail(PS_EINVAL, "nshards must be in 1..8");
     if (!shard_keys || !shard_vals || !shard_n || !ws) return fail(PS_EINVAL, "NULL pointer argument");
     ShardSet<K> S;
@@ -1122,152 +1129,81 @@ int shard_merge_impl(int32_t G, const void* const* shard_keys, const int32_t* co
     S.G = (uint32_t)G;
     uint64_t N = 0;
     for (int32_t h = 0; h < G; ++h) {
-        if (shard_n[h] < 0) return fail(PS_EINVAL, "negative shard length");
+        if (shard_n[h] < 0 || shard_n[h] > ((int64_t)1 << 31)) return fail(PS_EINVAL, "shard length outside [0, 2^31]");
         S.k[h] = reinterpret_cast<const K*>(shard_keys[h]);
         S.v[h] = shard_vals[h];
+        S.smp[h] = shard_samples ? reinterpret_cast<const K*>(shard_samples[h]) : nullptr;
         S.n[h] = (uint64_t)shard_n[h];
-        S.off[h] = N;
         N += (uint64_t)shard_n[h];
     }
     if (t0 < 0 || t1 < t0 || (uint64_t)t1 > N) return fail(PS_EINVAL, "slab range outside [0, sum(shard_n)]");
     const uint64_t slab = (uint64_t)(t1 - t0);
     if (slab > ((uint64_t)1 << 31)) return fail(PS_EINVAL, "slab longer than 2^31");
-    const ShardLayout L = shard_layout(slab, sizeof(K));
+    const ShardLayout L = shard_layout<K>(slab);
     if (wsb < L.total) return fail(PS_ENOMEM, "shard-merge workspace too small");
     if (slab == 0) return PS_OK;
-    const uint32_t cap = cut_cap<K>();
-
-    // ---- co-ranks of t0 and t1 by parallel bracketing ---------------------------
-    unsigned long long hb[2][2][MAX_SHARDS];
-    uint64_t tg[2] = {(uint64_t)t0, (uint64_t)t1};
-    for (int t = 0; t < 2; ++t)
-        for (uint32_t h = 0; h < MAX_SHARDS; ++h) {
-            uint64_t lo = 0, hi = 0;
-            if (h < (uint32_t)G) {
-                const uint64_t rest = N - S.n[h];
-                lo = tg[t] > rest ? tg[t] - rest : 0;
-                hi = std::min<uint64_t>(S.n[h], tg[t]);
-            }
-            hb[t][0][h] = lo;
-            hb[t][1][h] = hi;
-        }
     unsigned long long* bounds = at<unsigned long long>(ws, L.bounds);
     uint64_t* targets = at<uint64_t>(ws, L.targets);
-    PS_CUDA(cudaMemcpyAsync(bounds, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
-    PS_CUDA(cudaMemcpyAsync(targets, tg, sizeof(tg), cudaMemcpyHostToDevice, s));
+    uint32_t* d_err = at<uint32_t>(ws, L.err);
+    XPlan* plan = at<XPlan>(ws, L.plan);
+    K* smp = at<K>(ws, L.smp);
+    XRow<K>* rows = at<XRow<K>>(ws, L.rows);
+    PS_CUDA(cudaMemsetAsync(d_err, 0, 4, s));
+
+    // ---- co-ranks of t0 and t1: fixed rounds of parallel bracketing ----------------
+    launch_k(xs_init_kernel<K>, 1, 32, 0, s, S, (uint64_t)t0, (uint64_t)t1, bounds, targets);
+    PS_LAUNCH_CHECK();
     uint64_t maxw = 1;
     for (int32_t h = 0; h < G; ++h) maxw = std::max<uint64_t>(maxw, S.n[h]);
-    int rounds = 2;
-    for (uint64_t w = maxw; w > 1; w = w / (SEL_CANDIDATES + 1) + 1) rounds++;
-    const dim3 sgrid(cdiv((uint64_t)G * SEL_CANDIDATES, 8), 2);
-    for (int pass = 0; pass < 4; ++pass) {
-        for (int it = 0; it < rounds; ++it) {
-            launch_k(shard_select_kernel<K>, sgrid, 256, 0, s, S, targets, bounds);
-            PS_LAUNCH_CHECK();
-        }
-        PS_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
-        PS_CUDA(cudaStreamSynchronize(s));
-        bool conv = true;
-        for (int t = 0; t < 2; ++t)
-            for (int32_t h = 0; h < G; ++h) conv &= hb[t][0][h] == hb[t][1][h];
-        if (conv) break;
-        if (pass == 3) return fail(PS_EINVARIANT, "shard co-rank selection did not converge");
+    int rounds = 2;  // a window of w <= SEL_CANDIDATES + 1 positions is resolved in one round
+    for (uint64_t w = maxw; w > SEL_CANDIDATES + 1; w = w / (SEL_CANDIDATES + 1) + 1) rounds++;
+    const dim3 sgrid((unsigned)cdiv((uint64_t)G * SEL_CANDIDATES, 8), 2);
+    for (int it = 0; it < rounds; ++it) {
+        launch_k(shard_select_kernel<K>, sgrid, 256, 0, s, S, (const uint64_t*)targets, bounds);
+        PS_LAUNCH_CHECK();
     }
-    uint64_t run_len[MAX_SHARDS], tot = 0;
-    for (int32_t h = 0; h < G; ++h) {
-        if (hb[1][0][h] < hb[0][0][h]) return fail(PS_EINVARIANT, "shard co-ranks not monotone");
-        run_len[h] = hb[1][0][h] - hb[0][0][h];
-        tot += run_len[h];
-    }
-    if (tot != slab) return fail(PS_EINVARIANT, "shard co-ranks do not sum to the slab");
-
-    // ---- gather the windows (peer loads over NVLink) into Lk/Lv ------------------
-    K* lk = at<K>(ws, L.lk);
-    int32_t* lv = at<int32_t>(ws, L.lv);
-    launch_k(shard_gather_kernel<K>, (unsigned)std::min<uint64_t>(cdiv(slab, 256), 148 * 16), 256, 0, s, 
-        S, bounds, bounds + 2 * MAX_SHARDS, lk, lv, slab);
+    // ---- plan, local sample windows, cuts -----------------------------------------
+    const uint32_t m = shard_cut_samples<K>((uint32_t)G);
+    launch_k(xs_plan_kernel<K>, 1, 32, 0, s, S, (const unsigned long long*)bounds, (uint64_t)t0, (uint64_t)t1, m,
+             plan, d_err);
     PS_LAUNCH_CHECK();
-
-    // ---- local merge of the nonempty windows -------------------------------------
-    std::vector<uint32_t> runs_off;  // boundaries of nonempty runs in L
-    uint64_t acc = 0;
-    for (int32_t h = 0; h < G; ++h) {
-        if (run_len[h]) runs_off.push_back((uint32_t)acc);
-        acc += run_len[h];
+    const unsigned sgrid2 = (unsigned)std::min<uint64_t>(cdiv(slab / xs_stride<K>() + 1, 256), 148 * 8);
+    launch_k(xs_sample_copy_kernel<K>, sgrid2, 256, 0, s, S, (const XPlan*)plan, smp);
+    PS_LAUNCH_CHECK();
+    const uint64_t max_cuts = L.rows_cap;
+    launch_k(xs_cuts_kernel<K>, (unsigned)std::min<uint64_t>(cdiv(max_cuts, 256), 148 * 8), 256, 0, s, S,
+             (const XPlan*)plan, (const K*)smp, rows);
+    PS_LAUNCH_CHECK();
+    // ---- one merge launch: two CTAs per SM ------------------------------------------
+    static bool attr_set = false;
+    const size_t smem = xm_smem_bytes<K>();
+    if (!attr_set) {
+        PS_CUDA(cudaFuncSetAttribute(xs_merge_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
     }
-    runs_off.push_back((uint32_t)acc);
-    const uint32_t R = (uint32_t)runs_off.size() - 1;
-    if (R <= 1) {
-        PS_CUDA(cudaMemcpyAsync(out_k, lk, slab * sizeof(K), cudaMemcpyDeviceToDevice, s));
-        PS_CUDA(cudaMemcpyAsync(out_v, lv, slab * 4, cudaMemcpyDeviceToDevice, s));
-        PS_CUDA(cudaStreamSynchronize(s));
-        return PS_OK;
-    }
-    auto make_node = [&](const uint32_t* pos, uint32_t arity, uint32_t parity) {
-        Node nd;
-        memset(&nd, 0, sizeof(nd));
-        for (uint32_t a = 0; a <= arity; ++a) nd.pos[a] = pos[a];
-        nd.arity = (uint8_t)arity;
-        nd.parity = (uint8_t)parity;
-        nd.probe = 0;
-        nd.nchunks = node_chunks(nd, cap, SMALL_KERNEL_MAX);
-        return nd;
-    };
-    std::vector<std::vector<Node>> levels;
-    if (R <= MAX_WAY) {
-        levels.push_back({make_node(runs_off.data(), R, 0)});
-    } else {
-        const uint32_t left = (R + 1) / 2;
-        levels.push_back({make_node(runs_off.data(), left, 1), make_node(runs_off.data() + left, R - left, 1)});
-        const uint32_t p2[3] = {runs_off[0], runs_off[left], runs_off[R]};
-        levels.push_back({make_node(p2, 2, 0)});
-    }
-    Node* d_nodes = at<Node>(ws, L.nodes);
-    uint32_t* d_c2n = at<uint32_t>(ws, L.c2n);
-    uint4* d_cuts = at<uint4>(ws, L.cuts);
-    uint32_t* d_err = at<uint32_t>(ws, L.err);
-    PS_CUDA(cudaMemsetAsync(d_err, 0, 4, s));
-    for (size_t lvl = 0; lvl < levels.size(); ++lvl) {
-        std::vector<Node>& nds = levels[lvl];
-        std::vector<uint32_t> c2n;
-        uint32_t nsmall = 0;
-        for (uint32_t i = 0; i < nds.size(); ++i) {
-            nds[i].chunk_base = (uint32_t)c2n.size();
-            for (uint32_t c = 0; c < nds[i].nchunks; ++c) c2n.push_back(i);
-            nsmall += nds[i].nchunks == 0;
-        }
-        if (c2n.size() > L.chunks_max) return fail(PS_ENOMEM, "shard-merge chunk table too small");
-        PS_CUDA(cudaMemcpyAsync(d_nodes, nds.data(), nds.size() * sizeof(Node), cudaMemcpyHostToDevice, s));
-        if (!c2n.empty())
-            PS_CUDA(cudaMemcpyAsync(d_c2n, c2n.data(), c2n.size() * 4, cudaMemcpyHostToDevice, s));
-        Bufs<K> b;
-        if (levels.size() == 1) {  // L -> out
-            b.k[0] = out_k;
-            b.v[0] = out_v;
-            b.k[1] = lk;
-            b.v[1] = lv;
-        } else if (lvl == 0) {  // L -> T
-            b.k[0] = lk;
-            b.v[0] = lv;
-            b.k[1] = at<K>(ws, L.tk);
-            b.v[1] = at<int32_t>(ws, L.tv);
-        } else {  // T -> out
-            b.k[0] = out_k;
-            b.v[0] = out_v;
-            b.k[1] = at<K>(ws, L.tk);
-            b.v[1] = at<int32_t>(ws, L.tv);
-        }
-        MergeRunner<K> mr;
-        int rc = mr.init(b, slab, d_nodes, d_c2n, d_cuts, d_err, at<uint32_t>(ws, L.bars), NBARS, s);
-        if (rc) return rc;
-        rc = mr.stage(0, (uint32_t)nds.size(), 0, (uint32_t)c2n.size(), nsmall, SMALL_NODE, nullptr, (int)lvl);
-        if (rc) return rc;
-        PS_CUDA(cudaStreamSynchronize(s));  // host node/chunk tables are reused by the next level
-    }
+    int dev = 0, nsm = 148;
+    PS_CUDA(cudaGetDevice(&dev));
+    PS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned mgrid = (unsigned)std::min<uint64_t>(2 * (uint64_t)nsm, cdiv(slab, xm_cap<K>() / 2) + 1);
+    launch_k(xs_merge_kernel<K>, mgrid, XM_THREADS, smem, s, S, (const XPlan*)plan, (const XRow<K>*)rows, out_k,
+             out_v, (uint64_t)t0, d_err);
+    PS_LAUNCH_CHECK();
     uint32_t herr = 0;
     PS_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
     if (herr) return fail(PS_EINVARIANT, "shard merge invariant violated (flags " + std::to_string(herr) + ")");
+    return PS_OK;
+}
+
+template <class K>
+int shard_samples_impl(const void* keys, int64_t n, void* samples, cudaStream_t s) {
+    if (n < 0) return fail(PS_EINVAL, "n must be >= 0");
+    if (n == 0) return PS_OK;
+    if (!keys || !samples) return fail(PS_EINVAL, "NULL pointer argument");
+    const uint64_t ns = cdiv((uint64_t)n, xs_stride<K>());
+    launch_k(xs_samples_kernel<K>, (unsigned)std::min<uint64_t>(cdiv(ns, 256), 148 * 8), 256, 0, s,
+             (const K*)keys, (uint64_t)n, (K*)samples);
+    PS_LAUNCH_CHECK();
     return PS_OK;
 }
 
@@ -1490,7 +1426,25 @@ int64_t ps_run_stack_capacity(int64_t k, int64_t n) {
 
 size_t ps_shard_merge_workspace_size(int32_t nshards, int64_t slab_n) {
     if (nshards < 1 || nshards > (int32_t)MAX_SHARDS || slab_n < 0) return 0;
-    return (size_t)shard_layout((uint64_t)slab_n, 8).total;
+    return (size_t)std::max(shard_layout<int32_t>((uint64_t)slab_n).total, shard_layout<int64_t>((uint64_t)slab_n).total);
+}
+
+int64_t ps_shard_sample_count(int32_t dtype, int64_t n) {
+    if (n < 0) return -PS_EINVAL;
+    const int64_t s = (dtype == PS_INT64 || dtype == PS_FLOAT64) ? 16 : (dtype == PS_INT32 || dtype == PS_FLOAT32) ? 32 : 0;
+    if (!s) return -PS_EINVAL;
+    return (n + s - 1) / s;
+}
+
+int ps_shard_samples(int32_t dtype, const void* keys, int64_t n, void* samples, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (dtype) {
+        case PS_INT32: return shard_samples_impl<int32_t>(keys, n, samples, s);
+        case PS_INT64: return shard_samples_impl<int64_t>(keys, n, samples, s);
+        case PS_FLOAT32: return shard_samples_impl<float>(keys, n, samples, s);
+        case PS_FLOAT64: return shard_samples_impl<double>(keys, n, samples, s);
+        default: return fail(PS_EINVAL, "unsupported dtype " + std::to_string(dtype));
+    }
 }
 
 int ps_gather_rows(const void* src, const int32_t* perm, void* dst, int64_t n, int64_t row_bytes, void* stream) {
@@ -1518,28 +1472,21 @@ int ps_gather_rows(const void* src, const int32_t* perm, void* dst, int64_t n, i
 }
 
 int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys, const int32_t* const* shard_vals,
-                   const int64_t* shard_n, int64_t out_begin, int64_t out_end, void* out_keys, int32_t* out_vals,
-                   void* workspace, size_t workspace_bytes, void* stream) {
+                   const void* const* shard_samples, const int64_t* shard_n, int64_t out_begin, int64_t out_end,
+                   void* out_keys, int32_t* out_vals, void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)workspace;
+#define PS_SM(K)                                                                                              \
+    return shard_merge_impl<K>(nshards, shard_keys, shard_vals, shard_samples, shard_n, out_begin, out_end, \
+                               (K*)out_keys, out_vals, ws, workspace_bytes, s)
     switch (dtype) {
-        case PS_INT32:
-            return shard_merge_impl<int32_t>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
-                                             (int32_t*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
-                                             (cudaStream_t)stream);
-        case PS_INT64:
-            return shard_merge_impl<int64_t>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
-                                             (int64_t*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
-                                             (cudaStream_t)stream);
-        case PS_FLOAT32:
-            return shard_merge_impl<float>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
-                                           (float*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
-                                           (cudaStream_t)stream);
-        case PS_FLOAT64:
-            return shard_merge_impl<double>(nshards, shard_keys, shard_vals, shard_n, out_begin, out_end,
-                                            (double*)out_keys, out_vals, (uint8_t*)workspace, workspace_bytes,
-                                            (cudaStream_t)stream);
-        default:
-            return fail(PS_EINVAL, "unsupported dtype " + std::to_string(dtype));
+        case PS_INT32: PS_SM(int32_t);
+        case PS_INT64: PS_SM(int64_t);
+        case PS_FLOAT32: PS_SM(float);
+        case PS_FLOAT64: PS_SM(double);
+        default: return fail(PS_EINVAL, "unsupported dtype " + std::to_string(dtype));
     }
+#undef PS_SM
 }
 
 }  // extern "C"

@@ -41,9 +41,25 @@ def plan(sizes, rank):
     return {"sizes": sizes, "offsets": offs[:-1], "total": total, "slab": (t0, t1)}
 
 
-def shard_merge(shard_keys, shard_vals, t0, t1, out_keys=None, out_vals=None):
+def shard_samples(keys, out=None):
+    """Sample array of a sorted shard (every 128 bytes of keys), the input
+    ps_shard_merge uses to cut the slab without peer searches."""
+    import torch
+
+    lib = _lib.load()
+    dt = _dtype_id(keys)
+    ns = int(lib.ps_shard_sample_count(dt, keys.numel()))
+    if out is None:
+        out = torch.empty(max(ns, 1), dtype=keys.dtype, device=keys.device)
+    stream = torch.cuda.current_stream(keys.device).cuda_stream
+    _lib.check(lib.ps_shard_samples(dt, keys.data_ptr(), keys.numel(), out.data_ptr(), stream))
+    return out
+
+
+def shard_merge(shard_keys, shard_vals, t0, t1, out_keys=None, out_vals=None, samples=None, workspace=None):
     """Slab [t0, t1) of the stable merge of the sorted shards (all tensors
-    addressable from the current device: local or peer-mapped)."""
+    addressable from the current device: local or peer-mapped).  ``samples``
+    are the shards' sample arrays (shard_samples) or None."""
     import torch
 
     lib = _lib.load()
@@ -59,52 +75,98 @@ def shard_merge(shard_keys, shard_vals, t0, t1, out_keys=None, out_vals=None):
         out_vals = torch.empty(n, dtype=torch.int32, device=dev)
     kp = (ctypes.c_void_p * G)(*[k.data_ptr() for k in shard_keys])
     vp = (ctypes.c_void_p * G)(*[v.data_ptr() for v in shard_vals])
+    sp = None if samples is None else (ctypes.c_void_p * G)(*[
+        (s.data_ptr() if s is not None and s.numel() else None) for s in samples])
     ns = (ctypes.c_int64 * G)(*[k.numel() for k in shard_keys])
-    nbytes = lib.ps_shard_merge_workspace_size(G, n)
-    ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+    nbytes = int(lib.ps_shard_merge_workspace_size(G, n))
+    ws = workspace
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    _lib.check(lib.ps_shard_merge(dt, G, kp, vp, ns, t0, t1, out_keys.data_ptr(), out_vals.data_ptr(),
+    _lib.check(lib.ps_shard_merge(dt, G, kp, vp, sp, ns, t0, t1, out_keys.data_ptr(), out_vals.data_ptr(),
                                   ws.data_ptr(), ws.numel(), stream))
     return out_keys, out_vals
+
+
+class DistributedSorter:
+    """Persistent multi-GPU sorter for one rank (one process per GPU).
+
+    Owns the rank's shard buffers (``keys``: fill it, then call ``sort``), the
+    global-index payload, the shard's sample array and the output slab.  The
+    CUDA IPC handles of the shard, payload and samples are exchanged once at
+    construction (``all_gather_object``, plumbing only) and the peers' buffers
+    stay mapped, so a sort is: local sort of the shard, its samples, a host
+    barrier, the single-pass cross-shard merge of this rank's slab (peer loads
+    over NVLink), and a closing barrier (peers keep their shards until every
+    slab is merged)."""
+
+    def __init__(self, n_local, dtype, config=None, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.config = config or SortConfig()
+        self.group = group
+        self.dist = dist
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        sizes = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(sizes, int(n_local), group=group)
+        else:
+            sizes = [int(n_local)]
+        self.plan = plan(sizes, self.rank)
+        off = self.plan["offsets"][self.rank]
+        self.keys = torch.empty(n_local, dtype=dtype, device=dev)
+        self.vals = torch.empty(n_local, dtype=torch.int32, device=dev)
+        self._iota = torch.arange(off, off + n_local, dtype=torch.int32, device=dev)
+        lib = _lib.load()
+        ns = int(lib.ps_shard_sample_count(_dtype_id(self.keys), n_local))
+        self.samples = torch.empty(max(ns, 1), dtype=dtype, device=dev)
+        t0, t1 = self.plan["slab"]
+        self.out_keys = torch.empty(t1 - t0, dtype=dtype, device=dev)
+        self.out_vals = torch.empty(t1 - t0, dtype=torch.int32, device=dev)
+        self.ws = torch.empty(max(int(lib.ps_shard_merge_workspace_size(self.world, t1 - t0)), 1),
+                              dtype=torch.uint8, device=dev)
+        self.peers = None
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, tuple(reduce_tensor(t) for t in (self.keys, self.vals, self.samples)),
+                                   group=group)
+            self.peers = []
+            for g, hs in enumerate(handles):
+                if g == self.rank:
+                    self.peers.append((self.keys, self.vals, self.samples))
+                else:
+                    self.peers.append(tuple(f(*a) for f, a in hs))
+
+    def sort(self):
+        """Sort the global array whose shard this rank holds in ``keys``;
+        returns (slab keys, slab global indices) views of this rank's slab."""
+        import torch
+
+        self.vals.copy_(self._iota)
+        if self.keys.numel():
+            _sort_tensor(self.keys, self.vals, self.config, _lib.VALUES_PERMUTE, collect_runs=False)
+        if self.world == 1:
+            return self.keys, self.vals
+        shard_samples(self.keys, self.samples)
+        torch.cuda.synchronize(self.keys.device)
+        self.dist.barrier(group=self.group)
+        t0, t1 = self.plan["slab"]
+        shard_merge([p[0] for p in self.peers], [p[1] for p in self.peers], t0, t1, self.out_keys, self.out_vals,
+                    samples=[p[2] if p[0].numel() else None for p in self.peers], workspace=self.ws)
+        torch.cuda.synchronize(self.keys.device)
+        self.dist.barrier(group=self.group)  # peers keep their shards alive until every slab is merged
+        return self.out_keys, self.out_vals
 
 
 def sort_distributed(keys, config=None, group=None):
     """Sort a globally sharded array: ``keys`` is this rank's contiguous shard
     (CUDA tensor).  Returns (slab_keys, slab_global_indices) of this rank's
-    slab of the global stable order."""
-    import torch
-    import torch.distributed as dist
-    from torch.multiprocessing.reductions import reduce_tensor
-
-    if config is None:
-        config = SortConfig()
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    sizes = [None] * world
-    if world > 1:
-        dist.all_gather_object(sizes, int(keys.numel()), group=group)
-    else:
-        sizes = [int(keys.numel())]
-    p = plan(sizes, rank)
-    off = p["offsets"][rank]
-    vals = torch.arange(off, off + keys.numel(), dtype=torch.int32, device=keys.device)
-    _sort_tensor(keys, vals, config, _lib.VALUES_PERMUTE, collect_runs=False)
-    if world == 1:
-        return keys, vals
-    torch.cuda.synchronize(keys.device)
-    handles = [None] * world
-    dist.all_gather_object(handles, (reduce_tensor(keys), reduce_tensor(vals)), group=group)
-    peers_k, peers_v = [], []
-    for g, ((fk, ak), (fv, av)) in enumerate(handles):
-        if g == rank:
-            peers_k.append(keys)
-            peers_v.append(vals)
-        else:
-            peers_k.append(fk(*ak))
-            peers_v.append(fv(*av))
-    t0, t1 = p["slab"]
-    out = shard_merge(peers_k, peers_v, t0, t1)
-    torch.cuda.synchronize(keys.device)
-    dist.barrier(group=group)  # peers keep their shards alive until every slab is merged
-    del peers_k, peers_v
-    return out
+    slab of the global stable order.  One-shot form of DistributedSorter."""
+    sorter = DistributedSorter(keys.numel(), keys.dtype, config, group, keys.device)
+    sorter.keys.copy_(keys)
+    k, v = sorter.sort()
+    return k, v

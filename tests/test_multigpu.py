@@ -123,6 +123,94 @@ def test_bracketing_selection_matches_stable_merge():
             assert c == expect, (trial, t)
 
 
+def _precedes(z, b, y, a):
+    """(b, key z) before (a, key y) in (key, shard) order (xs_precedes)."""
+    return z < y or (not (y < z) and b < a)
+
+
+def sample_cut_rows(shards, t0, t1, m, s):
+    """Python restatement of the device plan of ps_shard_merge (ps_shard.cuh:
+    xs_plan_kernel, xs_cuts_kernel): boundary rows (lo[], hi[], cut) in merged
+    order, from the exact co-ranks of t0 / t1 and rank searches among samples."""
+    G = len(shards)
+    c0 = bracket_select(shards, t0)
+    c1 = bracket_select(shards, t1)
+    cd = lambda a, b: -(-a // b)  # noqa: E731
+    w0 = [cd(c, s) for c in c0]
+    w1 = [cd(c, s) for c in c1]
+    j0 = [cd(w, m) for w in w0]
+    rows = {}
+    for a in range(G):
+        for j in range(j0[a], cd(w1[a], m)):
+            i = j * m
+            x = shards[a][i * s]
+            lo, hi, idx = [], [], 0
+            for b in range(G):
+                if b == a:
+                    rb = i
+                    lo.append(i * s)
+                    hi.append(i * s)
+                else:
+                    smp = shards[b][::s][w0[b]:w1[b]]
+                    r = 0
+                    while r < len(smp) and _precedes(smp[r], b, x, a):
+                        r += 1
+                    rb = w0[b] + r
+                    l_, h_ = ((rb - 1) * s + 1 if rb else 0), rb * s
+                    lo.append(min(max(l_, c0[b]), c1[b]))
+                    hi.append(min(max(h_, c0[b]), c1[b]))
+                idx += cd(rb, m) - j0[b]
+            assert idx not in rows
+            rows[idx] = (lo, hi, (x, a, i * s))
+    out = [(list(c0), list(c0), None)] + [rows[i] for i in range(len(rows))] + [(list(c1), list(c1), None)]
+    return out
+
+
+def _exact(shard, b, lo, hi, cut):
+    if cut is None or cut[1] == b:
+        return lo
+    x, a, _ = cut
+    q = lo
+    while q < hi and _precedes(shard[q], b, x, a):
+        q += 1
+    return q
+
+
+def test_sample_cuts_partition_the_slab():
+    """The rows of the device plan cut every slab into chunks whose bracketed
+    windows fit one unit, and the chunks' exact boundaries (resolved inside
+    the brackets, as xs_merge_kernel does in shared memory) reproduce the
+    stable merge."""
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        G = int(rng.integers(1, 9))
+        s = int(rng.choice([2, 4, 8]))
+        m = int(rng.integers(1, 5))
+        shards = []
+        for _ in range(G):
+            n = int(rng.integers(0, 300))
+            hi = int(rng.choice([3, 40, 10**6]))
+            shards.append(np.sort(rng.integers(0, hi, size=n)))
+        allk = np.concatenate(shards)
+        sid = np.concatenate([np.full(len(x), h) for h, x in enumerate(shards)])
+        pos = np.concatenate([np.arange(len(x)) for x in shards])
+        order = np.lexsort((sid, allk))
+        N = len(allk)
+        for W in (1, 2, 3):
+            for g in range(W):
+                t0, t1 = multigpu.slab_bounds(N, W, g)
+                rows = sample_cut_rows(shards, t0, t1, m, s)
+                E = [[_exact(shards[b], b, lo[b], hi[b], cut) for b in range(G)] for lo, hi, cut in rows]
+                got = []
+                for r in range(len(rows) - 1):
+                    loaded = sum(rows[r + 1][1][b] - rows[r][0][b] for b in range(G))
+                    assert loaded <= G * (m + 2) * s, (trial, loaded)
+                    part = [(shards[b][q], b, q) for b in range(G) for q in range(E[r][b], E[r + 1][b])]
+                    got += sorted(part, key=lambda t: (t[0], t[1], t[2]))
+                exp = [(allk[o], sid[o], pos[o]) for o in order[t0:t1]]
+                assert [(int(a), int(b), int(c)) for a, b, c in got] == [(int(a), int(b), int(c)) for a, b, c in exp]
+
+
 # --------------------------------------------------------------------- GPU
 torch = pytest.importorskip("torch")
 
@@ -153,15 +241,55 @@ def test_shard_merge_emulated_on_one_gpu(G, kind):
             stable_sort_with(k, SortConfig(), values=v)
         sk.append(k)
         sv.append(v)
+    smp = [multigpu.shard_samples(k) if k.numel() else None for k in sk] if G % 2 == 0 else None
     out_k, out_v = [], []
     for g in range(G):
         t0, t1 = multigpu.slab_bounds(n, G, g)
-        k, v = multigpu.shard_merge(sk, sv, t0, t1)
+        k, v = multigpu.shard_merge(sk, sv, t0, t1, samples=smp)
         out_k.append(k.cpu().numpy())
         out_v.append(v.cpu().numpy())
     perm = np.argsort(keys, kind="stable")
     assert np.array_equal(np.concatenate(out_v), perm)
     assert np.array_equal(np.concatenate(out_k), keys[perm])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["float32", "int64", "float64", "int32"])
+@pytest.mark.parametrize("G", [2, 7, 8])
+def test_shard_merge_dtypes_sizes_and_empty_shards(dtype, G):
+    """Slabs of 8 shards (some empty, some tiny) with many units per slab;
+    published samples; ties across shards; odd slab bounds."""
+    from paper_2209_06909_b200 import SortConfig, stable_sort_with
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(G * 31 + len(dtype))
+    sizes = rng.integers(0, 700_000, size=G)
+    sizes[rng.integers(0, G)] = 0
+    if G > 2:
+        sizes[(rng.integers(0, G) + 1) % G] = 17
+    n = int(sizes.sum())
+    if dtype.startswith("float"):
+        keys = (rng.integers(-5000, 5000, size=n) * 0.25).astype(dtype)
+    else:
+        keys = rng.integers(-3000, 3000, size=n).astype(dtype) * np.array(2**33 if dtype == "int64" else 1,
+                                                                          dtype=dtype)
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    sk, sv = [], []
+    for g in range(G):
+        a, b = int(bounds[g]), int(bounds[g + 1])
+        k = torch.from_numpy(keys[a:b].copy()).to(dev)
+        v = torch.arange(a, b, dtype=torch.int32, device=dev)
+        if k.numel():
+            stable_sort_with(k, SortConfig(), values=v)
+        sk.append(k)
+        sv.append(v)
+    smp = [multigpu.shard_samples(k) if k.numel() else None for k in sk]
+    perm = np.argsort(keys, kind="stable")
+    cuts = [0, 1, n // 3 + 5, n // 2, n - 1, n]
+    for t0, t1 in zip(cuts[:-1], cuts[1:]):
+        k, v = multigpu.shard_merge(sk, sv, t0, t1, samples=smp)
+        assert np.array_equal(v.cpu().numpy(), perm[t0:t1]), (t0, t1)
+        assert np.array_equal(k.cpu().numpy().view(np.uint8), keys[perm[t0:t1]].view(np.uint8)), (t0, t1)
 
 
 def _dist_worker(rank, world, port, n, q):
