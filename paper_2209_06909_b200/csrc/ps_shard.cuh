@@ -41,19 +41,21 @@ template <class K>
 PS_DEV __host__ constexpr uint32_t xs_stride() {
     return 128u / (uint32_t)sizeof(K);
 }
-// merge geometry: two CTAs per SM (one loads while the other merges)
+// merge geometry: two CTAs per SM (one loads while the other merges).  A
+// thread produces VT consecutive outputs of every pass; VT is odd, so the
+// k-th outputs of a warp's lanes land in distinct banks.
 constexpr uint32_t XM_THREADS = 256;
 template <class K>
-PS_DEV __host__ constexpr uint32_t xm_cap() {  // loaded records per unit
-    return sizeof(K) == 4 ? 4096u : 2560u;
-}
-template <class K>
 PS_DEV __host__ constexpr uint32_t xm_vt() {
-    return xm_cap<K>() / XM_THREADS;
+    return sizeof(K) == 4 ? 15u : 9u;
 }
 template <class K>
-PS_DEV __host__ constexpr size_t xm_smem_bytes() {  // three SoA record buffers
-    return 3 * (size_t)xm_cap<K>() * (sizeof(K) + 4);
+PS_DEV __host__ constexpr uint32_t xm_cap() {  // loaded records per unit
+    return xm_vt<K>() * XM_THREADS;
+}
+template <class K>
+PS_DEV __host__ constexpr size_t xm_smem_bytes() {  // three SoA record buffers (+ over-read slack)
+    return 3 * (size_t)xm_cap<K>() * (sizeof(K) + 4) + 128;
 }
 
 template <class K>
@@ -314,6 +316,8 @@ PS_DEV void cp_async8(void* dst, const void* src) {
 PS_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Merge-path outputs [o, oe) of merge(A, B) (ties to A) into (ok, ov)[o...].
+// The heads live in registers; a read one past a run's end stays inside the
+// CTA's shared memory (the next run, the next buffer or the slack).
 template <class K>
 PS_DEV void xs_merge_piece(const K* ak, const int32_t* av, uint32_t la, const K* bk, const int32_t* bv,
                            uint32_t lb, uint32_t o, uint32_t oe, K* ok, int32_t* ov) {
@@ -325,12 +329,16 @@ PS_DEV void xs_merge_piece(const K* ak, const int32_t* av, uint32_t la, const K*
         hi = le ? hi : mid;
     }
     uint32_t i = lo, j = o - lo;
+    K a = ak[i], b = bk[j];
     for (; o < oe; ++o) {
-        const bool ta = i < la && (j >= lb || !(bk[j] < ak[i]));
-        ok[o] = ta ? ak[i] : bk[j];
-        ov[o] = ta ? av[i] : bv[j];
+        const bool ta = i < la && (j >= lb || !(b < a));
+        ok[o] = ta ? a : b;
+        ov[o] = *(ta ? av + i : bv + j);
         i += ta;
         j += !ta;
+        const K nk = *(ta ? ak + i : bk + j);
+        a = ta ? nk : a;
+        b = ta ? b : nk;
     }
 }
 
@@ -359,49 +367,62 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
     const uint32_t nch = nrows - 1;
     const uint32_t cbeg = (uint32_t)(((uint64_t)nch * blockIdx.x) / gridDim.x);
     const uint32_t cend = (uint32_t)(((uint64_t)nch * (blockIdx.x + 1)) / gridDim.x);
-    for (uint32_t c = cbeg; c < cend;) {
-        // ---- pack chunks c .. c2-1 (rows c .. c2) into a unit of <= CAP loaded records
-        if (tid < 32) {
-            const uint32_t r = c + 1 + lane;
-            uint32_t tot = INF32;
-            if (r <= cend) {
-                tot = 0;
-                for (uint32_t b = 0; b < G; ++b) tot += rows[r].hi[b] - rows[c].lo[b];
+    // warp 0: pack chunks c .. c2-1 (rows c .. c2) into a unit of <= CAP loaded
+    // records; its bracketed window of shard b is [s_L[b], s_L[b] + len) at
+    // buffer offset s_off[b]
+    auto pack = [&](uint32_t c) {
+        const uint32_t r = c + 1 + lane;
+        uint32_t tot = INF32;
+        if (r <= cend) {
+            tot = 0;
+            for (uint32_t b = 0; b < G; ++b) tot += rows[r].hi[b] - rows[c].lo[b];
+        }
+        const uint32_t fit = __ballot_sync(PS_FULL, tot <= CAP);
+        const uint32_t nfit = __ffs(~fit) ? __ffs(~fit) - 1 : 32;  // leading chunks that fit
+        const uint32_t c2 = c + max(nfit, 1u);
+        if (lane == 0) {
+            if (nfit == 0) atomicOr(err, ERR_CUT);
+            s_next = c2;
+        }
+        if (lane < MAX_SHARDS) {
+            const uint32_t L = lane < G ? rows[c].lo[lane] : 0;
+            const uint32_t H = lane < G ? rows[c2].hi[lane] : 0;
+            s_L[lane] = L;
+            uint32_t inc = H - L;
+            for (int d = 1; d < 8; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFu, inc, d);
+                if (lane >= (uint32_t)d) inc += y;
             }
-            const uint32_t fit = __ballot_sync(PS_FULL, tot <= CAP);
-            const uint32_t nfit = __ffs(~fit) ? __ffs(~fit) - 1 : 32;  // leading chunks that fit
-            if (lane == 0) {
-                if (nfit == 0) atomicOr(err, ERR_CUT);
-                s_next = c + max(nfit, 1u);
-            }
-            if (lane < MAX_SHARDS) {
-                const uint32_t c2 = c + max(nfit, 1u);
-                const uint32_t L = lane < G ? rows[c].lo[lane] : 0;
-                const uint32_t H = lane < G ? rows[c2].hi[lane] : 0;
-                s_L[lane] = L;
-                uint32_t len = H - L, inc = len;
-                for (int d = 1; d < 8; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xFFu, inc, d);
-                    if (lane >= (uint32_t)d) inc += y;
-                }
-                s_off[lane + 1] = inc;
-                if (lane == 0) s_off[0] = 0;
+            s_off[lane + 1] = min(inc, CAP);
+            if (lane == 0) s_off[0] = 0;
+        }
+    };
+    // all threads: asynchronous copies of the packed windows into buffer 0
+    auto issue_loads = [&]() {
+        for (uint32_t b = 0; b < G; ++b) {
+            const uint32_t e0 = s_off[b], e1 = s_off[b + 1];
+            const int64_t sh = (int64_t)s_L[b] - (int64_t)e0;  // shard position of buffer slot e: e + sh
+            const K* __restrict__ gk = S.k[b] + sh;
+            const int32_t* __restrict__ gv = S.v[b] + sh;
+            for (uint32_t e = e0 + tid; e < e1; e += XM_THREADS) {
+                if (sizeof(K) == 4)
+                    cp_async4(BK(0) + e, gk + e);
+                else
+                    cp_async8(BK(0) + e, gk + e);
+                cp_async4(BV(0) + e, gv + e);
             }
         }
+    };
+    if (cbeg < cend) {
+        if (tid < 32) pack(cbeg);
         __syncthreads();
+        issue_loads();
+    }
+    // Software pipeline: the next unit's windows are loaded into buffer 0 as
+    // soon as the first pass has consumed it, while the later passes and the
+    // store of the current unit run on buffers 1 and 2.
+    for (uint32_t c = cbeg; c < cend;) {
         const uint32_t c2 = s_next;
-        const uint32_t tot = min(s_off[MAX_SHARDS], CAP);
-        // ---- load the bracketed windows (asynchronous copies, peers over NVLink)
-        for (uint32_t e = tid; e < tot; e += XM_THREADS) {
-            uint32_t b = 0;
-            while (b + 1 < G && e >= s_off[b + 1]) ++b;
-            const uint64_t q = (uint64_t)s_L[b] + (e - s_off[b]);
-            if (sizeof(K) == 4)
-                cp_async4(BK(0) + e, S.k[b] + q);
-            else
-                cp_async8(BK(0) + e, S.k[b] + q);
-            cp_async4(BV(0) + e, S.v[b] + q);
-        }
         cp_async_wait_all();
         __syncthreads();
         // ---- exact boundaries inside the loaded windows (threads 0..G-1: row c,
@@ -440,7 +461,8 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
         __syncthreads();
         // ---- pairwise merge passes: buffer 0 -> 1 -> 2 -> 1 ...
         uint32_t R = G, src = 0, dst = 1;
-        uint32_t U = s_ro[G];
+        const uint32_t U = s_ro[G];
+        bool prefetched = false;
         while (R > 1) {
             const uint32_t Rn = (R + 1) / 2;
             // output pair q at compact offset sum(len of runs < 2q)
@@ -458,8 +480,8 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
                     break;
                 }
                 const uint32_t ra = s_ro[2 * q], rb = 2 * q + 1 < R ? s_ro[2 * q + 1] : ra;
-                xs_merge_piece<K>(BK(src) + ra, BV(src) + ra, la, BK(src) + rb, BV(src) + rb, lb, o - base, pe - base,
-                                  BK(dst) + base, BV(dst) + base);
+                xs_merge_piece<K>(BK(src) + ra, BV(src) + ra, la, BK(src) + rb, BV(src) + rb, lb, o - base,
+                                  pe - base, BK(dst) + base, BV(dst) + base);
                 o = pe;
             }
             __syncthreads();
@@ -472,19 +494,38 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
                     base += pl;
                 }
             }
-            __syncthreads();
+            if (!prefetched) {  // buffer 0 is consumed: pack and load the next unit
+                prefetched = true;
+                if (tid < 32 && c2 < cend) pack(c2);
+                __syncthreads();
+                if (c2 < cend) issue_loads();
+            } else {
+                __syncthreads();
+            }
             R = Rn;
             src = dst;
             dst = dst == 1 ? 2 : 1;
         }
-        // ---- store the unit (src holds the merged records, compact from s_ro[0])
-        const uint64_t ob = s_out;
-        const uint32_t r0 = s_ro[0];
-        for (uint32_t e = tid; e < U; e += XM_THREADS) {
-            out_k[ob + e] = BK(src)[r0 + e];
-            out_v[ob + e] = BV(src)[r0 + e];
+        if (!prefetched) {  // G == 1: the unit is stored straight from buffer 0
+            const uint64_t ob = s_out;
+            const uint32_t r0 = s_ro[0];
+            for (uint32_t e = tid; e < U; e += XM_THREADS) {
+                out_k[ob + e] = BK(0)[r0 + e];
+                out_v[ob + e] = BV(0)[r0 + e];
+            }
+            __syncthreads();
+            if (tid < 32 && c2 < cend) pack(c2);
+            __syncthreads();
+            if (c2 < cend) issue_loads();
+        } else {
+            // ---- store the unit (src holds the merged records, compact from s_ro[0])
+            const uint64_t ob = s_out;
+            const uint32_t r0 = s_ro[0];
+            for (uint32_t e = tid; e < U; e += XM_THREADS) {
+                out_k[ob + e] = BK(src)[r0 + e];
+                out_v[ob + e] = BV(src)[r0 + e];
+            }
         }
-        __syncthreads();  // the next unit reuses buffer 0 and the descriptors
         c = c2;
     }
 }
