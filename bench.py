@@ -123,8 +123,13 @@ def load_traffic(config, n):
     try:
         with open(paths[-1]) as f:
             t = json.load(f)
-        return {"dram_bytes_per_launch": t["dram_bytes_per_launch"], "launches": t["launches"],
-                "dram_bytes_per_step": t["dram_bytes_total"], "source": os.path.relpath(paths[-1], REPO)}
+        out = {"dram_bytes_per_launch": t["dram_bytes_per_launch"], "launches": t["launches"],
+               "dram_bytes_per_step": t["dram_bytes_total"], "source": os.path.relpath(paths[-1], REPO)}
+        if "traffic_incl_writeback_per_launch" in t:
+            # DRAM reads + L2 write sectors: the writes still in L2 when a launch ends count too
+            out["incl_writeback_bytes_per_launch"] = t["traffic_incl_writeback_per_launch"]
+            out["incl_writeback_bytes_per_step"] = t["traffic_incl_writeback_total"]
+        return out
     except Exception:
         return None
 
@@ -629,6 +634,8 @@ def run_ours(args):
     traffic = load_traffic(args.config, n)
     if traffic:
         traffic["dram_over_algorithmic"] = traffic["dram_bytes_per_step"] / (merge_bytes / K) if merge_bytes else None
+        if "incl_writeback_bytes_per_step" in traffic and merge_bytes:
+            traffic["incl_writeback_over_algorithmic"] = traffic["incl_writeback_bytes_per_step"] / (merge_bytes / K)
     roofline = {
         "bound": "hbm",
         "kernel": "merge_pipe_kernel + small/tiny merge kernels (all merge launches of a step)",

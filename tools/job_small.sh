@@ -1,5 +1,10 @@
 #!/bin/bash
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
-out=gpurun_out/small_ab.txt; : > $out
-for c in cfg4 cfg1 cfg2 cfg3; do for E in PS_OLD_SMALL=1 PS_NONE=1; do env $E python tools/marginal.py $c | sed "s|^|$E |" >> $out; done; done
-python tools/stage_profile.py cfg4 > gpurun_out/stage_cfg4.txt 2>&1
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+( timeout 900 python -m pytest tests/test_reference_suite.py -q -rA ) > gpurun_out/pytest_refsuite.log 2>&1
+tail -3 gpurun_out/pytest_refsuite.log
+for c in cfg1 cfg4; do python tools/stage_profile.py $c > gpurun_out/stages_$c.txt 2>&1; done
+for c in cfg1 cfg4; do PS_LIB=$PWD/paper_2209_06909_b200/libpowersort_b200_debug.so python tools/marginal.py $c; done > gpurun_out/marginal.txt 2>&1
+for s in -3 -2 -1 0; do PS_LIB=$PWD/paper_2209_06909_b200/libpowersort_b200_debug.so PS_DEBUG_STAGES=$s python tools/marginal.py cfg1; done >> gpurun_out/marginal.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg1.csv python tools/one_sort.py cfg1 > /dev/null 2>&1
+python tools/host_time.py cfg1 > gpurun_out/host_time_cfg1.txt 2>&1
