@@ -22,7 +22,7 @@ whole runs; smaller configs: the whole input).
 
 Multi-GPU (torchrun, one process per GPU): strong scaling of the same global
 input -- rank g holds the contiguous shard [g n/G, (g+1) n/G) -- sorted per
-shard and merged across shards over NVLink P2P (multigpu.sort_distributed);
+shard and merged across shards over NVLink P2P (multigpu.DistributedSorter);
 the time is the max over ranks.
 """
 
