@@ -133,22 +133,48 @@ struct HostMap {
 thread_local HostMap g_map;
 
 // Copies the 32-bit words of a || b (each zero-padded to 16 bytes) to mapped
-// host memory, three per 16-byte store with the sequence number as the fourth:
-// a 16-byte store arrives whole, so the host knows every word once every store
-// carries seq.  (No system-scope fence: it would wait behind the bulk host
-// copies other streams keep on the link.)
+// host memory, three per 16-byte store with the sequence number as the fourth,
+// then one more record with two checksums of all the words.  The host waits
+// until every record carries seq and the checksums match: a 16-byte store that
+// reached the host torn (tag before data) is caught and re-read.  (No
+// system-scope fence: it would wait behind the bulk host copies other streams
+// keep on the link.)
+__host__ __device__ inline void publish_mix(uint32_t w, uint32_t i, uint32_t& s1, uint32_t& s2) {
+    s1 += w * (2u * i + 1u);
+    s2 ^= (w << (i & 15u)) | (w >> ((32u - (i & 15u)) & 31u));
+}
 __global__ void publish_kernel(const uint32_t* __restrict__ a, uint32_t na, const uint32_t* __restrict__ b,
                                uint32_t nb, uint4* __restrict__ dst, uint32_t seq) {
     pdl_wait();
     const uint32_t nw = na + nb, ns = (nw + 2) / 3;
+    uint32_t s1 = 0, s2 = 0;
     for (uint32_t q = threadIdx.x; q < ns; q += blockDim.x) {
         uint32_t v[3];
 #pragma unroll
         for (uint32_t t = 0; t < 3; ++t) {
             const uint32_t w = 3 * q + t;
             v[t] = w < na ? a[w] : (w < nw ? b[w - na] : 0u);
+            publish_mix(v[t], w, s1, s2);
         }
         dst[q] = make_uint4(v[0], v[1], v[2], seq);
+    }
+    __shared__ uint32_t r1[32], r2[32];
+    for (int d = 16; d; d >>= 1) {
+        s1 += __shfl_xor_sync(PS_FULL, s1, d);
+        s2 ^= __shfl_xor_sync(PS_FULL, s2, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        r1[threadIdx.x >> 5] = s1;
+        r2[threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t1 = 0, t2 = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            t1 += r1[w];
+            t2 ^= r2[w];
+        }
+        dst[ns] = make_uint4(t1, t2, ns, seq);
     }
 }
 
@@ -181,6 +207,8 @@ int host_map_ensure(size_t bytes) {
 // unpacks the bytes.  Sources are 16-byte aligned workspace regions.
 struct Pending {
     uint32_t seq = 0;
+    const void* a_src = nullptr;  // device sources (the fallback copy)
+    const void* b_src = nullptr;
     size_t abytes = 0, bbytes = 0;
     void* a_out = nullptr;
     void* b_out = nullptr;
@@ -189,12 +217,14 @@ int publish_begin(const void* a, size_t abytes, void* a_out, const void* b, size
                   cudaStream_t s, Pending& pend) {
     const size_t na = (abytes + 15) / 16 * 4, nb = (bbytes + 15) / 16 * 4;
     const size_t ns = (na + nb + 2) / 3;
-    int rc = host_map_ensure(ns * 16);
+    int rc = host_map_ensure((ns + 1) * 16);
     if (rc) return rc;
     const uint32_t seq = ++g_map.seq;
     PS_CUDA(launch_k(publish_kernel, 1, 256, 0, s, (const uint32_t*)a, (uint32_t)na, (const uint32_t*)b,
                      (uint32_t)nb, (uint4*)g_map.d, seq));
     pend.seq = seq;
+    pend.a_src = a;
+    pend.b_src = b;
     pend.abytes = abytes;
     pend.bbytes = bbytes;
     pend.a_out = a_out;
@@ -206,21 +236,39 @@ int publish_wait(const Pending& pend, cudaStream_t s) {
     const size_t ns = (na + nb + 2) / 3;
     const volatile uint32_t* hw = reinterpret_cast<const volatile uint32_t*>(g_map.h);
     auto arrived = [&]() {
-        for (size_t q = ns; q-- > 0;)  // the last stores are the likeliest to be missing
+        for (size_t q = ns + 1; q-- > 0;)  // the last stores are the likeliest to be missing
             if (hw[4 * q + 3] != pend.seq) return false;
         return true;
     };
-    for (uint32_t spins = 1; !arrived(); ++spins) {
+    std::vector<uint32_t> tmp(na + nb);
+    auto consistent = [&]() {  // every word read once, against the checksum record
+        std::atomic_thread_fence(std::memory_order_acquire);
+        uint32_t s1 = 0, s2 = 0;
+        for (size_t w = 0; w < ns * 3; ++w) {
+            const uint32_t v = hw[4 * (w / 3) + (w % 3)];
+            if (w < na + nb) tmp[w] = v;
+            publish_mix(v, (uint32_t)w, s1, s2);
+        }
+        return s1 == hw[4 * ns] && s2 == hw[4 * ns + 1];
+    };
+    bool ok = false;
+    for (uint32_t spins = 1;; ++spins) {
+        if (arrived() && consistent()) {
+            ok = true;
+            break;
+        }
         if ((spins & 255u) == 0) {  // a failed stream never delivers
             const cudaError_t e = cudaStreamQuery(s);
             if (e != cudaSuccess && e != cudaErrorNotReady) PS_CUDA(e);
-            if (e == cudaSuccess && !arrived()) return fail(PS_EINVARIANT, "published summary did not arrive");
+            if (e == cudaSuccess && !(arrived() && consistent())) break;  // done, but not (yet) coherent here
         }
     }
-    std::atomic_thread_fence(std::memory_order_acquire);
-    auto word = [&](size_t w) -> uint32_t { return hw[4 * (w / 3) + (w % 3)]; };
-    std::vector<uint32_t> tmp(na + nb);
-    for (size_t w = 0; w < na + nb; ++w) tmp[w] = word(w);
+    if (!ok) {
+        // the stream has finished: read the device sources directly
+        PS_CUDA(cudaStreamSynchronize(s));
+        PS_CUDA(cudaMemcpy(tmp.data(), pend.a_src, na * 4, cudaMemcpyDeviceToHost));
+        if (nb) PS_CUDA(cudaMemcpy(tmp.data() + na, pend.b_src, nb * 4, cudaMemcpyDeviceToHost));
+    }
     memcpy(pend.a_out, tmp.data(), pend.abytes);
     if (pend.bbytes) memcpy(pend.b_out, tmp.data() + na, pend.bbytes);
     return PS_OK;

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
                                                               uint32_t* err) {
     pdl_wait();
     constexpr uint32_t CAP = xm_cap<K>(), VT = xm_vt<K>();
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     // buffer q: CAP keys then CAP values
     auto BK = [&](uint32_t q) { return reinterpret_cast<K*>(smem + (size_t)q * CAP * (sizeof(K) + 4)); };
     auto BV = [&](uint32_t q) {

@@ -1,9 +1,11 @@
 """Pinned H2D and D2H copies of the e2e workload's sizes, alone and
 concurrently on two streams: the PCIe bound of bench.py's e2e step.
-usage: python tools/copy_duplex.py"""
+usage: python tools/copy_duplex.py [log2 n]   (24: cfg2, 31: cfg5)"""
+import sys
+
 import torch
 dev = torch.device('cuda', 0)
-n = 1 << 24
+n = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 24)
 h_in = torch.empty(n, dtype=torch.int32).pin_memory()
 h_out = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(2)]
 d_in = torch.empty(n, dtype=torch.int32, device=dev)
@@ -31,6 +33,10 @@ def run(h2d, d2h, reps=20):
     return a.elapsed_time(b) / reps
 
 
-run(True, True, 3)
-for name, h, d in (("H2D 64 MB", True, False), ("D2H 128 MB", False, True), ("both", True, True)):
-    print("%-12s %.3f ms per step" % (name, run(h, d)))
+reps = 20 if n <= (1 << 26) else 3
+run(True, True, 1)
+for name, h, d in (("H2D %d MB" % (4 * n >> 20), True, False), ("D2H %d MB" % (8 * n >> 20), False, True),
+                   ("both", True, True)):
+    ms = run(h, d, reps)
+    print("%-12s %.3f ms per step (%.1f GB/s H2D, %.1f GB/s D2H)" % (
+        name, ms, 4 * n / ms / 1e6 if h else 0, 8 * n / ms / 1e6 if d else 0), flush=True)
