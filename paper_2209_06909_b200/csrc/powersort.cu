@@ -980,7 +980,7 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             auto go = [&](auto kern, size_t wsm) -> int {
                 PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
                 launch_k(kern, wg, FORM_THREADS, wsm, s, bufs, (const uint32_t*)b, (const uint32_t*)nat,
-                         (const uint8_t*)leafpar, r, counting ? sum : nullptr);
+                         (const uint8_t*)leafpar, r, (const uint32_t*)ty, (uint64_t)n, counting ? sum : nullptr);
                 return PS_OK;
             };
             if (argsort) {

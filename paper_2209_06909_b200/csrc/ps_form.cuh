@@ -175,6 +175,7 @@ template <class K, int S, bool ARGSORT>
 __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs, const uint32_t* __restrict__ b,
                                                                     const uint32_t* __restrict__ nat,
                                                                     const uint8_t* __restrict__ leafpar, uint32_t r,
+                                                                    const uint32_t* __restrict__ ty, uint64_t n,
                                                                     Summary* __restrict__ counters) {
     pdl_wait();
     extern __shared__ __align__(128) uint8_t smem[];
@@ -212,6 +213,13 @@ __global__ void __launch_bounds__(FORM_THREADS) form_windows_kernel(Bufs<K> bufs
     }
     if (counters) {
         unsigned long long c_cmp = 0, c_mov = 0;
+        // the window's natural run (runs.py:23-47): its pair compares plus the
+        // failing one before the array end; a strictly descending one is reversed
+        if (len && nprefix >= 2) {
+            c_cmp += nprefix - 1 + ((uint64_t)b0 + nprefix < n ? 1 : 0);
+            const uint64_t q = (uint64_t)b0 + 1;
+            if (!((ty[q >> 5] >> (q & 31)) & 1u)) c_mov += nprefix;
+        }
 #pragma unroll
         for (int q = 1; q < S; ++q) {
             uint32_t sh = 0;
@@ -345,9 +353,9 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
     const uint64_t span0 = (uint64_t)tb * FORM_TILE, span1 = min((uint64_t)te * FORM_TILE, n);
     locate(tb, te, span0, span1);
     const bool whole = net && s_cnt <= 16;
-    if (net && !whole && !counters) {
-        // spans made only of extended windows (form_windows_kernel's) have nothing to do
-        // (unless their detection compares are counted)
+    if (net && !whole) {
+        // spans made only of extended windows (form_windows_kernel's, which also
+        // counts their detection compares) have nothing to do
         bool anynat = false;
         for (uint32_t i = tid; i < s_cnt; i += FORM_THREADS) {
             const uint32_t j = s_first + i;
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(FORM_THREADS, 3) form_leaves_kernel(Bufs<K> bu
             const uint64_t bj = sb[i];
             if (bj < t0) continue;  // counted by the tile it starts in
             const uint32_t nj = snat[i];
+            if (net && nj < sb[i + 1] - bj) continue;  // an extended window: form_windows_kernel counts it
             if (nj >= 2) {
                 c_cmp += nj - 1 + (bj + nj < n ? 1 : 0);
                 const uint64_t q = bj + 1;

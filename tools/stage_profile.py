@@ -1,5 +1,5 @@
 """Per-stage CUDA-event profile of one sort (diagnostics; run on the GPU box).
-usage: python tools/stage_profile.py [cfg2] [n]"""
+usage: python tools/stage_profile.py [cfg2] [n] [nocount]"""
 import sys
 import torch
 sys.path.insert(0, '.')
@@ -7,7 +7,8 @@ from paper_2209_06909_b200 import SortConfig, _lib, workloads
 from paper_2209_06909_b200.policy import _sort_tensor
 
 name = sys.argv[1] if len(sys.argv) > 1 else 'cfg2'
-n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+n = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "0" else None
+count = not (len(sys.argv) > 3 and sys.argv[3] == "nocount")
 keys_np = workloads.generate(name, n=n)
 dev = torch.device('cuda', 0)
 src = torch.from_numpy(keys_np).to(dev)
@@ -18,7 +19,7 @@ for it in range(3):
     keys.copy_(src)
     torch.cuda.synchronize()
     lib.ps_profile_enable(1)
-    _sort_tensor(keys, perm, SortConfig(), _lib.VALUES_ARGSORT, collect_runs=False)
+    _sort_tensor(keys, perm, SortConfig(count_comparisons=count), _lib.VALUES_ARGSORT, collect_runs=False)
     lib.ps_profile_enable(0)
 prof = _lib.profile_read()
 tot = 0
