@@ -88,3 +88,43 @@ def test_cfg5_full_size(dev):
     assert scanned_elements_estimate(stats, n) == 4 * cost + 2 * n
     # and the device tree builder on the same profile
     assert merge_cost_for_profile(runs.tolist(), 4) == cost
+
+
+def _adversarial(kind, n, seed=7):
+    rng = np.random.default_rng(seed)
+    if kind == "equal":
+        return np.full(n, 5, dtype=np.int32)  # one run, every key tied
+    if kind == "descending":
+        return np.arange(n, 0, -1, dtype=np.int32)  # one strictly descending run (reversed)
+    if kind == "zigzag":
+        return np.tile(np.array([1, 0], dtype=np.int32), n // 2) + np.repeat(
+            np.arange(n // 2, dtype=np.int32), 2)  # runs of two, every leaf an extended window
+    if kind == "organ":
+        h = np.arange(n // 2, dtype=np.int32)
+        return np.concatenate([h, h[::-1]])  # one ascending run, then one descending
+    if kind == "fewkeys_f64":
+        return rng.integers(0, 3, size=n).astype(np.float64) * 0.5  # float64, three distinct keys
+    if kind == "saw_i64":
+        return (np.arange(n, dtype=np.int64) % 1000003) * (1 << 33)  # int64 ascending saw teeth
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind,k", [("equal", 4), ("descending", 4), ("zigzag", 4), ("zigzag", 2), ("organ", 4),
+                                    ("fewkeys_f64", 4), ("saw_i64", 2)])
+def test_full_size_adversarial(kind, k, dev):
+    """2^24-key adversarial inputs (ties everywhere, one reversed run, runs of
+    two, two huge runs, float64 with three keys, int64 saw teeth) against the
+    oracle: permutation, keys as bytes, run profile, trace and every counter."""
+    n = 1 << 24
+    keys_np = _adversarial(kind, n)
+    variant = "4way" if k == 4 else "2way"
+    ref = oracle.sort(keys_np, k=k, variant=variant)
+    keys = torch.from_numpy(keys_np.copy()).to(dev)
+    out, perm, stats = stable_argsort(keys, SortConfig(k=k, variant=variant))
+    assert np.array_equal(perm.cpu().numpy(), ref.values), "permutation"
+    assert np.array_equal(out.cpu().numpy().view(np.uint8), ref.keys.view(np.uint8)), "keys"
+    for f in STAT_FIELDS:
+        assert getattr(stats, f) == ref.stats[f], f
+    assert stats.run_lengths == ref.run_lengths
+    assert stats.natural_run_lengths == ref.natural_run_lengths
+    assert read_trace(device=dev) == ref.trace
