@@ -381,3 +381,29 @@ def test_distributed_certificate_gloo_world2(tamper):
         assert res == {0: "ok", 1: "ok"}
     else:
         assert any(v != "ok" for v in res.values()), res
+
+
+@pytest.mark.gpu
+def test_shard_merge_eight_shards_at_scale():
+    """8 shards of 2^23 cfg5-recipe keys (2^26 in all), every slab merged with
+    published samples and checked against numpy's stable argsort of the whole
+    input: thousands of units and cuts per slab."""
+    from paper_2209_06909_b200 import SortConfig, stable_sort_with, workloads
+
+    dev = torch.device("cuda", 0)
+    G, m = 8, 1 << 23
+    keys = workloads.cfg5(n=G * m, seed=3)
+    sk, sv = [], []
+    for g in range(G):
+        k = torch.from_numpy(keys[g * m:(g + 1) * m].copy()).to(dev)
+        v = torch.arange(g * m, (g + 1) * m, dtype=torch.int32, device=dev)
+        stable_sort_with(k, SortConfig(), values=v)
+        sk.append(k)
+        sv.append(v)
+    smp = [multigpu.shard_samples(k) for k in sk]
+    out_v = []
+    for g in range(G):
+        t0, t1 = multigpu.slab_bounds(G * m, G, g)
+        _, v = multigpu.shard_merge(sk, sv, t0, t1, samples=smp)
+        out_v.append(v.cpu().numpy())
+    assert np.array_equal(np.concatenate(out_v), np.argsort(keys, kind="stable"))
