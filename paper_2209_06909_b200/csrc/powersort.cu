@@ -606,6 +606,8 @@ struct MergeRunner {
         ssmem = merge_small_smem_bytes<K>();
         PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
         PS_CUDA(cudaFuncSetAttribute(merge_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+        PS_CUDA(cudaFuncSetAttribute(merge_mid_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)mid_smem_bytes<K>()));
         int dev = 0, sms = 148, occ = 1;
         PS_CUDA(cudaGetDevice(&dev));
         PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -715,9 +717,16 @@ struct MergeRunner {
             else if (use_tiny && small_max <= 256)
                 tiny(merge_tiny_kernel<K, 256>, merge_tiny_smem_bytes<K, 256>(), TinyCfg<K, 256>::WARPS);
             else {
-                const uint32_t G = small_group(small_max);
-                launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32, ssmem,
-                         s, bufs, nodes, nlo, nhi, G);
+                static const bool warp_small = knob_set("PS_WARP_SMALL");  // A/B: the warp-per-group kernel
+                if (warp_small) {
+                    const uint32_t G = small_group(small_max);
+                    launch_k(merge_small_kernel<K>, grid_for(cdiv(nhi - nlo, G), SMALL_WARPS), SMALL_WARPS * 32,
+                             ssmem, s, bufs, nodes, nlo, nhi, G);
+                } else {
+                    const uint32_t G = mid_group<K>(small_max);
+                    launch_k(merge_mid_kernel<K>, (unsigned)cdiv(nhi - nlo, G), MID_THREADS, mid_smem_bytes<K>(), s,
+                             bufs, nodes, nlo, nhi, G);
+                }
             }
             PS_LAUNCH_CHECK();
         }

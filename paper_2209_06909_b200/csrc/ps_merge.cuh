@@ -677,6 +677,191 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
     }
 }
 
+// 4- or 8-byte asynchronous global -> shared copy (LDGSTS)
+template <class T>
+PS_DEV void cp_async_small(T* smem_dst, const T* gmem_src) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4 or 8 bytes");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gmem_src), "n"(sizeof(T))
+                 : "memory");
+}
+
+// Merge-path outputs [o, oe) of merge(A, B) (ties to A) into (ok, ov)[o...]:
+// diagonal search, then one record per step with the heads in registers.  A
+// read one past a run's end stays inside the CTA's shared memory.
+template <class K>
+PS_DEV void smem_merge_piece(const K* ak, const int32_t* av, uint32_t la, const K* bk, const int32_t* bv,
+                           uint32_t lb, uint32_t o, uint32_t oe, K* ok, int32_t* ov) {
+    uint32_t lo = o > lb ? o - lb : 0, hi = o < la ? o : la;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const bool le = !(bk[o - 1 - mid] < ak[mid]);
+        lo = le ? mid + 1 : lo;
+        hi = le ? hi : mid;
+    }
+    uint32_t i = lo, j = o - lo;
+    K a = ak[i], b = bk[j];
+    for (; o < oe; ++o) {
+        const bool ta = i < la && (j >= lb || !(b < a));
+        ok[o] = ta ? a : b;
+        ov[o] = *(ta ? av + i : bv + j);
+        i += ta;
+        j += !ta;
+        const K nk = *(ta ? ak + i : bk + j);
+        a = ta ? nk : a;
+        b = ta ? b : nk;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Mid-size nodes (<= SMALL_KERNEL_MAX records): a CTA per batch of G
+// consecutive nodes of the stage (G * largest <= MID_CAP), packed into shared
+// memory with asynchronous copies (a warp per node, coalesced), merged by
+// the pipe's two passes with VT consecutive outputs per thread (odd VT:
+// conflict-free stores) -- X = merge(A,B), Y = merge(C,D) into buffer 1,
+// then merge(X,Y) back into buffer 0 (2-way nodes: merge(A,B) into buffer 1,
+// which their first pass leaves unused) -- and stored a warp per node.  Two
+// buffers, so three CTAs fit an SM.  Ties go to the lower run in every pass
+// (merges.py:204-334).
+constexpr uint32_t MID_THREADS = 256;
+constexpr uint32_t MID_MAXG = 64;
+template <class K>
+PS_DEV __host__ constexpr uint32_t mid_vt() {
+    return sizeof(K) == 4 ? 15u : 9u;
+}
+template <class K>
+PS_DEV __host__ constexpr uint32_t mid_cap() {
+    return mid_vt<K>() * MID_THREADS;
+}
+template <class K>
+PS_DEV __host__ constexpr size_t mid_smem_bytes() {  // two SoA record buffers
+    return 2 * (size_t)mid_cap<K>() * (sizeof(K) + 4) + 128;
+}
+// nodes per CTA for a stage whose largest small node has `maxsz` records
+template <class K>
+inline uint32_t mid_group(uint32_t maxsz) {
+    const uint32_t g = maxsz ? mid_cap<K>() / maxsz : MID_MAXG;
+    return g < 1 ? 1 : (g > MID_MAXG ? MID_MAXG : g);
+}
+
+template <class K>
+__global__ void __launch_bounds__(MID_THREADS) merge_mid_kernel(Bufs<K> bufs, const Node* __restrict__ nodes,
+                                                               uint32_t nlo, uint32_t nhi, uint32_t G) {
+    pdl_wait();
+    constexpr uint32_t CAP = mid_cap<K>(), VT = mid_vt<K>();
+    extern __shared__ __align__(128) uint8_t smem[];
+    auto KB = [&](uint32_t q) { return reinterpret_cast<K*>(smem + (size_t)q * CAP * (sizeof(K) + 4)); };
+    auto VB = [&](uint32_t q) {
+        return reinterpret_cast<int32_t*>(smem + (size_t)q * CAP * (sizeof(K) + 4) + (size_t)CAP * sizeof(K));
+    };
+    __shared__ uint32_t s_pre[MID_MAXG + 1], s_p0[MID_MAXG], s_rel[MID_MAXG][4];
+    __shared__ uint8_t s_par[MID_MAXG], s_w[MID_MAXG];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t first64 = (uint64_t)nlo + (uint64_t)blockIdx.x * G;
+    if (first64 >= nhi) return;
+    const uint32_t first = (uint32_t)first64, cnt = min(G, nhi - first);
+    if (warp == 0) {
+        uint32_t sz = 0;
+        for (uint32_t base = 0; base < cnt; base += 32) {  // (cnt <= 64: two rounds)
+            const uint32_t j = base + lane;
+            uint32_t size = 0;
+            if (j < cnt) {
+                const Node nd = nodes[first + j];
+                const uint32_t w = nd.arity, p0 = nd.pos[0];
+                size = nd.pos[w] - p0;
+                if (size > SMALL_KERNEL_MAX) size = 0;  // a big node of the stage: the pipe's
+                s_p0[j] = p0;
+                s_par[j] = nd.parity;
+                s_w[j] = (uint8_t)w;
+#pragma unroll
+                for (uint32_t a = 0; a < 4; ++a) s_rel[j][a] = a + 1 <= w ? nd.pos[a + 1] - p0 : size;
+            }
+            uint32_t inc = size;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(PS_FULL, inc, d);
+                if (lane >= (uint32_t)d) inc += y;
+            }
+            if (j < cnt) s_pre[j + 1] = sz + inc;
+            if (base == 0 && lane == 0) s_pre[0] = 0;
+            sz += __shfl_sync(PS_FULL, inc, 31);
+        }
+    }
+    __syncthreads();
+    const uint32_t total = s_pre[cnt];
+    if (total == 0) return;
+    // ---- load: a warp per node, records of buffer parity ^ 1 into buffer 0
+    for (uint32_t j = warp; j < cnt; j += MID_THREADS / 32) {
+        const uint32_t o = s_pre[j], size = s_pre[j + 1] - o;
+        if (!size) continue;
+        const uint32_t sp = s_par[j] ^ 1u;
+        const K* gk = bufs.kb(sp) + s_p0[j];
+        const int32_t* gv = bufs.vb(sp) + s_p0[j];
+        for (uint32_t t = lane; t < size; t += 32) {
+            cp_async_small(KB(0) + o + t, gk + t);
+            cp_async_small(VB(0) + o + t, gv + t);
+        }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // ---- two passes over the packed nodes, VT outputs per thread (pieces may
+    //      span nodes and X / Y halves)
+    for (uint32_t pass = 0; pass < 2; ++pass) {
+        for (uint32_t o = tid * VT, oe = min(o + VT, total); o < oe;) {
+            uint32_t lo = 0, hi = cnt;  // last node with s_pre <= o
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= o)
+                    lo = mid;
+                else
+                    hi = mid;
+            }
+            const uint32_t j = lo, nb = s_pre[j], ne = s_pre[j + 1], w = s_w[j];
+            const uint32_t r1 = s_rel[j][0], r2 = s_rel[j][1], r3 = s_rel[j][2];
+            const uint32_t q = o - nb;
+            if (pass == 0) {
+                if (w < 3) {  // 2-way nodes merge in pass 2
+                    o = min(oe, ne);
+                    continue;
+                }
+                if (q < r2) {  // X = merge(A, B)
+                    const uint32_t pe = min(oe, nb + r2);
+                    smem_merge_piece<K>(KB(0) + nb, VB(0) + nb, r1, KB(0) + nb + r1, VB(0) + nb + r1, r2 - r1, q,
+                                        pe - nb, KB(1) + nb, VB(1) + nb);
+                    o = pe;
+                } else {  // Y = merge(C, D) (3-way: C)
+                    const uint32_t pe = min(oe, ne), r4 = ne - nb;
+                    const uint32_t c1 = w == 4 ? r3 : r4;
+                    smem_merge_piece<K>(KB(0) + nb + r2, VB(0) + nb + r2, c1 - r2, KB(0) + nb + c1, VB(0) + nb + c1,
+                                        r4 - c1, q - r2, pe - nb - r2, KB(1) + nb + r2, VB(1) + nb + r2);
+                    o = pe;
+                }
+            } else {
+                const uint32_t pe = min(oe, ne), r4 = ne - nb;
+                const uint32_t src = w >= 3 ? 1u : 0u, m = w >= 3 ? r2 : r1;
+                smem_merge_piece<K>(KB(src) + nb, VB(src) + nb, m, KB(src) + nb + m, VB(src) + nb + m, r4 - m, q,
+                                    pe - nb, KB(src ^ 1u) + nb, VB(src ^ 1u) + nb);
+                o = pe;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- store: a warp per node
+    for (uint32_t j = warp; j < cnt; j += MID_THREADS / 32) {
+        const uint32_t o = s_pre[j], size = s_pre[j + 1] - o;
+        if (!size) continue;
+        K* dk = bufs.kb(s_par[j]) + s_p0[j];
+        int32_t* dv = bufs.vb(s_par[j]) + s_p0[j];
+        const uint32_t q = s_w[j] >= 3 ? 0u : 1u;  // the buffer its second pass wrote
+        const K* sk = KB(q) + o;
+        const int32_t* sv = VB(q) + o;
+        for (uint32_t t = lane; t < size; t += 32) {
+            dk[t] = sk[t];
+            dv[t] = sv[t];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Tiny nodes (every small node of the stage <= TINY records): one node per
 // thread.  A warp stages its 32 nodes' keys as rows of TINY+1 elements (odd
@@ -688,14 +873,6 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) merge_small_kernel(Bufs<K> b
 // per-node barrier: ~15 instructions per output and 32 independent merges per
 // warp, where the warp-per-node kernel spends most of its time in diagonal
 // searches for two outputs per lane.
-// 4- or 8-byte asynchronous global -> shared copy (LDGSTS)
-template <class T>
-PS_DEV void cp_async_small(T* smem_dst, const T* gmem_src) {
-    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4 or 8 bytes");
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
-                 "l"(gmem_src), "n"(sizeof(T))
-                 : "memory");
-}
 
 template <class K, uint32_t TINY>
 struct TinyCfg {

@@ -30,6 +30,7 @@
 #pragma once
 
 #include "ps_common.cuh"
+#include "ps_merge.cuh"
 
 namespace ps {
 
@@ -315,33 +316,6 @@ PS_DEV void cp_async8(void* dst, const void* src) {
 }
 PS_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Merge-path outputs [o, oe) of merge(A, B) (ties to A) into (ok, ov)[o...].
-// The heads live in registers; a read one past a run's end stays inside the
-// CTA's shared memory (the next run, the next buffer or the slack).
-template <class K>
-PS_DEV void xs_merge_piece(const K* ak, const int32_t* av, uint32_t la, const K* bk, const int32_t* bv,
-                           uint32_t lb, uint32_t o, uint32_t oe, K* ok, int32_t* ov) {
-    uint32_t lo = o > lb ? o - lb : 0, hi = o < la ? o : la;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const bool le = !(bk[o - 1 - mid] < ak[mid]);
-        lo = le ? mid + 1 : lo;
-        hi = le ? hi : mid;
-    }
-    uint32_t i = lo, j = o - lo;
-    K a = ak[i], b = bk[j];
-    for (; o < oe; ++o) {
-        const bool ta = i < la && (j >= lb || !(b < a));
-        ok[o] = ta ? a : b;
-        ov[o] = *(ta ? av + i : bv + j);
-        i += ta;
-        j += !ta;
-        const K nk = *(ta ? ak + i : bk + j);
-        a = ta ? nk : a;
-        b = ta ? b : nk;
-    }
-}
-
 // Persistent unit loop over the boundary rows (chunks [row c, row c+1]).
 template <class K>
 __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, const XPlan* __restrict__ plan,
@@ -480,7 +454,7 @@ __global__ void __launch_bounds__(XM_THREADS) xs_merge_kernel(ShardSet<K> S, con
                     break;
                 }
                 const uint32_t ra = s_ro[2 * q], rb = 2 * q + 1 < R ? s_ro[2 * q + 1] : ra;
-                xs_merge_piece<K>(BK(src) + ra, BV(src) + ra, la, BK(src) + rb, BV(src) + rb, lb, o - base,
+                smem_merge_piece<K>(BK(src) + ra, BV(src) + ra, la, BK(src) + rb, BV(src) + rb, lb, o - base,
                                   pe - base, BK(dst) + base, BV(dst) + base);
                 o = pe;
             }
