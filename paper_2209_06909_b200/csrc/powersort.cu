@@ -671,6 +671,12 @@ struct MergeRunner {
             if (rc) return rc;
         }
         const uint32_t nbig = (nhi - nlo) - nsmall;
+        // the tiny kernel counts its own nodes' comparisons for the sentinel /
+        // no-sentinel 2-way and 4-way variants (every small node of such a stage is its)
+        static const bool old_small = knob_set("PS_OLD_SMALL");  // A/B: warp-per-group kernel only
+        static const uint32_t tiny_min = (uint32_t)knob("PS_TINY_MIN", 32768);
+        const bool use_tiny = nsmall && !old_small && nsmall >= tiny_min && small_max <= 256;
+        const bool tiny_counts = use_tiny && (count_variant == 0 || count_variant == 2 || count_variant == 3);
         if (count_variant >= 0) {
             // The counters read the stage's inputs, which no merge of this stage
             // overwrites: they run on a side stream next to the stage's merges
@@ -682,7 +688,7 @@ struct MergeRunner {
                 PS_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
                 cs = side;
             }
-            if (nsmall) {
+            if (nsmall && !tiny_counts) {
                 launch_k(merge_counters_small_kernel<K>, grid_for(nhi - nlo, 256), 256, 0, cs, bufs, nodes, nlo, nhi,
                          count_variant, sum);
                 PS_LAUNCH_CHECK();
@@ -700,12 +706,10 @@ struct MergeRunner {
         if (nsmall) {
             // a thread per node while there are enough nodes to fill the GPU (a
             // warp per 32 nodes); otherwise the warp-per-group kernel
-            static const bool old_small = knob_set("PS_OLD_SMALL");  // A/B: warp-per-group kernel only
-            static const uint32_t tiny_min = (uint32_t)knob("PS_TINY_MIN", 32768);
-            const bool use_tiny = !old_small && nsmall >= tiny_min;
             auto tiny = [&](auto kern, size_t tsm, uint32_t warps) -> int {
                 PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-                launch_k(kern, grid_for(nhi - nlo, 32ull * warps), warps * 32, tsm, s, bufs, nodes, nlo, nhi);
+                launch_k(kern, grid_for(nhi - nlo, 32ull * warps), warps * 32, tsm, s, bufs, nodes, nlo, nhi,
+                         tiny_counts ? sum : nullptr);
                 return PS_OK;
             };
             if (use_tiny && small_max <= 64)

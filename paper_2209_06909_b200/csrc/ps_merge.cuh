@@ -888,10 +888,16 @@ size_t merge_tiny_smem_bytes() {
     return (size_t)TinyCfg<K, TINY>::WARPS * TinyCfg<K, TINY>::WARP_BYTES;
 }
 
+// With `sum` (merge variants 2way, 2way-nosentinel, 4way), each lane also
+// counts its node's CountingOrder comparisons from the positions its
+// tournament observes -- where every run's last record lands (e_a) and where
+// within its side (CX, CY) -- by node_counters' closed forms, so the stage
+// needs no separate counters launch.
 template <class K, uint32_t TINY>
 __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kernel(Bufs<K> bufs,
                                                                                   const Node* __restrict__ nodes,
-                                                                                  uint32_t nlo, uint32_t nhi) {
+                                                                                  uint32_t nlo, uint32_t nhi,
+                                                                                  Summary* __restrict__ sum) {
     static_assert(TINY <= 256, "offsets are bytes");
     using C = TinyCfg<K, TINY>;
     pdl_wait();
@@ -937,11 +943,14 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     // ---- the lane's tournament ----
-    if (T) {
+    unsigned long long cmp = 0;
+    auto tournament = [&](auto count) {
+        constexpr bool COUNT = decltype(count)::value;
         const K* row = rows + lane * C::RK;
         uint8_t* oi = outi + lane * C::RI;
         uint32_t i0 = 0, i1 = e0, i2 = e1, i3 = e2;
         K h0 = row[0], h1 = row[i1], h2 = row[i2], h3 = row[i3];
+        uint32_t E0 = 0, E1 = 0, E2 = 0, E3 = 0, P0 = 0, P1 = 0, P2 = 0, P3 = 0, xo = 0, yo = 0;
         for (uint32_t o = 0; o < T; ++o) {
             const bool v0 = i0 < e0, v1 = i1 < e1, v2 = i2 < e2, v3 = i3 < e3;
             const bool b1 = v1 && (!v0 || h1 < h0);  // ties to the lower run
@@ -953,6 +962,15 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
             oi[o] = (uint8_t)src;
             const K nk = row[src + 1];  // (one past a run reads its neighbour or the row's slack)
             const bool s0 = !right && !b1, s1 = !right && b1, s2 = right && !b3, s3 = right && b3;
+            if (COUNT) {  // the last record of a run: its merged position and its side position
+                const uint32_t side = right ? yo : xo;
+                if (s0 && src + 1 == e0) { E0 = o; P0 = side; }
+                if (s1 && src + 1 == e1) { E1 = o; P1 = side; }
+                if (s2 && src + 1 == e2) { E2 = o; P2 = side; }
+                if (s3 && src + 1 == e3) { E3 = o; P3 = side; }
+                xo += !right;
+                yo += right;
+            }
             i0 += s0;
             i1 += s1;
             i2 += s2;
@@ -962,6 +980,26 @@ __global__ void __launch_bounds__(TinyCfg<K, TINY>::WARPS * 32) merge_tiny_kerne
             h2 = s2 ? nk : h2;
             h3 = s3 ? nk : h3;
         }
+        if (COUNT) {
+            if (w == 2) {
+                cmp = min(E0, E1) + 1;  // merges.py:75-142 (sentinel compares uncounted)
+            } else {                    // merges.py:204-334: node_counters' 3/4-way closed form
+                const uint32_t MX = max(E0, E1), MY = w == 4 ? max(E2, E3) : E2;
+                const uint32_t CX = E0 < E1 ? P0 : P1;
+                const uint32_t CY = w == 4 ? (E2 < E3 ? P2 : P3) : 0u;
+                cmp = 1 + (w == 4 ? 1 : 0) + (min(MX, MY) + 1) + CX + CY;
+            }
+        }
+    };
+    if (T) {
+        if (sum)
+            tournament(std::true_type{});
+        else
+            tournament(std::false_type{});
+    }
+    if (sum) {
+        for (int dd = 16; dd; dd >>= 1) cmp += __shfl_xor_sync(PS_FULL, cmp, dd);
+        if (lane == 0 && cmp) atomicAdd(&sum->comparisons, cmp);
     }
     __syncwarp();
     // ---- stores: keys and payloads from the rows, one coalesced store per node ----
