@@ -516,7 +516,7 @@ def run_ours(args):
 
     from paper_2209_06909_b200 import SortConfig, _lib, workloads
     from paper_2209_06909_b200.certify import certify
-    from paper_2209_06909_b200.policy import _sort_tensor, check
+    from paper_2209_06909_b200.policy import _sort_tensor, check, finish_counters
 
     rank, local, world = dist_env()
     if world > 1:
@@ -538,8 +538,9 @@ def run_ours(args):
         flush.fill_(1)
 
     def sort_once():
-        # asynchronous: the merges stay queued so the closing event follows the
-        # last kernel directly; check() below reads their invariant flags
+        # asynchronous: the merges (and the device counters) stay queued so the
+        # closing event follows the last kernel directly; check() below reads
+        # their invariant flags, finish_counters() the comparisons / moves
         return _sort_tensor(keys, perm, cfg, _lib.VALUES_ARGSORT, collect_runs=False, asynchronous=True)
 
     # warm-up (+ one certified run)
@@ -547,6 +548,7 @@ def run_ours(args):
         reset()
         stats = sort_once()
         check(dev)
+        finish_counters(stats)  # comparisons / moves of an asynchronous sort, read after its stream
         if i == 0:
             certify(src, keys, perm)
     torch.cuda.synchronize()

@@ -74,7 +74,9 @@ enum { PS_FLAG_ASYNC = 1 };
 
 /* SortStats, statskit.py:75-98 (scalar fields).  comparisons / moves are
  * data-dependent counters of the reference's sequential kernels; they are
- * computed when ps_config.count_comparisons is set (then *_valid is 1). */
+ * computed when ps_config.count_comparisons is set (then *_valid is 1).  An
+ * asynchronous sort (PS_FLAG_ASYNC) leaves them on the device: *_valid is 2
+ * and ps_result_counters() returns them once the stream has finished. */
 typedef struct {
     int64_t comparisons;
     int64_t merge_cost;
@@ -116,6 +118,11 @@ int ps_check(void* workspace, void* stream);
 
 /* Number of runs r and merge nodes of the last ps_sort / ps_tree_from_profile
  * that used `workspace`. */
+/* comparisons / moves of the last asynchronous counting sort on `workspace`
+ * (ps_stats.*_valid == 2): synchronizes `stream`, checks the device invariant
+ * flags, and returns them (-1 where the sort could not count exactly). */
+int ps_result_counters(void* workspace, void* stream, int64_t* comparisons, int64_t* moves);
+
 int ps_result_counts(const void* workspace, int64_t* runs, int64_t* merges);
 
 /* Copy the run profile of the last sort to host arrays of length >= runs:

@@ -27,6 +27,7 @@ EXPORTS = (
     "ps_sort",
     "ps_check",
     "ps_result_counts",
+    "ps_result_counters",
     "ps_result_runs",
     "ps_result_trace",
     "ps_profile_workspace_size",
@@ -131,6 +132,8 @@ def load():
     lib.ps_shard_merge_workspace_size.restype = sz
     lib.ps_shard_merge.argtypes = [i32, i32, vp, vp, vp, vp, i64, i64, vp, vp, vp, sz, vp]
     lib.ps_shard_merge.restype = ctypes.c_int
+    lib.ps_result_counters.argtypes = [vp, vp, vp, vp]
+    lib.ps_result_counters.restype = ctypes.c_int
     lib.ps_shard_sample_count.argtypes = [i32, i64]
     lib.ps_shard_sample_count.restype = i64
     lib.ps_shard_samples.argtypes = [i32, vp, i64, vp, vp]

@@ -117,8 +117,10 @@ struct WsHeader {
     int32_t k, dtype;
     uint32_t r;
     uint32_t nmain, nspine_nodes;
-    uint32_t pad;
+    uint32_t counters_pending;  // comparisons / moves of an asynchronous sort still on the device
     uint64_t off_sum, off_b, off_nat, off_nodes;
+    int64_t moves_base;         // tree-determined part of `moves` (pending counters)
+    int32_t counters_exact, pad2;
 };
 
 // Small device->host reads go through a host-mapped pinned buffer written by a
@@ -789,9 +791,12 @@ struct MergeRunner {
 };
 
 int write_header(uint8_t* ws, const Layout& L, int64_t n, int64_t m, int k, int dtype, uint32_t r, uint32_t nmain,
-                 uint32_t nspine, cudaStream_t s) {
+                 uint32_t nspine, cudaStream_t s, int64_t moves_base = -1, bool exact = false) {
     WsHeader h;
     memset(&h, 0, sizeof(h));
+    h.counters_pending = moves_base >= 0 ? 1u : 0u;
+    h.moves_base = moves_base;
+    h.counters_exact = exact ? 1 : 0;
     h.magic = WS_MAGIC;
     h.n = n;
     h.m = m;
@@ -1075,7 +1080,11 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
     // after the merges (unless the caller asked for PS_FLAG_ASYNC).
     Summary c;
     memset(&c, 0, sizeof(c));
-    if (need_counts || !(cfg.flags & PS_FLAG_ASYNC)) {
+    // An asynchronous counting sort (not copy-smaller, whose buffer and scan
+    // counters are data-dependent too) leaves comparisons / moves on the
+    // device: ps_result_counters() reads them once the stream has finished.
+    const bool defer = counting && (cfg.flags & PS_FLAG_ASYNC) && cfg.variant != PS_VARIANT_2WAY_COPY_SMALLER;
+    if (!defer && (need_counts || !(cfg.flags & PS_FLAG_ASYNC))) {
         int rc = publish(sum, need_counts ? SUM_STATS : SUM_HEAD, &c, nullptr, 0, nullptr, s);
         if (rc) return rc;
         if (c.err & ERR_STACK) return fail(PS_EOVERFLOW, "run stack exceeded its height bound");
@@ -1122,6 +1131,16 @@ int sort_impl(K* keys, int32_t* values, int64_t n, const ps_config& cfg, uint8_t
             mv += 2 * M + (sentinel_tournament ? 0 : m34);
         st->moves = exact ? mv : -1;
         st->moves_valid = exact;
+        if (defer) {
+            // the header records what ps_result_counters needs (written behind the merges)
+            const int64_t base = mv - (int64_t)c.moves;  // (c is zero here: the tree part)
+            int rc = write_header(ws, L, n, (int64_t)m, cfg.k, 0, r, info.s.nmain, info.s.nspine_nodes, s, base,
+                                  exact);
+            if (rc) return rc;
+            PS_LAUNCH_CHECK();
+            st->comparisons = st->moves = -1;
+            st->comparisons_valid = st->moves_valid = exact ? 2 : 0;  // 2: pending (ps_result_counters)
+        }
     }
     return PS_OK;
 }
@@ -1354,6 +1373,26 @@ static int read_header(const void* workspace, WsHeader& h) {
     PS_CUDA(cudaDeviceSynchronize());
     PS_CUDA(cudaMemcpy(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost));
     if (h.magic != WS_MAGIC) return fail(PS_EINVAL, "workspace holds no sort result");
+    return PS_OK;
+}
+
+int ps_result_counters(void* workspace, void* stream, int64_t* comparisons, int64_t* moves) {
+    if (!workspace) return fail(PS_EINVAL, "NULL pointer argument");
+    PS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    WsHeader h;
+    int rc = read_header(workspace, h);
+    if (rc) return rc;
+    if (!h.counters_pending) return fail(PS_EINVAL, "the last sort on this workspace has no pending counters");
+    unsigned long long cm[2] = {0, 0};  // Summary.comparisons, Summary.moves (adjacent)
+    static_assert(offsetof(Summary, moves) == offsetof(Summary, comparisons) + 8, "Summary counter layout");
+    PS_CUDA(cudaMemcpy(cm, (const uint8_t*)workspace + h.off_sum + offsetof(Summary, comparisons), sizeof(cm),
+                       cudaMemcpyDeviceToHost));
+    uint32_t err = 0;
+    PS_CUDA(cudaMemcpy(&err, (const uint8_t*)workspace + h.off_sum + offsetof(Summary, err), 4,
+                       cudaMemcpyDeviceToHost));
+    if (err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(err) + ")");
+    if (comparisons) *comparisons = h.counters_exact ? (int64_t)cm[0] : -1;
+    if (moves) *moves = h.counters_exact ? (int64_t)cm[1] + h.moves_base : -1;
     return PS_OK;
 }
 

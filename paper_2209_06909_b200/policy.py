@@ -15,6 +15,8 @@ reference's output.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -153,6 +155,26 @@ def check(device=None):
     _lib.check(lib.ps_check(ws.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
 
 
+def finish_counters(stats):
+    """Fills ``comparisons`` and ``moves`` of the SortStats of an asynchronous
+    sort (their device counters are read once its stream has finished,
+    ps_result_counters); a no-op for any other SortStats."""
+    dev = getattr(stats, "_pending", None)
+    if dev is None:
+        return stats
+    torch = _torch()
+    ws = _WS.last(dev)
+    lib = _lib.load()
+    cmp_ = ctypes.c_int64()
+    mov = ctypes.c_int64()
+    _lib.check(lib.ps_result_counters(ws.data_ptr(), torch.cuda.current_stream(dev).cuda_stream, ctypes.byref(cmp_),
+                                      ctypes.byref(mov)))
+    stats.comparisons = int(cmp_.value) if cmp_.value >= 0 else None
+    stats.moves = int(mov.value) if mov.value >= 0 else None
+    stats._pending = None
+    return stats
+
+
 def _cfg_struct(config, values_mode, asynchronous=False):
     return _lib.PsConfig(
         config.k, _lib.VARIANT_IDS[config.variant], config.min_run_len, int(bool(config.strict_merge_down)),
@@ -241,8 +263,10 @@ def _sort_tensor(keys, values, config, values_mode, collect_runs=True, asynchron
     for f in ("merge_cost", "buffer_cost", "max_stack_height", "runs_detected", "merges2", "merges3", "merges4",
               "scan_reads", "scan_writes"):
         setattr(stats, f, int(getattr(st, f)))
-    stats.comparisons = int(st.comparisons) if st.comparisons_valid else None
-    stats.moves = int(st.moves) if st.moves_valid else None
+    stats.comparisons = int(st.comparisons) if st.comparisons_valid == 1 else None
+    stats.moves = int(st.moves) if st.moves_valid == 1 else None
+    if st.comparisons_valid == 2:  # asynchronous counting sort: finish_counters() reads them
+        stats._pending = keys.device
     if collect_runs:
         stats.run_lengths, stats.natural_run_lengths = _read_runs(lib, ws, stats.runs_detected)
     if config.on_merge is not None:

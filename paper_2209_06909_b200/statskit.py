@@ -34,6 +34,9 @@ class SortStats:
     scan_writes: int = 0
     run_lengths: list = field(default_factory=list)
     natural_run_lengths: list = field(default_factory=list)
+    # device of an asynchronous counting sort whose comparisons / moves are
+    # still on the device (policy.finish_counters); not a reference field
+    _pending: object = field(default=None, repr=False, compare=False)
 
     @property
     def merges_total(self) -> int:

@@ -426,3 +426,23 @@ def test_asynchronous_sorts_then_check(dev):
         with torch.cuda.stream(s):
             check(dev)
         assert np.array_equal(perm.cpu().numpy(), oracle.sort(x, want_trace=False).values)
+
+
+@pytest.mark.parametrize("name,k", [("cfg2", 4), ("cfg4", 4), ("cfg1", 2)])
+def test_asynchronous_counting_sort_then_finish_counters(name, k, dev):
+    # PS_FLAG_ASYNC with the counters on: comparisons / moves stay on the device
+    # (ps_stats.*_valid == 2) until finish_counters() reads them after the stream
+    from paper_2209_06909_b200 import _lib
+    from paper_2209_06909_b200.policy import _sort_tensor, finish_counters
+
+    x = workloads.generate(name, n=1 << 20, seed=71)
+    variant = "4way" if k == 4 else "2way"
+    keys = torch.from_numpy(x).to(dev)
+    perm = torch.empty(x.shape[0], dtype=torch.int32, device=dev)
+    st = _sort_tensor(keys, perm, SortConfig(k=k, variant=variant), _lib.VALUES_ARGSORT, collect_runs=False,
+                      asynchronous=True)
+    assert st.comparisons is None and st.moves is None
+    finish_counters(st)
+    ref = oracle.sort(x, k=k, variant=variant, want_trace=False)
+    assert st.comparisons == ref.stats["comparisons"] and st.moves == ref.stats["moves"]
+    assert np.array_equal(perm.cpu().numpy(), ref.values)
