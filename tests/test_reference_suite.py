@@ -4,9 +4,13 @@
 ``paper_2209_06909_b200``'s.  These tests run the
 reference's test modules for the public surface -- test_policy.py (the sort:
 anchors, hand-traced schedules, merge_down arities, stability on records,
-SENTINEL fallback, simulator == real trace, k=2 strict tree), test_statskit.py
-and test_power.py -- in a subprocess with ``compat/`` first on sys.path, so
-every ``stable_sort_with`` they call sorts on the GPU.
+SENTINEL fallback, simulator == real trace, k=2 strict tree), test_statskit.py,
+test_power.py and test_acceptance.py (the 10,000-trial correctness and
+stability matrix over every variant, generator and min_run_len, the
+merge-cost, comparison and stack-height theorems, oracle dominance,
+near-optimality, merge-cost halving, scanned-element consistency, trivial
+anchors) -- in a subprocess with ``compat/`` first on sys.path, so every
+``stable_sort_with`` they call sorts on the GPU.
 
 The reference sources are staged by tools/stage_reference.sh into the
 git-ignored ``baseline/_ref`` (installed package + a copy of its tests); the
@@ -68,3 +72,10 @@ def test_reference_policy_suite():
 @pytest.mark.gpu
 def test_reference_statskit_suite():
     _run_suite(["test_statskit.py"])
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite():
+    # the reference's acceptance criteria, every stable_sort_with on the GPU
+    out = _run_suite(["test_acceptance.py"])
+    assert " failed" not in out
