@@ -1378,21 +1378,25 @@ static int read_header(const void* workspace, WsHeader& h) {
 
 int ps_result_counters(void* workspace, void* stream, int64_t* comparisons, int64_t* moves) {
     if (!workspace) return fail(PS_EINVAL, "NULL pointer argument");
-    PS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    // the header and the summary's flags and counters through the host-mapped
+    // publish, stream-ordered behind the sort: no device-wide synchronization
+    // and no copy-engine transfer, which would queue behind bulk copies of
+    // other streams (a pipelined caller's)
+    static_assert(sizeof(WsHeader) <= 256, "the summary follows the header at byte 256");
     WsHeader h;
-    int rc = read_header(workspace, h);
+    Summary* sp = new Summary;
+    memset(sp, 0, sizeof(Summary));
+    const uint8_t* ws = (const uint8_t*)workspace;
+    int rc = publish(ws, sizeof(WsHeader), &h, ws + 256, offsetof(Summary, moves) + 8, sp, (cudaStream_t)stream);
+    const uint32_t err = sp->err;
+    const unsigned long long cm = sp->comparisons, mv = sp->moves;
+    delete sp;
     if (rc) return rc;
+    if (h.magic != WS_MAGIC || h.off_sum != 256) return fail(PS_EINVAL, "workspace holds no sort result");
     if (!h.counters_pending) return fail(PS_EINVAL, "the last sort on this workspace has no pending counters");
-    unsigned long long cm[2] = {0, 0};  // Summary.comparisons, Summary.moves (adjacent)
-    static_assert(offsetof(Summary, moves) == offsetof(Summary, comparisons) + 8, "Summary counter layout");
-    PS_CUDA(cudaMemcpy(cm, (const uint8_t*)workspace + h.off_sum + offsetof(Summary, comparisons), sizeof(cm),
-                       cudaMemcpyDeviceToHost));
-    uint32_t err = 0;
-    PS_CUDA(cudaMemcpy(&err, (const uint8_t*)workspace + h.off_sum + offsetof(Summary, err), 4,
-                       cudaMemcpyDeviceToHost));
     if (err) return fail(PS_EINVARIANT, "device invariant violated (flags " + std::to_string(err) + ")");
-    if (comparisons) *comparisons = h.counters_exact ? (int64_t)cm[0] : -1;
-    if (moves) *moves = h.counters_exact ? (int64_t)cm[1] + h.moves_base : -1;
+    if (comparisons) *comparisons = h.counters_exact ? (int64_t)cm : -1;
+    if (moves) *moves = h.counters_exact ? (int64_t)mv + h.moves_base : -1;
     return PS_OK;
 }
 

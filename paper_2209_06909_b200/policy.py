@@ -156,9 +156,10 @@ def check(device=None):
 
 
 def finish_counters(stats):
-    """Fills ``comparisons`` and ``moves`` of the SortStats of an asynchronous
-    sort (their device counters are read once its stream has finished,
-    ps_result_counters); a no-op for any other SortStats."""
+    """Completes the SortStats of an asynchronous sort: waits for it on the
+    current stream, checks its device invariants and fills ``comparisons``
+    and ``moves`` (ps_result_counters: a host-mapped read, no device-wide
+    synchronization); a no-op for any other SortStats."""
     dev = getattr(stats, "_pending", None)
     if dev is None:
         return stats
@@ -275,15 +276,18 @@ def _sort_tensor(keys, values, config, values_mode, collect_runs=True, asynchron
     return stats
 
 
-def stable_argsort(keys, config=None, collect_runs=True):
+def stable_argsort(keys, config=None, collect_runs=True, asynchronous=False):
     """Sort the CUDA tensor ``keys`` in place; return ``(keys, perm, stats)``
     where ``perm`` (int32) holds the source index of every output element --
-    the reference's (key, index) records after the sort."""
+    the reference's (key, index) records after the sort.  ``asynchronous``:
+    return once the sort is queued (PS_FLAG_ASYNC); ``finish_counters(stats)``
+    later waits for it, checks its device invariants and fills comparisons /
+    moves."""
     torch = _torch()
     if config is None:
         config = SortConfig()
     perm = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
-    stats = _sort_tensor(keys, perm, config, _lib.VALUES_ARGSORT, collect_runs)
+    stats = _sort_tensor(keys, perm, config, _lib.VALUES_ARGSORT, collect_runs, asynchronous)
     return keys, perm, stats
 
 
