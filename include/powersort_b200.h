@@ -171,6 +171,17 @@ int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys
                    const void* const* shard_samples, const int64_t* shard_n, int64_t out_begin, int64_t out_end,
                    void* out_keys, int32_t* out_vals, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Peer shards for ps_shard_merge (plumbing for the multi-GPU mode only; no
+ * reference counterpart).  ps_ipc_export writes the 64-byte cudaIpcMemHandle_t
+ * of the allocation holding device pointer `ptr` and ptr's byte offset in it.
+ * ps_ipc_open opens another process's handle in `device`'s context with lazy
+ * peer access enabled, so kernels on `device` load from it over NVLink
+ * (*base = the allocation's base; add the exporter's offset).  ps_ipc_close
+ * unmaps it. */
+int ps_ipc_export(int32_t device, const void* ptr, void* handle, int64_t* offset);
+int ps_ipc_open(int32_t device, const void* handle, void** base);
+int ps_ipc_close(int32_t device, void* base);
+
 /* Sample array of a sorted shard for ps_shard_merge: samples[i] = keys[i *
  * stride], stride = 128 bytes of keys (32 four-byte or 16 eight-byte keys);
  * ps_shard_sample_count gives the array length, ceil(n / stride). */

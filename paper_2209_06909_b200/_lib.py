@@ -38,6 +38,9 @@ EXPORTS = (
     "ps_shard_merge",
     "ps_shard_sample_count",
     "ps_shard_samples",
+    "ps_ipc_export",
+    "ps_ipc_open",
+    "ps_ipc_close",
     "ps_gather_rows",
     "ps_profile_enable",
     "ps_profile_read",
@@ -137,6 +140,12 @@ def load():
     lib.ps_shard_sample_count.argtypes = [i32, i64]
     lib.ps_shard_sample_count.restype = i64
     lib.ps_shard_samples.argtypes = [i32, vp, i64, vp, vp]
+    lib.ps_ipc_export.argtypes = [i32, vp, vp, i64p]
+    lib.ps_ipc_export.restype = ctypes.c_int
+    lib.ps_ipc_open.argtypes = [i32, vp, ctypes.POINTER(ctypes.c_void_p)]
+    lib.ps_ipc_open.restype = ctypes.c_int
+    lib.ps_ipc_close.argtypes = [i32, vp]
+    lib.ps_ipc_close.restype = ctypes.c_int
     lib.ps_shard_samples.restype = ctypes.c_int
     lib.ps_profile_enable.argtypes = [i32]
     lib.ps_profile_enable.restype = ctypes.c_int

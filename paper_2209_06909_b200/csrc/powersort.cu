@@ -1575,6 +1575,52 @@ int ps_gather_rows(const void* src, const int32_t* perm, void* dst, int64_t n, i
     return PS_OK;
 }
 
+// Peer shards: a CUDA IPC handle of another rank's allocation is opened in the
+// CALLER's device context with lazy peer access, so the shard-merge kernel on
+// this device can load from it over NVLink (an allocation opened in the peer
+// device's own context would need cudaDeviceEnablePeerAccess as well).
+int ps_ipc_export(int32_t device, const void* ptr, void* handle, int64_t* offset) {
+    if (!ptr || !handle || !offset) return fail(PS_EINVAL, "NULL pointer argument");
+    PS_CUDA(cudaSetDevice(device));
+    // allocation base of ptr (cuMemGetAddressRange through the runtime's
+    // driver entry point: no link-time libcuda dependency)
+    using range_fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static range_fn range = nullptr;
+    if (!range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PS_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) return fail(PS_ECUDA, "cuMemGetAddressRange not found");
+        range = (range_fn)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
+        return fail(PS_ECUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    PS_CUDA(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+    memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return PS_OK;
+}
+
+int ps_ipc_open(int32_t device, const void* handle, void** base) {
+    if (!handle || !base) return fail(PS_EINVAL, "NULL pointer argument");
+    PS_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    *base = nullptr;
+    PS_CUDA(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+    return PS_OK;
+}
+
+int ps_ipc_close(int32_t device, void* base) {
+    if (!base) return PS_OK;
+    PS_CUDA(cudaSetDevice(device));
+    PS_CUDA(cudaIpcCloseMemHandle(base));
+    return PS_OK;
+}
+
 int ps_shard_merge(int32_t dtype, int32_t nshards, const void* const* shard_keys, const int32_t* const* shard_vals,
                    const void* const* shard_samples, const int64_t* shard_n, int64_t out_begin, int64_t out_end,
                    void* out_keys, int32_t* out_vals, void* workspace, size_t workspace_bytes, void* stream) {

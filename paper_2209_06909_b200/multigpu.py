@@ -8,9 +8,10 @@ One process per GPU.  Every rank holds a contiguous shard of the global input
    its own array: its run powers use the shard length, so its merge tree
    differs from the 1-GPU tree.  Tree parity is defined at G = 1 only.
 2. ``ps_shard_merge`` produces this rank's slab of the global stable order,
-   ranks [g*N/G, (g+1)*N/G).  It finds the slab's co-ranks in all G sorted
-   shards and reads the peer shards directly over NVLink (CUDA IPC mappings,
-   peer loads in the gather kernel).  It then merges the G windows locally.
+   ranks [g*N/G, (g+1)*N/G), in one pass: it finds the slab's co-ranks in
+   all G sorted shards and loads the peer shards' windows directly over
+   NVLink (CUDA IPC mappings opened in this device's context with lazy peer
+   access, ``ps_ipc_open``) into the merge kernel's shared memory.
 
 ``torch.distributed`` is used only as plumbing: sizes and IPC handles are
 exchanged as Python objects, plus barriers.  No collective touches the key
@@ -62,22 +63,32 @@ def shard_merge(shard_keys, shard_vals, t0, t1, out_keys=None, out_vals=None, sa
     are the shards' sample arrays (shard_samples) or None."""
     import torch
 
-    lib = _lib.load()
     G = len(shard_keys)
     if G != len(shard_vals) or not 1 <= G <= 8:
         raise ValueError("need 1..8 shards with matching value arrays")
-    dt = _dtype_id(shard_keys[0])
-    dev = torch.device("cuda", torch.cuda.current_device())
+    sp = None if samples is None else [
+        (s.data_ptr() if s is not None and s.numel() else None) for s in samples]
+    return _shard_merge_ptrs(shard_keys[0].dtype, [k.data_ptr() for k in shard_keys],
+                             [v.data_ptr() for v in shard_vals], sp, [k.numel() for k in shard_keys], t0, t1,
+                             torch.device("cuda", torch.cuda.current_device()), out_keys, out_vals, workspace)
+
+
+def _shard_merge_ptrs(dtype, kptrs, vptrs, sptrs, sizes, t0, t1, dev, out_keys=None, out_vals=None, workspace=None):
+    """shard_merge over raw device pointers (local or peer-mapped)."""
+    import torch
+
+    lib = _lib.load()
+    G = len(kptrs)
+    dt = _dtype_id(torch.empty(0, dtype=dtype))
     n = t1 - t0
     if out_keys is None:
-        out_keys = torch.empty(n, dtype=shard_keys[0].dtype, device=dev)
+        out_keys = torch.empty(n, dtype=dtype, device=dev)
     if out_vals is None:
         out_vals = torch.empty(n, dtype=torch.int32, device=dev)
-    kp = (ctypes.c_void_p * G)(*[k.data_ptr() for k in shard_keys])
-    vp = (ctypes.c_void_p * G)(*[v.data_ptr() for v in shard_vals])
-    sp = None if samples is None else (ctypes.c_void_p * G)(*[
-        (s.data_ptr() if s is not None and s.numel() else None) for s in samples])
-    ns = (ctypes.c_int64 * G)(*[k.numel() for k in shard_keys])
+    kp = (ctypes.c_void_p * G)(*kptrs)
+    vp = (ctypes.c_void_p * G)(*vptrs)
+    sp = None if sptrs is None else (ctypes.c_void_p * G)(*sptrs)
+    ns = (ctypes.c_int64 * G)(*[int(x) for x in sizes])
     nbytes = int(lib.ps_shard_merge_workspace_size(G, n))
     ws = workspace
     if ws is None or ws.numel() < nbytes:
@@ -86,6 +97,16 @@ def shard_merge(shard_keys, shard_vals, t0, t1, out_keys=None, out_vals=None, sa
     _lib.check(lib.ps_shard_merge(dt, G, kp, vp, sp, ns, t0, t1, out_keys.data_ptr(), out_vals.data_ptr(),
                                   ws.data_ptr(), ws.numel(), stream))
     return out_keys, out_vals
+
+
+def _ipc_export(t):
+    """(CUDA IPC handle of the allocation holding ``t``, byte offset of ``t``
+    in it, element count): plain bytes and ints, exchanged as plumbing."""
+    lib = _lib.load()
+    handle = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _lib.check(lib.ps_ipc_export(t.device.index, t.data_ptr(), handle, ctypes.byref(off)))
+    return handle.raw, int(off.value), t.numel()
 
 
 class DistributedSorter:
@@ -103,14 +124,15 @@ class DistributedSorter:
     def __init__(self, n_local, dtype, config=None, group=None, device=None):
         import torch
         import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
 
         self.config = config or SortConfig()
         self.group = group
         self.dist = dist
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        dev = device or torch.device("cuda", torch.cuda.current_device())
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         sizes = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(sizes, int(n_local), group=group)
@@ -129,17 +151,34 @@ class DistributedSorter:
         self.out_vals = torch.empty(t1 - t0, dtype=torch.int32, device=dev)
         self.ws = torch.empty(max(int(lib.ps_shard_merge_workspace_size(self.world, t1 - t0)), 1),
                               dtype=torch.uint8, device=dev)
+        self.device = dev
         self.peers = None
+        self._mapped = []
         if self.world > 1:
+            # each rank's shard, payload and samples are opened in THIS device's
+            # context (ps_ipc_open: lazy peer access), not the peer's, so the
+            # shard-merge kernel here loads them over NVLink
             handles = [None] * self.world
-            dist.all_gather_object(handles, tuple(reduce_tensor(t) for t in (self.keys, self.vals, self.samples)),
+            dist.all_gather_object(handles, tuple(_ipc_export(t) for t in (self.keys, self.vals, self.samples)),
                                    group=group)
             self.peers = []
             for g, hs in enumerate(handles):
                 if g == self.rank:
-                    self.peers.append((self.keys, self.vals, self.samples))
-                else:
-                    self.peers.append(tuple(f(*a) for f, a in hs))
+                    self.peers.append(tuple(t.data_ptr() for t in (self.keys, self.vals, self.samples)))
+                    continue
+                ptrs = []
+                for handle, off, _ in hs:
+                    base = ctypes.c_void_p()
+                    _lib.check(lib.ps_ipc_open(dev.index, handle, ctypes.byref(base)))
+                    self._mapped.append(base.value)
+                    ptrs.append(base.value + off)
+                self.peers.append(tuple(ptrs))
+
+    def close(self):
+        """Unmap the peers' buffers (after a closing barrier of every rank)."""
+        lib = _lib.load()
+        while self._mapped:
+            _lib.check(lib.ps_ipc_close(self.device.index, self._mapped.pop()))
 
     def sort(self):
         """Sort the global array whose shard this rank holds in ``keys``;
@@ -155,8 +194,10 @@ class DistributedSorter:
         torch.cuda.synchronize(self.keys.device)
         self.dist.barrier(group=self.group)
         t0, t1 = self.plan["slab"]
-        shard_merge([p[0] for p in self.peers], [p[1] for p in self.peers], t0, t1, self.out_keys, self.out_vals,
-                    samples=[p[2] if p[0].numel() else None for p in self.peers], workspace=self.ws)
+        sizes = self.plan["sizes"]
+        _shard_merge_ptrs(self.keys.dtype, [p[0] for p in self.peers], [p[1] for p in self.peers],
+                          [p[2] if sizes[g] else None for g, p in enumerate(self.peers)], sizes, t0, t1,
+                          self.device, self.out_keys, self.out_vals, self.ws)
         torch.cuda.synchronize(self.keys.device)
         self.dist.barrier(group=self.group)  # peers keep their shards alive until every slab is merged
         return self.out_keys, self.out_vals
@@ -169,4 +210,6 @@ def sort_distributed(keys, config=None, group=None):
     sorter = DistributedSorter(keys.numel(), keys.dtype, config, group, keys.device)
     sorter.keys.copy_(keys)
     k, v = sorter.sort()
+    k, v = k.clone(), v.clone()
+    sorter.close()
     return k, v
