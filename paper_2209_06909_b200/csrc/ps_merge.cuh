@@ -1100,7 +1100,7 @@ constexpr uint32_t MAXSEG = 32;
 template <class K>
 struct PipeLayout {
     static constexpr uint32_t CAP = pipe_cap<K>();
-    static constexpr uint32_t PADN = CAP + pipe_vt<K>() + 16;  // record capacity (+ over-read / don't-care slack)
+    static constexpr uint32_t PADN = (CAP + pipe_vt<K>() + 16 + 3) & ~3u;  // record capacity (+ over-read / don't-care slack)
     static_assert(PADN >= CAP + pipe_vt<K>() - 1, "record slack must hold a thread's don't-care outputs");
     static constexpr uint32_t RECB = (uint32_t)sizeof(Rec<K>);
     // slot = TMA landing zone of the key windows + value windows of all segments
@@ -1234,6 +1234,96 @@ PS_DEV uint32_t diag_search(const C& c) {
     return lo;
 }
 
+// PS_LOADS_FIRST=1: the merge step of a WinCur issues its two shared-memory
+// loads (the value of the record it emits and the key behind it, one address
+// register: the new head is the next element of the run just consumed) before
+// its two stores.  The stores may alias the loads as far as the compiler knows,
+// so source order is issue order: with the value load, its store and only then
+// the key load (the order until round 2) every step waits for two dependent
+// shared-memory round trips instead of one.
+#ifndef PS_LOADS_FIRST
+#define PS_LOADS_FIRST 1
+#endif
+
+// One merge chain over two SoA windows, heads in registers, pointer cursors.
+// 4-byte keys: a value sits at a fixed byte offset dv from its key in both
+// windows (TMA slot: KEY_BYTES, windows share their 16-byte phases; scratch:
+// XV), so one selected pointer serves both loads.
+template <class K>
+struct MChain {
+    const K *pa, *pb, *ea, *eb;
+    const int32_t *va, *vb;  // 8-byte keys: value cursors
+    K a, b;
+    PS_DEV void init(const WinCur<K>& c, uint32_t i, uint32_t j) {
+        pa = c.ak + i;
+        pb = c.bk + j;
+        ea = c.ak + c.la;
+        eb = c.bk + c.lb;
+        va = c.av + i;
+        vb = c.bv + j;
+        a = *pa;
+        b = *pb;
+    }
+    // emits one record: returns its key, loads its value into v
+    PS_DEV K step(ptrdiff_t dv, int32_t& v) {
+        const bool tA = pa < ea && (pb >= eb || !(b < a));
+        const K k = tA ? a : b;
+        const K* p = tA ? pa : pb;
+        const K nk = p[1];
+        if constexpr (sizeof(K) == 4) {
+            v = *reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(p) + dv);
+        } else {
+            v = *(tA ? va : vb);
+            va += tA;
+            vb += !tA;
+        }
+        pa = tA ? p + 1 : pa;
+        pb = tA ? pb : p + 1;
+        a = tA ? nk : a;
+        b = tA ? b : nk;
+        return k;
+    }
+};
+
+// The VT outputs [o, o + VT) of a WinCur merge, written by put(t, key, value)
+// with t relative to o (a thread with fewer outputs writes don't-care records,
+// see single_merge).
+template <class K, class Put>
+PS_DEV void win_merge(const WinCur<K>& c, Put put) {
+    const ptrdiff_t dv = reinterpret_cast<const uint8_t*>(c.av) - reinterpret_cast<const uint8_t*>(c.ak);
+    const uint32_t i0 = diag_search(c);
+    MChain<K> A;
+    A.init(c, i0, c.o - i0);
+#pragma unroll
+    for (uint32_t t = 0; t < pipe_vt<K>(); ++t) {
+        int32_t v;
+        const K k = A.step(dv, v);
+        put(t, k, v);
+    }
+}
+
+template <class K>
+PS_DEV void single_merge(WinCur<K>& c, Rec<K>* out) {
+    if (c.o >= c.oe) return;
+    if (PS_LOADS_FIRST) {
+        Rec<K>* outp = out + c.base + c.o;
+        win_merge<K>(c, [&](uint32_t t, K k, int32_t v) {
+            Rec<K> r;
+            r.k = k;
+            r.v = v;
+            outp[t] = r;
+        });
+        return;
+    }
+    const uint32_t lo = diag_search(c);
+    c.i = lo;
+    c.j = c.o - lo;
+    c.heads();
+    Rec<K>* outp = out + c.base + c.o;
+#pragma unroll
+    for (uint32_t t = 0; t < pipe_vt<K>(); ++t) c.step(outp, t);
+}
+
 template <class C, class K>
 PS_DEV void single_merge(C& c, Rec<K>* out) {
     if (c.o >= c.oe) return;
@@ -1274,6 +1364,15 @@ PS_DEV void single_merge_soa(RecCur<K>& c, K* outk, int32_t* outv) {
 template <class K>
 PS_DEV void single_merge_soa(WinCur<K>& c, K* outk, int32_t* outv) {
     if (c.o >= c.oe) return;
+    if (PS_LOADS_FIRST) {
+        K* ok2 = outk + c.base + c.o;
+        int32_t* ov2 = outv + c.base + c.o;
+        win_merge<K>(c, [&](uint32_t t, K k, int32_t v) {
+            ok2[t] = k;
+            ov2[t] = v;
+        });
+        return;
+    }
     const uint32_t lo = diag_search(c);
     c.i = lo;
     c.j = c.o - lo;
