@@ -607,6 +607,9 @@ struct MergeRunner {
         psmem = merge_pipe_smem_bytes<K>();
         ssmem = merge_small_smem_bytes<K>();
         PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        // 4-byte keys: two CTAs per SM need the largest shared-memory carve-out
+        PS_CUDA(cudaFuncSetAttribute(merge_pipe_kernel<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
         PS_CUDA(cudaFuncSetAttribute(merge_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
         PS_CUDA(cudaFuncSetAttribute(merge_mid_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)mid_smem_bytes<K>()));

@@ -30,11 +30,16 @@
 
 namespace ps {
 
-// consumer threads per merge_pipe_kernel CTA, per key width (measured: 4-byte
-// keys 576 consumers x VT 15, 0.8% faster than 512 x 17 on cfg2; 8-byte keys
-// 352 x 13, 2.8% faster than 512 x 9 on cfg3)
+// consumer threads per merge_pipe_kernel CTA, per key width.  4-byte keys: 288
+// consumers x VT 15 (units of 4320 records, ~111 KB of shared memory), so two
+// CTAs share an SM and each fills the other's barrier and load waits: the merge
+// kernels of cfg5 run 7% faster than with one CTA of 576 x 15 per SM (the
+// geometry until round 2; 0.8% faster than 512 x 17 on cfg2), at twice the
+// cuts (cfg5 partition 4.3 -> 7.3 ms; cfg5 -2.8%, cfg4 -4%, cfg2 +1.6% per sort).
+// 8-byte keys: one CTA of 352 x 13 per SM (2.8% faster than 512 x 9 on cfg3; two
+// CTAs of 160 x 13 are 1% slower).
 #ifndef PS_CONSUMERS4
-#define PS_CONSUMERS4 576
+#define PS_CONSUMERS4 288
 #endif
 #ifndef PS_CONSUMERS8
 #define PS_CONSUMERS8 352
@@ -62,6 +67,18 @@ PS_DEV __host__ constexpr uint32_t pipe_threads() {
 template <class K>
 PS_DEV __host__ constexpr uint32_t pipe_vt() {
     return sizeof(K) == 4 ? PS_VT4 : PS_VT8;
+}
+// segments per unit (bounds the slot's window-alignment slack: two CTAs of
+// 4-byte keys must fit an SM)
+#ifndef PS_MAXSEG4
+#define PS_MAXSEG4 8
+#endif
+#ifndef PS_MAXSEG8
+#define PS_MAXSEG8 32
+#endif
+template <class K>
+PS_DEV __host__ constexpr uint32_t pipe_maxseg() {
+    return sizeof(K) == 4 ? PS_MAXSEG4 : PS_MAXSEG8;
 }
 // records per unit (smem slot capacity)
 template <class K>
@@ -1075,7 +1092,7 @@ struct alignas(sizeof(K) == 4 ? 8 : 16) Rec {
 };
 
 
-// Units hold up to MAXSEG segments; a segment is a contiguous chunk range of
+// Units hold up to pipe_maxseg<K>() <= MAXSEG segments; a segment is a contiguous chunk range of
 // one node (a unit of one segment may be several chunks of one node; several
 // segments pack consecutive whole small-to-mid nodes or chunk ranges).
 constexpr uint32_t MAXSEG = 32;
@@ -1106,8 +1123,8 @@ struct PipeLayout {
     // slot = TMA landing zone of the key windows + value windows of all segments
     // (SoA, <= 31 bytes of 16-byte alignment slack per window), and afterwards
     // the records of the last pass
-    static constexpr uint32_t KEY_BYTES = align16c(CAP * (uint32_t)sizeof(K)) + MAXSEG * MAX_WAY * 32u;
-    static constexpr uint32_t VAL_BYTES = align16c(CAP * 4u) + MAXSEG * MAX_WAY * 32u;
+    static constexpr uint32_t KEY_BYTES = align16c(CAP * (uint32_t)sizeof(K)) + pipe_maxseg<K>() * MAX_WAY * 32u;
+    static constexpr uint32_t VAL_BYTES = align16c(CAP * 4u) + pipe_maxseg<K>() * MAX_WAY * 32u;
     static constexpr uint32_t SLOT = align16c(cmax(KEY_BYTES + VAL_BYTES, PADN * RECB));
     // scratch: first-pass records X || Y of every segment (or the 2-way output)
     static constexpr uint32_t SCRATCH = align16c(PADN * RECB);
@@ -1546,7 +1563,7 @@ __global__ void __launch_bounds__(pipe_threads<K>()) merge_pipe_kernel(Bufs<K> b
                 const uint32_t sumC = PC - XCu + (sgsu ? 0u : 2 * VT);
                 const uint32_t nsg = PS - XSu + (sgsu ? 0u : 1u);
                 const bool ok = lane >= u && lane < nvalid &&
-                                (same ? sumT <= ucapu : (sumC <= LY::CAP && nsg <= MAXSEG));
+                                (same ? sumT <= ucapu : (sumC <= LY::CAP && nsg <= pipe_maxseg<K>()));
                 const uint32_t bal = __ballot_sync(PS_FULL, ok) >> u;
                 const uint32_t runlen = __ffs(~bal) ? __ffs(~bal) - 1 : 32 - u;
                 const uint32_t V = u + max(runlen, 1u) - 1;
