@@ -188,7 +188,7 @@ inline cudaError_t launch_coop(bool pdl, void (*kernel)(KArgs...), dim3 grid, di
 }
 
 // Barrier over all CTAs of a grid whose CTAs are co-resident (persistent
-// grids of <= one CTA per SM).  ctr is zeroed before the launch; the k-th
+// grids of <= occupancy x SMs CTAs, launched cooperatively).  ctr is zeroed before the launch; the k-th
 // barrier of a launch waits for target = k * gridDim.x arrivals.  A bounded
 // spin turns a missing CTA into ERR_BARRIER instead of a hang.
 PS_DEV void grid_barrier(uint32_t* ctr, uint32_t target, uint32_t* err) {
