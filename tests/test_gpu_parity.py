@@ -273,6 +273,46 @@ def test_edge_sizes(dev):
             assert stats.merge_cost == ref.stats["merge_cost"]
 
 
+def test_unit_capacity_edges(dev):
+    # nodes whose size or run lengths sit at the pipe kernel's unit capacities
+    # (4-byte keys: 288 x 15 = 4320 records per unit, cuts every (4320 - 15) / arity;
+    # 8-byte keys: 352 x 13 = 4576) and their multiples: one chunk exactly full,
+    # one record more, runs one record around the cut spacing, and nodes that
+    # fill a whole grid of units
+    rng = np.random.default_rng(4320)
+
+    def runs_of(lengths, dtype):
+        parts = []
+        for ln in lengths:
+            v = np.sort(rng.integers(-(1 << 30), 1 << 30, ln)).astype(dtype)
+            if ln:  # a descent between runs: every run ends high and starts low
+                v[-1] = (1 << 30) + 7
+                v[0] = -(1 << 30) - 7
+            parts.append(v)
+        return np.concatenate(parts)
+
+    cases = []
+    for cap, vt in ((4320, 15), (4576, 13)):
+        cc = cap - vt
+        for w in (2, 3, 4):
+            s = cc // w
+            for total in (cc - 1, cc, cc + 1, cap, cap + 1, 2 * cc, 2 * cc + 1):
+                base = total // w
+                cases.append([base] * (w - 1) + [total - base * (w - 1)])
+            cases.append([s - 1, s, s + 1, 2 * s][:w])
+            cases.append([2 * s, 2 * s + 1, 25, 4 * s][:w])
+    cases.append([4320 * 74] * 4)      # 296 full units of one 4-way node
+    cases.append([4305 * 74 + 1] * 4)
+    for dtype in (np.int32, np.int64):
+        for lengths in cases:
+            keys = runs_of(lengths, dtype)
+            ref = oracle.sort(keys)
+            out, perm, stats = gpu_sort(keys, dev)
+            assert np.array_equal(perm, ref.values), (dtype, lengths)
+            assert stats.run_lengths == ref.run_lengths, (dtype, lengths)
+            assert stats.merge_cost == ref.stats["merge_cost"], (dtype, lengths)
+
+
 def test_float_signed_zero_and_ties(dev):
     rng = np.random.default_rng(9)
     keys = rng.choice(np.array([-0.0, 0.0, 1.0, -1.0, 2.5], dtype=np.float32), size=50000)
